@@ -1,0 +1,244 @@
+/*
+ * if_b200.h — C ABI of the B200-native block-quantized GEMV/GEMM library for
+ * Inferflow's hot path (arxiv 2401.08294).
+ *
+ * Citations: "P:n" = line n of PAPER.md (the Inferflow report); "S:n" = line n
+ * of SPEC.md; "Qn" = reading n in DESIGN.md §Readings.
+ *
+ * Conventions for every entry point
+ *  - Pointers named W, x, y, X, Y, packed, h_*, workspace are DEVICE pointers
+ *    (cudaMalloc / torch CUDA tensors) unless stated otherwise.  The library owns
+ *    no tensor memory and never allocates on the hot path; the only internal
+ *    state is inside an if_comm.
+ *  - Calls are stream-ordered and asynchronous on `stream` (a cudaStream_t;
+ *    NULL = legacy default stream).  No entry point synchronises except
+ *    if_comm_* set-up calls.  All compute entry points are CUDA-graph capturable.
+ *  - Host-detectable errors (argument, shape, scheme, plan, grid) return
+ *    immediately and launch nothing.  Data-dependent errors are written to an
+ *    optional device int32 `dev_status` (0 = OK; the first error wins), which
+ *    the caller reads after synchronising.  Launch failures return IF_ERR_CUDA.
+ *    if_last_error() returns a thread-local message for the last non-OK status.
+ *  - Packed tensors: W is [N, K] row-major with quantization blocks running
+ *    along K (the reduction dimension; Q9).  Block (n, b) covers
+ *    W[n, b*block .. (b+1)*block) and is stored at byte offset
+ *    (n*(K/block) + b) * if_block_bytes(s) as
+ *        [lo fp16 LE][hi fp16 LE][codes, tightly bit-packed LSB-first]
+ *    (two FP16 numbers per block P:191; Q2/Q11/Q12).  K % block == 0.
+ */
+#ifndef IF_B200_H
+#define IF_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st* if_stream_t; /* identical to cudaStream_t */
+
+typedef enum {
+  IF_OK = 0,
+  IF_ERR_ARG = 1,     /* null pointer, bad enum, bad batch, misaligned pointer       */
+  IF_ERR_SHAPE = 2,   /* K % block != 0, negative or inconsistent sizes              */
+  IF_ERR_SCHEME = 3,  /* qtype/block outside Table 3's family      */
+  IF_ERR_INPUT = 4,   /* (device) non-finite weight or |w| beyond fp16 range (Q8)    */
+  IF_ERR_DECODE = 5,  /* (device) Q3H pair code > 120 (Q14)              */
+  IF_ERR_PLAN = 6,    /* indivisible heads/kv-heads/FFN, layers < stages     */
+  IF_ERR_GRID = 7,    /* devices != stages x groups                          */
+  IF_ERR_CUDA = 8,    /* CUDA launch / runtime failure                               */
+  IF_ERR_COMM = 9,    /* peer-memory communicator failure                            */
+  IF_ERR_UNSUPPORTED = 10
+} if_status;
+
+/* Schemes ("2, 3, 4, 5, 6, and 8" bits plus 3.5-bit Q3H). */
+typedef enum { IF_Q2 = 2, IF_Q3 = 3, IF_Q3H = 35, IF_Q4 = 4, IF_Q5 = 5, IF_Q6 = 6, IF_Q8 = 8 } if_qtype;
+
+/* block in {32, 64} for every type (Table 3 defaults). */
+typedef struct {
+  int32_t type;  /* if_qtype */
+  int32_t block; /* weights per block */
+} if_scheme;
+
+/* ---------------------------------------------------------------------------
+ * Sizes (host only, no device work)
+ * ------------------------------------------------------------------------- */
+
+/* Bytes of one block: 4 (two fp16) + ceil(block*bits/8).
+ * Returns -1 for an invalid scheme. */
+int64_t if_block_bytes(if_scheme s);
+
+/* N*(K/block)*if_block_bytes(s); -1 if the scheme is invalid, N<0, K<0 or K%block. */
+int64_t if_packed_bytes(if_scheme s, int64_t N, int64_t K);
+
+/* Actual bits per weight as a reduced fraction num/den = (block*bits + 32)/block
+ * (Table 3).  IF_ERR_SCHEME for an invalid scheme. */
+if_status if_bits_per_weight(if_scheme s, int64_t* num, int64_t* den);
+
+/* ---------------------------------------------------------------------------
+ * Synthetic inputs: out[i] = float(s(idx)) * scale with
+ * idx = offset + i and the counter-based Irwin-Hall(4) generator of synth/.
+ * Device out[n], fp32.  Not part of the method; used to fill HBM with weights
+ * and activations without a host round trip.
+ * ------------------------------------------------------------------------- */
+if_status if_synth_fill(uint64_t seed, uint64_t tensor_id, float scale, float* out, int64_t n,
+                        int64_t offset, if_stream_t stream);
+
+/* ---------------------------------------------------------------------------
+ * a1 + a2: quantize (Eq. 1; 3.5-bit P:120-127; pair code P:124-127)
+ * W       device fp32 [N, K] row-major, read only.
+ * packed  device uint8 [if_packed_bytes(s, N, K)], written.
+ * Per block: min/max (−0 -> +0), lo = fp16 round-down(min), hi = fp16
+ * round-up(max) (Q3), q = roundf(((w - lo) / (hi - lo)) * D) in binary32 (Q1,
+ * Q4), D = 2^k-1 or 10; Q3H codes v = q_{2i}*11 + q_{2i+1}.  Bit-exact with
+ * the oracle.  Non-finite inputs or min/max beyond fp16 -> dev_status = 4 (the
+ * block is still written with undefined content).
+ * ------------------------------------------------------------------------- */
+if_status if_quantize(if_scheme s, const float* W, int64_t N, int64_t K, uint8_t* packed,
+                      int32_t* dev_status /* nullable */, if_stream_t stream);
+
+/* ---------------------------------------------------------------------------
+ * a3: dequantize (Eq. 2; Q3H decode P:129-136)
+ * packed  device uint8 [if_packed_bytes], W_out device fp32 [N, K].
+ * w' = fma32(q, (hi - lo)/D, lo) (Q5).  Q3H codes > 120 -> dev_status = 5.
+ * ------------------------------------------------------------------------- */
+if_status if_dequantize(if_scheme s, const uint8_t* packed, int64_t N, int64_t K, float* W_out,
+                        int32_t* dev_status /* nullable */, if_stream_t stream);
+
+/* ---------------------------------------------------------------------------
+ * a4: decode GEMV with fused dequantization
+ *   y[b, n] = sum_k W'[n, k] * x[b, k]       (fp32 accumulation)
+ * W  device packed [N, K]; x device fp32 [B, K]; y device fp32 [B, N].
+ * 1 <= B <= 64.  x and y 16-byte aligned, W 16-byte aligned (cudaMalloc /
+ * torch allocations are).  Codes are not validated (invalid Q3H codes give
+ * unspecified values, memory-safe).  Result within 1e-3 normwise of the fp64
+ * definition (BASELINE.json north_star); deterministic (same bits every call).
+ * ------------------------------------------------------------------------- */
+if_status if_qgemv(if_scheme s, const uint8_t* W, int64_t N, int64_t K, const float* x, int64_t B,
+                   float* y, if_stream_t stream);
+
+/* Same, y[b, n] += sum_k W'[n,k] x[b,k]  (residual add fused; y read then written). */
+if_status if_qgemv_acc(if_scheme s, const uint8_t* W, int64_t N, int64_t K, const float* x,
+                       int64_t B, float* y, if_stream_t stream);
+
+/* ---------------------------------------------------------------------------
+ * a5: prefill GEMM with fused dequantization on tcgen05 tensor cores
+ *   Y[m, n] = sum_k W'[n, k] * X[m, k]       (bf16 x bf16 -> fp32 accumulate)
+ * W device packed [N, K]; X device bf16 [M, K] (raw uint16 bit patterns);
+ * Y device fp32 [M, N].  W' is rounded to bf16 inside the kernel (the
+ * dequantized tile is staged in shared memory as bf16).  Within 2e-2 normwise
+ * of the fp64 definition evaluated on the same bf16 X (north_star).
+ * ------------------------------------------------------------------------- */
+if_status if_qgemm(if_scheme s, const uint8_t* W, int64_t N, int64_t K, const uint16_t* X_bf16,
+                   int64_t M, float* Y, if_stream_t stream);
+
+/* ---------------------------------------------------------------------------
+ * a7/a8: partition planner (Table 4; Q20)
+ * ------------------------------------------------------------------------- */
+typedef enum { IF_BY_LAYER = 0, IF_BY_TENSOR = 1, IF_HYBRID = 2 } if_strategy;
+
+/* Llama-shaped stack (Q18): d = hidden, H heads, G kv heads,
+ * head_dim, F = ffn.  Requirements: d, H*head_dim, F multiples of 64;
+ * H % G == 0. */
+typedef struct {
+  int32_t layers, hidden, heads, kv_heads, head_dim, ffn;
+  if_scheme scheme;
+} if_stack_shape;
+
+/* One device's share.  0-based half-open ranges (reports print them 1-based
+ * inclusive).  FFN ranges are in units of 64 weights (Q20). */
+typedef struct {
+  int32_t rank, stage, group_rank;
+  int32_t layer_begin, layer_end;
+  int32_t head_begin, head_end;
+  int32_t kv_begin, kv_end;
+  int32_t ffn_blk_begin, ffn_blk_end;
+} if_assignment;
+
+typedef struct {
+  int32_t strategy; /* if_strategy */
+  int32_t devices, stages, groups;
+  if_assignment a[8];
+} if_plan;
+
+/* Balanced contiguous ranges, remainder to earlier stages/ranks.
+ * by_layer: stages = devices, groups = 1; by_tensor: stages = 1,
+ * groups = devices; hybrid: stages x groups = devices (IF_ERR_GRID otherwise),
+ * devices of one stage are adjacent ranks (Table 4).  heads, kv_heads
+ * divisible by groups, F/64 >= groups, layers >= stages (IF_ERR_PLAN).
+ * 1 <= devices <= 8. */
+if_status if_plan_partition(int32_t strategy, const if_stack_shape* shape, int32_t devices,
+                            int32_t stages, int32_t groups, if_plan* out);
+
+/* ---------------------------------------------------------------------------
+ * Peer-memory communicator for the TP merges (a7, "merged twice") and
+ * the pipeline hand-off (a8).  One process per GPU.  Set-up:
+ *   if_comm_create(plan, rank, max_tokens, &c)   allocates this rank's
+ *       symmetric mailbox (device memory owned by the communicator);
+ *   if_comm_ipc_handle(c, out64)                 64-byte CUDA IPC handle of it;
+ *   (caller all-gathers the handles, e.g. torch.distributed.all_gather_object)
+ *   if_comm_open_peers(c, handles)              handles: host, devices x 64 bytes
+ *   if_comm_destroy(c).
+ * Set-up calls synchronise the device.  devices == 1 needs no peers.
+ * ------------------------------------------------------------------------- */
+typedef struct if_comm_s* if_comm;
+if_status if_comm_create(const if_plan* plan, int32_t rank, int64_t max_tokens, int32_t hidden,
+                         if_comm* out);
+if_status if_comm_ipc_handle(if_comm c, uint8_t* handle64 /* host, 64 bytes */);
+if_status if_comm_open_peers(if_comm c, const uint8_t* handles /* host, devices*64 bytes */);
+if_status if_comm_destroy(if_comm c);
+
+/* In-place all-reduce(sum) of buf[n] fp32 over this rank's TP group, through
+ * peer memory; every rank of the group ends with bit-identical sums (fixed
+ * rank order).  Stream-ordered, graph capturable. */
+if_status if_comm_allreduce(if_comm c, float* buf, int64_t n, if_stream_t stream);
+/* Pipeline hand-off: send buf[n] to the same group rank of stage+1 / receive
+ * from stage-1 into buf. */
+if_status if_comm_send_next(if_comm c, const float* buf, int64_t n, if_stream_t stream);
+if_status if_comm_recv_prev(if_comm c, float* buf, int64_t n, if_stream_t stream);
+
+/* ---------------------------------------------------------------------------
+ * The Llama-shaped linear stack on this rank (Q18), decode or prefill.
+ * Per layer of this rank's stage (rank-local shards, see if_plan):
+ *   a = rms(h); [q|k|v] = a W_qkv^T; ctx_i = v_{floor(i/(H/G))};
+ *   h += all_reduce(ctx W_o^T); a = rms(h); [g|u] = a W_gu^T;
+ *   h += all_reduce((silu(g)*u) W_down^T)
+ * stage_layers[i] holds the packed shards of layer layer_begin+i:
+ *   wqkv  [(lh + 2 lkv) head_dim, d] : q rows of my heads, then k, then v rows
+ *   wo    [d, lh head_dim]           : K-columns of my heads
+ *   wgu   [2 lf, d]                  : gate rows of my FFN range, then up rows
+ *   wdown [d, lf]                    : K-columns of my FFN range
+ * h_in  device fp32 [T, d] (ignored on stages > 0, which receive from stage-1),
+ * h_out device fp32 [T, d] (valid on the last stage), last_qkv device fp32
+ * [T, (lh + 2 lkv) head_dim] of the stage's last layer (nullable).
+ * mode IF_DECODE (1 <= T <= 64, qGEMV, fp32 activations) or IF_PREFILL
+ * (T <= 4096, qGEMM on tcgen05 with bf16 activations).
+ * workspace: device, if_stack_workspace_bytes().  comm may be NULL when
+ * plan->devices == 1.  Never synchronises; graph capturable.
+ * ------------------------------------------------------------------------- */
+enum { IF_DECODE = 0, IF_PREFILL = 1 };
+typedef struct {
+  const uint8_t* wqkv;
+  const uint8_t* wo;
+  const uint8_t* wgu;
+  const uint8_t* wdown;
+} if_layer_weights;
+
+if_status if_stack_workspace_bytes(const if_stack_shape* shape, const if_plan* plan, int32_t rank,
+                                   int64_t max_tokens, int32_t mode, size_t* bytes);
+if_status if_run_stack(const if_stack_shape* shape, const if_plan* plan, int32_t rank, if_comm comm,
+                       const if_layer_weights* stage_layers, const float* h_in, int64_t T,
+                       int32_t mode, float* h_out, float* last_qkv, void* workspace,
+                       if_stream_t stream);
+
+/* Thread-local message for the last non-OK status returned on this thread. */
+const char* if_last_error(void);
+
+/* Number of kernels this library launched on this host thread since the last
+ * reset (instrumentation for bench.py's gpu_launches). */
+int64_t if_launch_count(int32_t reset);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* IF_B200_H */

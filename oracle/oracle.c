@@ -29,6 +29,8 @@
 #include <stdlib.h>
 #include <string.h>
 
+#define REF_MAX_BLOCK 4096 /* longest block accepted (tensor blocks are 32/64; test mode any) */
+
 /* ------------------------------------------------------------------------ */
 /* scheme                                                                   */
 /* ------------------------------------------------------------------------ */
@@ -163,19 +165,21 @@ int ref_unpack_pair(int v, int* q_first, int* q_second) {
 /* ------------------------------------------------------------------------ */
 
 static void put_bits(uint8_t* area, int64_t bitpos, int width, uint32_t value) {
-  for (int b = 0; b < width; b++) {
-    int64_t p = bitpos + b;
-    if ((value >> b) & 1u) area[p / 8] |= (uint8_t)(1u << (p % 8));
-  }
+  /* width <= 8: the field lies in byte bitpos/8 and possibly the next one */
+  int64_t byte = bitpos / 8;
+  int off = (int)(bitpos % 8);
+  uint32_t window = (value & ((1u << width) - 1u)) << off;
+  area[byte] |= (uint8_t)(window & 0xFFu);
+  if (off + width > 8) area[byte + 1] |= (uint8_t)(window >> 8);
 }
 
 static uint32_t get_bits(const uint8_t* area, int64_t bitpos, int width) {
-  uint32_t v = 0;
-  for (int b = 0; b < width; b++) {
-    int64_t p = bitpos + b;
-    if ((area[p / 8] >> (p % 8)) & 1u) v |= (1u << b);
-  }
-  return v;
+  /* width <= 8: the field lies in byte bitpos/8 and possibly the next one */
+  int64_t byte = bitpos / 8;
+  int off = (int)(bitpos % 8);
+  uint32_t window = area[byte];
+  if (off + width > 8) window |= (uint32_t)area[byte + 1] << 8;
+  return (window >> off) & ((1u << width) - 1u);
 }
 
 /* ------------------------------------------------------------------------ */
@@ -190,7 +194,7 @@ int ref_quantize_block(int qtype, int n, const float* w, uint8_t* out) {
   if (!(qtype == 2 || qtype == 3 || qtype == 4 || qtype == 5 || qtype == 6 || qtype == 8 ||
         qtype == 35))
     return 3;
-  if (n < 1 || (qtype == 35 && (n % 2) != 0)) return 3;
+  if (n < 1 || n > REF_MAX_BLOCK || (qtype == 35 && (n % 2) != 0)) return 3;
   const int D = ref_levels(qtype);
   /* step 1: finite inputs only */
   for (int i = 0; i < n; i++)
@@ -211,7 +215,7 @@ int ref_quantize_block(int qtype, int n, const float* w, uint8_t* out) {
   const float hi = ref_f16_to_f32(hi16);
   const float r = hi - lo;
   /* step 4: q_i = Round((w_i - min)/(max - min) * D) */
-  int32_t* q = (int32_t*)malloc(sizeof(int32_t) * (size_t)n);
+  int32_t q[REF_MAX_BLOCK];
   for (int i = 0; i < n; i++) {
     if (r == 0.0f) {
       q[i] = 0; /* Q6: degenerate block */
@@ -239,7 +243,6 @@ int ref_quantize_block(int qtype, int n, const float* w, uint8_t* out) {
   } else {
     for (int i = 0; i < n; i++) put_bits(area, (int64_t)i * qtype, qtype, (uint32_t)q[i]);
   }
-  free(q);
   return 0;
 }
 
@@ -265,19 +268,16 @@ int ref_dequantize_block(int qtype, int n, const uint8_t* in, float* w_out) {
   if (!(qtype == 2 || qtype == 3 || qtype == 4 || qtype == 5 || qtype == 6 || qtype == 8 ||
         qtype == 35))
     return 3;
-  int32_t* q = (int32_t*)malloc(sizeof(int32_t) * (size_t)n);
+  if (n < 1 || n > REF_MAX_BLOCK) return 3;
+  int32_t q[REF_MAX_BLOCK];
   int st = ref_block_codes(qtype, n, in, q);
-  if (st) {
-    free(q);
-    return st;
-  }
+  if (st) return st;
   uint16_t lo16 = (uint16_t)(in[0] | (in[1] << 8));
   uint16_t hi16 = (uint16_t)(in[2] | (in[3] << 8));
   const float lo = ref_f16_to_f32(lo16);
   const float hi = ref_f16_to_f32(hi16);
   const float step = (hi - lo) / (float)ref_levels(qtype);
   for (int i = 0; i < n; i++) w_out[i] = fmaf((float)q[i], step, lo);
-  free(q);
   return 0;
 }
 

@@ -1,0 +1,180 @@
+"""B200-native block-quantized GEMV/GEMM for Inferflow's hot path (arxiv 2401.08294).
+
+Thin Python binding over the C ABI of include/if_b200.h (libif_b200.so): the
+functions here carry the C names and only marshal arguments (torch CUDA
+tensors -> device pointers, current CUDA stream).  Every step of the path runs
+in the library's sm_100a kernels; there is no CPU or PyTorch fallback and a
+missing library raises at import of the first call.
+"""
+from __future__ import annotations
+
+import ctypes
+
+from . import _lib
+from ._lib import Assignment, LayerWeights, Plan, Scheme, StackShape
+
+QTYPES = {"Q2": 2, "Q3": 3, "Q3H": 35, "Q4": 4, "Q5": 5, "Q6": 6, "Q8": 8}
+IF_BY_LAYER, IF_BY_TENSOR, IF_HYBRID = 0, 1, 2
+IF_DECODE, IF_PREFILL = 0, 1
+STATUS = {0: "OK", 1: "ARG", 2: "SHAPE", 3: "SCHEME", 4: "INPUT", 5: "DECODE", 6: "PLAN", 7: "GRID",
+          8: "CUDA", 9: "COMM", 10: "UNSUPPORTED"}
+
+
+class IFError(RuntimeError):
+    def __init__(self, status: int, fn: str):
+        msg = _lib.load().if_last_error().decode(errors="replace")
+        super().__init__(f"{fn}: IF_ERR_{STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+def _check(st: int, fn: str):
+    if st != 0:
+        raise IFError(st, fn)
+
+
+def lib():
+    return _lib.load()
+
+
+def scheme(qtype, block: int = 64) -> Scheme:
+    if isinstance(qtype, str):
+        qtype = QTYPES[qtype]
+    return Scheme(int(qtype), int(block))
+
+
+def _ptr(t) -> int:
+    if t is None:
+        return None
+    return t.data_ptr()
+
+
+def _stream(stream):
+    if stream is None:
+        import torch
+        return torch.cuda.current_stream().cuda_stream
+    if hasattr(stream, "cuda_stream"):
+        return stream.cuda_stream
+    return int(stream)
+
+
+# ---- sizes ------------------------------------------------------------------
+def if_block_bytes(s: Scheme) -> int:
+    return lib().if_block_bytes(s)
+
+
+def if_packed_bytes(s: Scheme, N: int, K: int) -> int:
+    return lib().if_packed_bytes(s, N, K)
+
+
+def if_bits_per_weight(s: Scheme):
+    num, den = ctypes.c_int64(), ctypes.c_int64()
+    _check(lib().if_bits_per_weight(s, ctypes.byref(num), ctypes.byref(den)), "if_bits_per_weight")
+    return num.value, den.value
+
+
+# ---- kernels ------------------------------------------------------------------
+def if_synth_fill(seed: int, tensor_id: int, scale: float, out, offset: int = 0, stream=None):
+    _check(lib().if_synth_fill(seed, tensor_id, float(scale), _ptr(out), out.numel(), offset, _stream(stream)),
+           "if_synth_fill")
+
+
+def if_quantize(s: Scheme, W, N: int, K: int, packed, dev_status=None, stream=None):
+    _check(lib().if_quantize(s, _ptr(W), N, K, _ptr(packed), _ptr(dev_status), _stream(stream)), "if_quantize")
+
+
+def if_dequantize(s: Scheme, packed, N: int, K: int, W_out, dev_status=None, stream=None):
+    _check(lib().if_dequantize(s, _ptr(packed), N, K, _ptr(W_out), _ptr(dev_status), _stream(stream)),
+           "if_dequantize")
+
+
+def if_qgemv(s: Scheme, W, N: int, K: int, x, B: int, y, stream=None):
+    _check(lib().if_qgemv(s, _ptr(W), N, K, _ptr(x), B, _ptr(y), _stream(stream)), "if_qgemv")
+
+
+def if_qgemv_acc(s: Scheme, W, N: int, K: int, x, B: int, y, stream=None):
+    _check(lib().if_qgemv_acc(s, _ptr(W), N, K, _ptr(x), B, _ptr(y), _stream(stream)), "if_qgemv_acc")
+
+
+def if_qgemm(s: Scheme, W, N: int, K: int, X_bf16, M: int, Y, stream=None):
+    _check(lib().if_qgemm(s, _ptr(W), N, K, _ptr(X_bf16), M, _ptr(Y), _stream(stream)), "if_qgemm")
+
+
+# ---- partition ----------------------------------------------------------------
+def stack_shape(layers, hidden, heads, kv_heads, head_dim, ffn, s: Scheme) -> StackShape:
+    return StackShape(layers, hidden, heads, kv_heads, head_dim, ffn, s)
+
+
+def if_plan_partition(strategy: int, shape: StackShape, devices: int, stages: int = 0, groups: int = 0) -> Plan:
+    p = Plan()
+    _check(lib().if_plan_partition(strategy, ctypes.byref(shape), devices, stages, groups, ctypes.byref(p)),
+           "if_plan_partition")
+    return p
+
+
+# ---- communicator -------------------------------------------------------------
+class Comm:
+    """Peer-memory communicator (if_comm_*).  Handles are exchanged through
+    torch.distributed.all_gather_object (plumbing only)."""
+
+    def __init__(self, plan: Plan, rank: int, max_tokens: int, hidden: int):
+        self.h = ctypes.c_void_p()
+        _check(lib().if_comm_create(ctypes.byref(plan), rank, max_tokens, hidden, ctypes.byref(self.h)),
+               "if_comm_create")
+        self.plan = plan
+
+    def ipc_handle(self) -> bytes:
+        buf = (ctypes.c_uint8 * 64)()
+        _check(lib().if_comm_ipc_handle(self.h, buf), "if_comm_ipc_handle")
+        return bytes(buf)
+
+    def open_peers(self, handles: list[bytes]):
+        blob = b"".join(handles)
+        buf = (ctypes.c_uint8 * len(blob)).from_buffer_copy(blob)
+        _check(lib().if_comm_open_peers(self.h, buf), "if_comm_open_peers")
+
+    def exchange(self, group=None):
+        import torch.distributed as dist
+        hs = [None] * dist.get_world_size(group)
+        dist.all_gather_object(hs, self.ipc_handle(), group=group)
+        self.open_peers(hs)
+
+    def allreduce(self, buf, stream=None):
+        _check(lib().if_comm_allreduce(self.h, _ptr(buf), buf.numel(), _stream(stream)), "if_comm_allreduce")
+
+    def send_next(self, buf, stream=None):
+        _check(lib().if_comm_send_next(self.h, _ptr(buf), buf.numel(), _stream(stream)), "if_comm_send_next")
+
+    def recv_prev(self, buf, stream=None):
+        _check(lib().if_comm_recv_prev(self.h, _ptr(buf), buf.numel(), _stream(stream)), "if_comm_recv_prev")
+
+    def destroy(self):
+        if self.h:
+            _check(lib().if_comm_destroy(self.h), "if_comm_destroy")
+            self.h = ctypes.c_void_p()
+
+
+# ---- stack --------------------------------------------------------------------
+def if_stack_workspace_bytes(shape: StackShape, plan: Plan, rank: int, max_tokens: int, mode: int) -> int:
+    n = ctypes.c_size_t()
+    _check(lib().if_stack_workspace_bytes(ctypes.byref(shape), ctypes.byref(plan), rank, max_tokens, mode,
+                                          ctypes.byref(n)), "if_stack_workspace_bytes")
+    return n.value
+
+
+def layer_weights_array(layers) -> ctypes.Array:
+    """layers: list of (wqkv, wo, wgu, wdown) uint8 CUDA tensors."""
+    arr = (LayerWeights * max(1, len(layers)))()
+    for i, (a, b, c, d) in enumerate(layers):
+        arr[i] = LayerWeights(a.data_ptr(), b.data_ptr(), c.data_ptr(), d.data_ptr())
+    return arr
+
+
+def if_run_stack(shape: StackShape, plan: Plan, rank: int, comm, layers_arr, h_in, T: int, mode: int, h_out,
+                 last_qkv, workspace, stream=None):
+    _check(lib().if_run_stack(ctypes.byref(shape), ctypes.byref(plan), rank, comm.h if comm else None, layers_arr,
+                              _ptr(h_in), T, mode, _ptr(h_out), _ptr(last_qkv), _ptr(workspace), _stream(stream)),
+           "if_run_stack")
+
+
+def if_launch_count(reset: bool = False) -> int:
+    return lib().if_launch_count(1 if reset else 0)

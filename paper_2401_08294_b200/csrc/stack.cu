@@ -1,0 +1,248 @@
+// stack.cu — the Llama-shaped linear stack on one rank (Q18) and its
+// glue (a6): RMSNorm (eps 1e-5, unit gain), single-position GQA
+// attention (softmax over one key = the v row of head i's kv group
+// floor(i/(H/G)), contiguous groups S:393), SiLU(g)*u,
+// residual adds; plus the TP merges and pipeline hand-off (a7/a8)
+// through comm.cu.
+#include <cuda_bf16.h>
+
+#include "comm.cuh"
+#include "common.cuh"
+#include "qgemm.cuh"
+
+namespace ifb {
+
+template <typename T>
+__device__ __forceinline__ T to_out(float v);
+template <>
+__device__ __forceinline__ float to_out<float>(float v) {
+  return v;
+}
+template <>
+__device__ __forceinline__ __nv_bfloat16 to_out<__nv_bfloat16>(float v) {
+  return __float2bfloat16(v);
+}
+
+// a[t] = h[t] / sqrt(mean(h[t]^2) + 1e-5)
+template <typename OutT>
+__global__ void __launch_bounds__(256) rmsnorm_kernel(const float* __restrict__ h, OutT* __restrict__ a, int d) {
+  __shared__ float red[8];
+  const float* hr = h + (int64_t)blockIdx.x * d;
+  float ss = 0.f;
+  for (int i = threadIdx.x; i < d; i += blockDim.x) ss = fmaf(hr[i], hr[i], ss);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
+  __syncthreads();
+  float tot = 0.f;
+  for (int w = 0; w < (int)(blockDim.x >> 5); w++) tot += red[w];
+  const float inv = 1.0f / sqrtf(tot / (float)d + 1e-5f);
+  OutT* ar = a + (int64_t)blockIdx.x * d;
+  for (int i = threadIdx.x; i < d; i += blockDim.x) ar[i] = to_out<OutT>(hr[i] * inv);
+}
+
+// ctx[t, i*hd + e] = v[t, j*hd + e],  j = floor((h0 + i)/(H/G)) - k0  (local heads/kv-heads)
+template <typename OutT>
+__global__ void vbcast_kernel(const float* __restrict__ qkv, OutT* __restrict__ ctx, int T, int lh, int lkv, int hd,
+                              int h0, int k0, int per) {
+  const int64_t nq = (int64_t)lh * hd, nqkv = (int64_t)(lh + 2 * lkv) * hd;
+  const int64_t total = (int64_t)T * nq;
+  for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total; idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t t = idx / nq, r = idx - t * nq;
+    const int i = (int)(r / hd), e = (int)(r - (int64_t)i * hd);
+    const int j = (h0 + i) / per - k0;
+    ctx[idx] = to_out<OutT>(qkv[t * nqkv + (int64_t)(lh + lkv) * hd + (int64_t)j * hd + e]);
+  }
+}
+
+// act[t, f] = silu(g) * u,  [g|u] = gu[t]
+template <typename OutT>
+__global__ void silu_mul_kernel(const float* __restrict__ gu, OutT* __restrict__ act, int T, int lf) {
+  const int64_t total = (int64_t)T * lf;
+  for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total; idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t t = idx / lf, f = idx - t * lf;
+    const float g = gu[t * 2 * lf + f], u = gu[t * 2 * lf + lf + f];
+    act[idx] = to_out<OutT>(g / (1.0f + expf(-g)) * u);
+  }
+}
+
+static int ew_grid(int64_t n) {
+  int64_t g = (n + 255) / 256;
+  if (g > 148 * 8) g = 148 * 8;
+  if (g < 1) g = 1;
+  return (int)g;
+}
+
+struct Local {
+  int lh, lkv, lf, nq, nqkv, d, hd;
+};
+
+static if_status local_dims(const if_stack_shape* s, const if_plan* p, int rank, Local* L) {
+  if (!s || !p) return set_error(IF_ERR_ARG, "stack: null shape/plan");
+  if (!scheme_ok(s->scheme)) return set_error(IF_ERR_SCHEME, "stack: invalid scheme");
+  if (rank < 0 || rank >= p->devices || p->devices > 8) return set_error(IF_ERR_ARG, "stack: rank %d", rank);
+  if (s->hidden % 64 || (s->heads * s->head_dim) % 64 || s->ffn % 64 || s->kv_heads < 1 || s->heads % s->kv_heads)
+    return set_error(IF_ERR_SHAPE, "stack: bad shape");
+  const if_assignment& a = p->a[rank];
+  if (a.head_begin < 0 || a.head_end > s->heads || a.kv_end > s->kv_heads || a.ffn_blk_end > s->ffn / 64 ||
+      a.layer_end > s->layers || a.layer_begin < 0 || a.head_end <= a.head_begin || a.kv_end <= a.kv_begin ||
+      a.ffn_blk_end <= a.ffn_blk_begin)
+    return set_error(IF_ERR_PLAN, "stack: assignment of rank %d inconsistent with shape", rank);
+  L->lh = a.head_end - a.head_begin;
+  L->lkv = a.kv_end - a.kv_begin;
+  L->lf = (a.ffn_blk_end - a.ffn_blk_begin) * 64;
+  L->hd = s->head_dim;
+  L->d = s->hidden;
+  L->nq = L->lh * s->head_dim;
+  L->nqkv = (L->lh + 2 * L->lkv) * s->head_dim;
+  return IF_OK;
+}
+
+static size_t al256(size_t x) { return (x + 255) & ~size_t(255); }
+
+struct WS {
+  float* a;
+  float* qkv;
+  float* ctx;
+  float* gu;
+  float* act;
+  float* part;
+  size_t bytes;
+};
+
+static WS carve(void* base, const Local& L, int64_t T) {
+  WS w;
+  char* p = static_cast<char*>(base);
+  size_t off = 0;
+  auto take = [&](size_t elems) {
+    float* r = reinterpret_cast<float*>(p ? p + off : nullptr);
+    off += al256(elems * 4);
+    return r;
+  };
+  w.a = take((size_t)T * L.d);
+  w.qkv = take((size_t)T * L.nqkv);
+  w.ctx = take((size_t)T * L.nq);
+  w.gu = take((size_t)T * 2 * L.lf);
+  w.act = take((size_t)T * L.lf);
+  w.part = take((size_t)T * L.d);
+  w.bytes = off;
+  return w;
+}
+
+}  // namespace ifb
+
+using namespace ifb;
+
+extern "C" if_status if_stack_workspace_bytes(const if_stack_shape* shape, const if_plan* plan, int32_t rank,
+                                              int64_t max_tokens, int32_t mode, size_t* bytes) {
+  Local L;
+  if_status st = local_dims(shape, plan, rank, &L);
+  if (st) return st;
+  if (!bytes) return set_error(IF_ERR_ARG, "if_stack_workspace_bytes: null");
+  if (max_tokens < 1 || (mode == IF_DECODE && max_tokens > 64) || max_tokens > 4096)
+    return set_error(IF_ERR_ARG, "if_stack_workspace_bytes: max_tokens=%lld", (long long)max_tokens);
+  *bytes = carve(nullptr, L, max_tokens).bytes;
+  return IF_OK;
+}
+
+extern "C" if_status if_run_stack(const if_stack_shape* shape, const if_plan* plan, int32_t rank, if_comm comm,
+                                  const if_layer_weights* stage_layers, const float* h_in, int64_t T, int32_t mode,
+                                  float* h_out, float* last_qkv, void* workspace, if_stream_t stream) {
+  Local L;
+  if_status st = local_dims(shape, plan, rank, &L);
+  if (st) return st;
+  if (mode != IF_DECODE && mode != IF_PREFILL) return set_error(IF_ERR_ARG, "if_run_stack: mode %d", mode);
+  if (T < 1 || (mode == IF_DECODE && T > 64) || T > 4096) return set_error(IF_ERR_ARG, "if_run_stack: T=%lld", (long long)T);
+  if (!h_out || !workspace || !stage_layers) return set_error(IF_ERR_ARG, "if_run_stack: null pointer");
+  const if_assignment& asg = plan->a[rank];
+  const bool first = asg.stage == 0, last = asg.stage == plan->stages - 1;
+  if (first && !h_in) return set_error(IF_ERR_ARG, "if_run_stack: null h_in on stage 0");
+  if ((plan->devices > 1) && !comm) return set_error(IF_ERR_ARG, "if_run_stack: comm required for %d devices", plan->devices);
+  const int groups = plan->groups;
+  cudaStream_t cs = (cudaStream_t)stream;
+  const if_scheme sc = shape->scheme;
+  WS w = carve(workspace, L, T);
+  const int64_t nh = T * (int64_t)L.d;
+  const int per = shape->heads / shape->kv_heads;
+
+  // stage input: h_in on stage 0, hand-off from stage-1 otherwise
+  if (first) {
+    if (h_out != h_in && cudaMemcpyAsync(h_out, h_in, nh * 4, cudaMemcpyDeviceToDevice, cs) != cudaSuccess)
+      return check_launch("if_run_stack: copy h_in");
+  } else {
+    if ((st = comm_recv(comm, h_out, nh, cs))) return st;
+  }
+  const int nlayers = asg.layer_end - asg.layer_begin;
+  for (int l = 0; l < nlayers; l++) {
+    const if_layer_weights& Wl = stage_layers[l];
+    if (!Wl.wqkv || !Wl.wo || !Wl.wgu || !Wl.wdown) return set_error(IF_ERR_ARG, "if_run_stack: null weights, layer %d", l);
+    if (mode == IF_DECODE) {
+      // ---- attention sub-layer ----
+      rmsnorm_kernel<float><<<(unsigned)T, 256, 0, cs>>>(h_out, w.a, L.d);
+      count_launch();
+      if ((st = if_qgemv(sc, Wl.wqkv, L.nqkv, L.d, w.a, T, w.qkv, stream))) return st;
+      vbcast_kernel<float><<<ew_grid(T * L.nq), 256, 0, cs>>>(w.qkv, w.ctx, (int)T, L.lh, L.lkv, L.hd, asg.head_begin,
+                                                             asg.kv_begin, per);
+      count_launch();
+      if (groups == 1) {
+        if ((st = if_qgemv_acc(sc, Wl.wo, L.d, L.nq, w.ctx, T, h_out, stream))) return st;
+      } else {
+        if ((st = if_qgemv(sc, Wl.wo, L.d, L.nq, w.ctx, T, w.part, stream))) return st;
+        if ((st = comm_allreduce_into(comm, w.part, h_out, nh, 1, cs))) return st;  // merge #1
+      }
+      // ---- feed-forward sub-layer ----
+      rmsnorm_kernel<float><<<(unsigned)T, 256, 0, cs>>>(h_out, w.a, L.d);
+      count_launch();
+      if ((st = if_qgemv(sc, Wl.wgu, 2 * L.lf, L.d, w.a, T, w.gu, stream))) return st;
+      silu_mul_kernel<float><<<ew_grid(T * L.lf), 256, 0, cs>>>(w.gu, w.act, (int)T, L.lf);
+      count_launch();
+      if (groups == 1) {
+        if ((st = if_qgemv_acc(sc, Wl.wdown, L.d, L.lf, w.act, T, h_out, stream))) return st;
+      } else {
+        if ((st = if_qgemv(sc, Wl.wdown, L.d, L.lf, w.act, T, w.part, stream))) return st;
+        if ((st = comm_allreduce_into(comm, w.part, h_out, nh, 1, cs))) return st;  // merge #2
+      }
+    } else {
+      __nv_bfloat16* a16 = reinterpret_cast<__nv_bfloat16*>(w.a);
+      __nv_bfloat16* c16 = reinterpret_cast<__nv_bfloat16*>(w.ctx);
+      __nv_bfloat16* f16 = reinterpret_cast<__nv_bfloat16*>(w.act);
+      rmsnorm_kernel<__nv_bfloat16><<<(unsigned)T, 256, 0, cs>>>(h_out, a16, L.d);
+      count_launch();
+      if ((st = qgemm_impl("if_run_stack(qkv)", sc, Wl.wqkv, L.nqkv, L.d, reinterpret_cast<uint16_t*>(a16), T, w.qkv, 0, cs)))
+        return st;
+      vbcast_kernel<__nv_bfloat16><<<ew_grid(T * L.nq), 256, 0, cs>>>(w.qkv, c16, (int)T, L.lh, L.lkv, L.hd,
+                                                                     asg.head_begin, asg.kv_begin, per);
+      count_launch();
+      if (groups == 1) {
+        if ((st = qgemm_impl("if_run_stack(o)", sc, Wl.wo, L.d, L.nq, reinterpret_cast<uint16_t*>(c16), T, h_out, 1, cs)))
+          return st;
+      } else {
+        if ((st = qgemm_impl("if_run_stack(o)", sc, Wl.wo, L.d, L.nq, reinterpret_cast<uint16_t*>(c16), T, w.part, 0, cs)))
+          return st;
+        if ((st = comm_allreduce_into(comm, w.part, h_out, nh, 1, cs))) return st;
+      }
+      rmsnorm_kernel<__nv_bfloat16><<<(unsigned)T, 256, 0, cs>>>(h_out, a16, L.d);
+      count_launch();
+      if ((st = qgemm_impl("if_run_stack(gu)", sc, Wl.wgu, 2 * L.lf, L.d, reinterpret_cast<uint16_t*>(a16), T, w.gu, 0, cs)))
+        return st;
+      silu_mul_kernel<__nv_bfloat16><<<ew_grid(T * L.lf), 256, 0, cs>>>(w.gu, f16, (int)T, L.lf);
+      count_launch();
+      if (groups == 1) {
+        if ((st = qgemm_impl("if_run_stack(down)", sc, Wl.wdown, L.d, L.lf, reinterpret_cast<uint16_t*>(f16), T, h_out, 1, cs)))
+          return st;
+      } else {
+        if ((st = qgemm_impl("if_run_stack(down)", sc, Wl.wdown, L.d, L.lf, reinterpret_cast<uint16_t*>(f16), T, w.part, 0, cs)))
+          return st;
+        if ((st = comm_allreduce_into(comm, w.part, h_out, nh, 1, cs))) return st;
+      }
+    }
+    if (l == nlayers - 1 && last_qkv) {
+      if (cudaMemcpyAsync(last_qkv, w.qkv, (size_t)T * L.nqkv * 4, cudaMemcpyDeviceToDevice, cs) != cudaSuccess)
+        return check_launch("if_run_stack: last_qkv");
+    }
+  }
+  if (!last) {
+    if ((st = comm_send(comm, h_out, nh, cs))) return st;
+  }
+  return check_launch("if_run_stack");
+}
