@@ -206,7 +206,8 @@ if_status if_comm_recv_prev(if_comm c, float* buf, int64_t n, if_stream_t stream
  * stage_layers[i] holds the packed shards of layer layer_begin+i:
  *   wqkv  [(lh + 2 lkv) head_dim, d] : q rows of my heads, then k, then v rows
  *   wo    [d, lh head_dim]           : K-columns of my heads
- *   wgu   [2 lf, d]                  : gate rows of my FFN range, then up rows
+ *   wgu   [2 lf, d]                  : gate and up rows of my FFN range INTERLEAVED:
+ *                                      row 2f = gate row f, row 2f+1 = up row f
  *   wdown [d, lf]                    : K-columns of my FFN range
  * h_in  device fp32 [T, d] (ignored on stages > 0, which receive from stage-1),
  * h_out device fp32 [T, d] (valid on the last stage), last_qkv device fp32

@@ -10,7 +10,7 @@ import re
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
-LIB_PATH = os.path.join(HERE, "libif_b200.so")
+LIB_PATH = os.environ.get("IFB_LIB_PATH", os.path.join(HERE, "libif_b200.so"))  # override: experiments only
 HEADER = os.path.join(ROOT, "include", "if_b200.h")
 
 i32, i64, u64, f32, vp = ctypes.c_int32, ctypes.c_int64, ctypes.c_uint64, ctypes.c_float, ctypes.c_void_p

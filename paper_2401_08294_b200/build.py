@@ -18,8 +18,9 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 ROOT = os.path.dirname(HERE)
-OUT = os.path.join(HERE, "libif_b200.so")
-BUILD = os.path.join(HERE, "_build")
+OUT = os.environ.get("IFB_LIB_OUT", os.path.join(HERE, "libif_b200.so"))  # experiments: variant libraries
+BUILD = os.environ.get("IFB_BUILD_DIR", os.path.join(HERE, "_build"))
+EXTRA = os.environ.get("IFB_NVCC_FLAGS", "").split()
 
 NVCC = shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc"
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -42,7 +43,7 @@ def _newest(paths):
 def _compile(src: str, force: bool) -> str:
     obj = os.path.join(BUILD, os.path.basename(src)[:-3] + ".o")
     if force or not os.path.exists(obj) or os.path.getmtime(obj) < max(os.path.getmtime(src), _newest(_headers())):
-        cmd = [NVCC, *FLAGS, "-c", src, "-o", obj + ".tmp"]
+        cmd = [NVCC, *FLAGS, *EXTRA, "-c", src, "-o", obj + ".tmp"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"nvcc failed for {src}:\n{r.stdout}\n{r.stderr}")

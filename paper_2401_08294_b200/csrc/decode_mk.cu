@@ -1,0 +1,626 @@
+// decode_mk.cu — persistent batch-1 decode engine for Q3H_B64 (the hot path).
+//
+// One CTA per SM, launched once per decode step.  The whole stack (or one
+// standalone GEMV) is a sequence of phases; a phase is one fused-dequant GEMV
+// (a4) whose input is produced by the previous phase, with the stack glue (a6)
+// fused into the input staging and the output epilogue:
+//
+//   phase 4l+0  qkv  = W_qkv  rms(h)                   (x staged: h * 1/rms)
+//   phase 4l+1  h   += W_o    vbcast(v)                (x staged: v of kv group)
+//   phase 4l+2  gu   = W_gu   rms(h)
+//   phase 4l+3  h   += W_down silu(g)*u
+//
+// Warp roles (B200-first):
+//  * producer warp — one lane streams this CTA's row range of every phase, in
+//    order, into a shared-memory ring with cp.async.bulk (the TMA engine),
+//    completion tracked by mbarriers (full/empty per slot).  Weights never
+//    depend on activations, so the producer runs ahead across phase and layer
+//    boundaries and keeps HBM busy while consumers wait on a dependency.
+//  * 8 consumer warps — wait until every CTA finished the previous phase (a
+//    grid-wide counter, acquire/release at gpu scope), stage the transformed x
+//    for the new phase in shared memory (identity (*) of simd.cuh), then decode
+//    3.5-bit pair codes from the ring (2 SASS ops/weight) against x, R rows per
+//    x load; partial sums are reduced with shuffles, combined across 32-block
+//    chunks in a fixed order (deterministic), and written / residual-added.
+// Rows of each phase are split evenly over the CTAs (contiguous ranges), so a
+// CTA's share of a phase is one contiguous byte range of the packed tensor.
+#include <stdlib.h>
+
+#include <algorithm>
+
+#include "common.cuh"
+#include "decode_mk.cuh"
+#include "pipe.cuh"
+#include "simd.cuh"
+
+namespace ifb {
+
+#ifndef IFB_MK_NC
+#define IFB_MK_NC 15
+#endif
+#ifndef IFB_MK_RMAX
+#define IFB_MK_RMAX 4
+#endif
+constexpr int MK_NC = IFB_MK_NC;            // consumer warps
+constexpr int MK_RMAX = IFB_MK_RMAX;        // rows per unit (x reuse)
+constexpr int MK_THREADS = (MK_NC + 1) * 32;  // + producer warp
+constexpr int MK_SLOT = 32 * 1024;          // ring slot bytes
+constexpr int MK_MAXSLOT = 8;
+constexpr int MK_CT = MK_NC * 32;           // consumer threads
+
+struct Geo {
+  int N, K, nb, nchunk, nbp, row_bytes, r0, r1, rps, R;
+};
+
+__device__ __forceinline__ Geo phase_geo(int N, int K, int G, int cta, int pairs) {
+  Geo g;
+  g.N = N;
+  g.K = K;
+  g.nb = K >> 6;
+  g.nchunk = (g.nb + 31) >> 5;
+  g.nbp = g.nchunk << 5;
+  g.row_bytes = g.nb * 32;
+  // contiguous balanced row ranges; the gate/up phase splits (gate, up) row pairs
+  const int units = pairs ? N / 2 : N;
+  const int base = units / G, rem = units % G;
+  g.r0 = cta * base + min(cta, rem);
+  g.r1 = g.r0 + base + (cta < rem ? 1 : 0);
+  if (pairs) {
+    g.r0 *= 2;
+    g.r1 *= 2;
+  }
+  int rps = MK_SLOT / g.row_bytes;
+  if (MK_RMAX >= 8 && rps >= 8) {
+    g.R = 8;
+    rps &= ~7;
+  } else if (rps >= 4) {
+    g.R = 4;
+    rps &= ~3;
+  } else if (rps >= 2) {
+    g.R = 2;
+    rps = 2;
+  } else {
+    g.R = 2;  // rows > 16 KB: one row per slot, the unit's second row is masked
+    rps = 1;
+  }
+  g.rps = rps;
+  return g;
+}
+
+__device__ __forceinline__ void phase_dims(const MkParams& P, int p, const uint8_t** W, int* N, int* K, int* kind) {
+  if (P.mode == MK_MODE_GEMV) {
+    *W = P.w[0][0];
+    *N = P.gemv_N;
+    *K = P.gemv_K;
+    *kind = 4;
+    return;
+  }
+  const int l = p >> 2, k = p & 3;
+  *kind = k;
+  *W = P.w[l][k];
+  if (k == 0) {
+    *N = P.nqkv;
+    *K = P.d;
+  } else if (k == 1) {
+    *N = P.d;
+    *K = P.nq;
+  } else if (k == 2) {
+    *N = 2 * P.lf;
+    *K = P.d;
+  } else {
+    *N = P.d;
+    *K = P.lf;
+  }
+}
+
+// ---- consumer: R rows x one 32-block chunk ------------------------------------
+// Sum over the 32 lanes of v[0..R) with a transposed butterfly; returns the sum
+// of row (lane >> 3) on lanes 0, 8, 16, 24 (R = 4), row (lane >> 4) on lanes 0,
+// 16 (R = 2), row 0 on lane 0 (R = 1).
+template <int R>
+__device__ __forceinline__ float warp_rows_sum(float (&v)[R]) {
+  const int lane = threadIdx.x & 31;
+  if constexpr (R == 8) {
+    // 8 rows -> lanes 0,4,..,28 hold rows 0..7 (row = lane >> 2)
+    const bool h16 = lane & 16;
+    float a[4];
+#pragma unroll
+    for (int i = 0; i < 4; i++) {
+      const float keep = h16 ? v[4 + i] : v[i], give = h16 ? v[i] : v[4 + i];
+      a[i] = keep + __shfl_xor_sync(0xffffffffu, give, 16);
+    }
+    const bool h8 = lane & 8;
+    float b0 = h8 ? a[2] : a[0], b1 = h8 ? a[3] : a[1];
+    const float g0 = h8 ? a[0] : a[2], g1 = h8 ? a[1] : a[3];
+    b0 += __shfl_xor_sync(0xffffffffu, g0, 8);
+    b1 += __shfl_xor_sync(0xffffffffu, g1, 8);
+    const bool h4 = lane & 4;
+    float e = h4 ? b1 : b0;
+    const float f = h4 ? b0 : b1;
+    e += __shfl_xor_sync(0xffffffffu, f, 4);
+    e += __shfl_xor_sync(0xffffffffu, e, 2);
+    e += __shfl_xor_sync(0xffffffffu, e, 1);
+    return e;
+  } else if constexpr (R == 4) {
+    const bool hi16 = lane & 16;
+    float a = hi16 ? v[2] : v[0], b = hi16 ? v[3] : v[1];
+    const float c = hi16 ? v[0] : v[2], d = hi16 ? v[1] : v[3];
+    a += __shfl_xor_sync(0xffffffffu, c, 16);
+    b += __shfl_xor_sync(0xffffffffu, d, 16);
+    const bool hi8 = lane & 8;
+    float e = hi8 ? b : a;
+    const float f = hi8 ? a : b;
+    e += __shfl_xor_sync(0xffffffffu, f, 8);
+    e += __shfl_xor_sync(0xffffffffu, e, 4);
+    e += __shfl_xor_sync(0xffffffffu, e, 2);
+    e += __shfl_xor_sync(0xffffffffu, e, 1);
+    return e;
+  } else if constexpr (R == 2) {
+    const bool hi16 = lane & 16;
+    float a = hi16 ? v[1] : v[0];
+    const float c = hi16 ? v[0] : v[1];
+    a += __shfl_xor_sync(0xffffffffu, c, 16);
+#pragma unroll
+    for (int o = 8; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+    return a;
+  } else {
+    float a = v[0];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+    return a;
+  }
+}
+
+// One unit: R rows (R even) x one 32-block chunk, subnormal-form decode
+// (simd.cuh).  XS = row stride of xs in float4 (compile time when XS > 0).
+// FULL = every lane active and all R rows valid.
+template <int R, int XS, bool FULL>
+__device__ __forceinline__ void mk_unit(const unsigned char* slot_rows, int row_bytes, int nrows_valid, int c, int nb,
+                                        int xs_rt, const float4* xs, const float2* bs, float* part_rows, int nchunk,
+                                        const Q3HConst& kc) {
+  static_assert(R % 2 == 0, "rows are paired in FFMA2 lanes");
+  (void)kc;
+  const int lane = threadIdx.x & 31;
+  const int b = c * 32 + lane;
+  const bool active = FULL || b < nb;
+  const int xstride = XS > 0 ? XS : xs_rt;
+  uint32_t wv[R][8];
+#pragma unroll
+  for (int i = 0; i < R; i++) {
+    if (FULL || (active && i < nrows_valid)) {
+      const uint4* a = reinterpret_cast<const uint4*>(slot_rows + i * row_bytes + b * 32);
+      const uint4 lo = a[0], hi = a[1];
+      wv[i][0] = lo.x; wv[i][1] = lo.y; wv[i][2] = lo.z; wv[i][3] = lo.w;
+      wv[i][4] = hi.x; wv[i][5] = hi.y; wv[i][6] = hi.z; wv[i][7] = hi.w;
+    } else {
+#pragma unroll
+      for (int k = 0; k < 8; k++) wv[i][k] = 0u;
+    }
+  }
+  uint32_t vw[R][7];
+#pragma unroll
+  for (int i = 0; i < R; i++) {
+    vw[i][0] = q3h_sview<0>(wv[i]); vw[i][1] = q3h_sview<1>(wv[i]); vw[i][2] = q3h_sview<2>(wv[i]);
+    vw[i][3] = q3h_sview<3>(wv[i]); vw[i][4] = q3h_sview<4>(wv[i]); vw[i][5] = q3h_sview<5>(wv[i]);
+    vw[i][6] = q3h_sview<6>(wv[i]);
+  }
+  u64 accc[R / 2], accq[R / 2];
+#pragma unroll
+  for (int i = 0; i < R / 2; i++) accc[i] = accq[i] = 0ull;
+  const float4* xa = xs + b;
+  float4 xn = xa[0];
+#define IFB_MK_CODE(J, XC, XQ)                                                                  \
+  {                                                                                             \
+    constexpr uint32_t fm = q3h_floor_mult_bits(kQ3hSrc[J].pos);                                \
+    const u64 fm2 = pack2(__uint_as_float(fm), __uint_as_float(fm));                            \
+    const u64 xc2 = pack2(XC, XC), xq2 = pack2(XQ, XQ);                                         \
+    _Pragma("unroll") for (int ip = 0; ip < R / 2; ip++) {                                      \
+      const u64 cf = pack2(__uint_as_float(q3h_scode_bits<J>(wv[2 * ip], vw[2 * ip])),          \
+                           __uint_as_float(q3h_scode_bits<J>(wv[2 * ip + 1], vw[2 * ip + 1]))); \
+      const u64 qe = ffma2_rm(cf, fm2, 0ull);                                                   \
+      accc[ip] = ffma2(cf, xc2, accc[ip]);                                                      \
+      accq[ip] = ffma2(qe, xq2, accq[ip]);                                                      \
+    }                                                                                           \
+  }
+#define IFB_MK_QUAD(JJ)                                                                         \
+  {                                                                                             \
+    const float4 xv = xn;                                                                       \
+    if ((JJ) < 15) xn = xa[((JJ) + 1) * xstride]; /* prefetch the next x quad */                \
+    IFB_MK_CODE(2 * (JJ), xv.x, xv.z)                                                           \
+    IFB_MK_CODE(2 * (JJ) + 1, xv.y, xv.w)                                                       \
+  }
+  IFB_MK_QUAD(0) IFB_MK_QUAD(1) IFB_MK_QUAD(2) IFB_MK_QUAD(3) IFB_MK_QUAD(4) IFB_MK_QUAD(5)
+  IFB_MK_QUAD(6) IFB_MK_QUAD(7) IFB_MK_QUAD(8) IFB_MK_QUAD(9) IFB_MK_QUAD(10) IFB_MK_QUAD(11)
+  IFB_MK_QUAD(12) IFB_MK_QUAD(13) IFB_MK_QUAD(14) IFB_MK_QUAD(15)
+#undef IFB_MK_QUAD
+#undef IFB_MK_CODE
+  const float sx = bs[b].x;
+  float v[R];
+#pragma unroll
+  for (int ip = 0; ip < R / 2; ip++) {
+    const float2 a = unpack2(accc[ip]), q = unpack2(accq[ip]);
+#pragma unroll
+    for (int h = 0; h < 2; h++) {
+      const int i = 2 * ip + h;
+      const float lo = half_bits_to_float(wv[i][0] & 0xFFFFu);
+      const float hi = half_bits_to_float(wv[i][0] >> 16);
+      // Eq. 2 with D = 10; 2^64 undoes the accumulator scale
+      const float step = (hi - lo) * (0.1f * 18446744073709551616.0f);
+      const float sq = h ? (a.y + q.y) : (a.x + q.x);
+      const float r = fmaf(step, sq, lo * sx);
+      v[i] = active ? r : 0.f;
+    }
+  }
+  const float sum = warp_rows_sum<R>(v);
+  constexpr int SH = R == 8 ? 2 : (R == 4 ? 3 : (R == 2 ? 4 : 5));
+  const int row = lane >> SH;
+  if ((lane & ((1 << SH) - 1)) == 0 && (FULL || row < nrows_valid)) part_rows[row * nchunk + c] = sum;
+}
+
+template <int R, int XS>
+__device__ __forceinline__ void mk_unit_dispatch(const unsigned char* slot_rows, int row_bytes, int nrows_valid, int c,
+                                                 int nb, int xs_rt, const float4* xs, const float2* bs,
+                                                 float* part_rows, int nchunk, const Q3HConst& kc) {
+  if (nrows_valid >= R && (c + 1) * 32 <= nb)
+    mk_unit<R, XS, true>(slot_rows, row_bytes, nrows_valid, c, nb, xs_rt, xs, bs, part_rows, nchunk, kc);
+  else
+    mk_unit<R, XS, false>(slot_rows, row_bytes, nrows_valid, c, nb, xs_rt, xs, bs, part_rows, nchunk, kc);
+}
+
+// Stage the transformed x of one phase: for the float4 quad q (weights 4q..4q+3,
+// i.e. pairs 2q, 2q+1 of block b = q / 16, JJ = q % 16) write
+//   xs[JJ * xstride + b] = {512 x_o(2JJ), 512 x_o(2JJ+1), xe'(2JJ), xe'(2JJ+1)}
+// (identity (*) of simd.cuh) and bs[b] = {sum x, sum x_odd}.  src4(q) returns the
+// 4 raw inputs of quad q (already scaled).  Consecutive threads read
+// consecutive quads; xstride = nbp + 1 makes the transposed stores
+// conflict-free; a block's 16 quads sit in one half-warp for the block sums.
+// code bit position s_j of pair j (simd.cuh kQ3hSrc), for the per-pair x scaling
+__constant__ int kQ3hPosC[32] = {0, 7, 14, 0, 7, 3, 10, 17, 0, 7, 6, 13, 0, 7, 2, 9,
+                                 16, 0, 7, 5, 12, 0, 7, 1, 8, 15, 0, 7, 4, 11, 0, 7};
+
+// Stage the transformed x of one phase: for the float4 quad q (weights
+// 4q..4q+3 = pairs 2JJ, 2JJ+1 of block b = q / 16, JJ = q % 16) write
+//   xs[JJ * xstride + b] = {X_c(2JJ), X_c(2JJ+1), X_q(2JJ), X_q(2JJ+1)}
+//   X_c(j) = x_o(j) * 2^(85 - s_j),   X_q(j) = (x_e(j) - 11 x_o(j)) * 2^85
+// (subnormal-form decode, simd.cuh) and bs[b].x = sum of the block's x.
+// Consecutive threads read consecutive quads; xstride = 1 (mod 8) makes the
+// transposed stores conflict-free; a block's 16 quads sit in one half-warp.
+template <typename Src4>
+__device__ __forceinline__ void stage_x(int K, int nbp, int xstride, float4* xs, float2* bs, Src4 src4) {
+  const int ct = threadIdx.x - 32;  // consumer thread id
+  const int nq = K >> 2, nqp = nbp * 16;
+  const float s85 = 38685626227668133590597632.0f;  // 2^85
+  for (int q = ct; q < nqp; q += MK_CT) {
+    const int b = q >> 4, jj = q & 15;
+    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (q < nq) v = src4(q);
+    // pairs (v.x, v.y) and (v.z, v.w): x_e = .x/.z, x_o = .y/.w
+    const float c0 = __uint_as_float((uint32_t)(127 + 85 - kQ3hPosC[2 * jj]) << 23);
+    const float c1 = __uint_as_float((uint32_t)(127 + 85 - kQ3hPosC[2 * jj + 1]) << 23);
+    xs[jj * xstride + b] = make_float4(v.y * c0, v.w * c1, fmaf(-11.0f, v.y, v.x) * s85, fmaf(-11.0f, v.w, v.z) * s85);
+    float sx = (v.x + v.y) + (v.z + v.w);
+#pragma unroll
+    for (int o = 8; o > 0; o >>= 1) sx += __shfl_xor_sync(0xffffffffu, sx, o);
+    if (jj == 0) bs[b] = make_float2(sx, 0.f);
+  }
+}
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+template <int XS>
+__global__ void __launch_bounds__(MK_THREADS, 1) decode_mk_kernel(const __grid_constant__ MkParams P) {
+  const int xstride = XS > 0 ? XS : P.xstride;
+  extern __shared__ __align__(1024) unsigned char smem[];
+  const int G = gridDim.x, cta = blockIdx.x;
+  const int nslot = P.nslot;
+  unsigned char* ring = smem;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)nslot * MK_SLOT);
+  uint64_t* empty = full + MK_MAXSLOT;
+  float* red = reinterpret_cast<float*>(empty + MK_MAXSLOT);  // [MK_NC + 1]
+  uint64_t* xbar = reinterpret_cast<uint64_t*>(red + 30);
+  float4* xs = reinterpret_cast<float4*>(smem + (size_t)nslot * MK_SLOT + 2 * MK_MAXSLOT * 8 + 128);
+  float2* bs = reinterpret_cast<float2*>(xs + 16 * xstride);
+  float* raw = reinterpret_cast<float*>(bs + P.nbp_max);  // raw phase input (TMA bulk copy)
+  float* part = raw + P.raw_max;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < nslot; s++) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], MK_NC);  // every consumer warp arrives once per fill
+    }
+    mbar_init(xbar, 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  const int nphase = P.mode == MK_MODE_GEMV ? 1 : 4 * P.layers;
+
+  if (warp == 0) {
+    // ============================ producer ============================
+#ifdef IFB_MK_NOWAIT
+    if (false) {
+#else
+    if (lane == 0) {
+#endif
+      const uint64_t pol = policy_evict_first();
+      uint32_t slot = 0, round = 0;
+      for (int p = 0; p < nphase; p++) {
+        const uint8_t* W;
+        int N, K, kind;
+        phase_dims(P, p, &W, &N, &K, &kind);
+        const Geo g = phase_geo(N, K, G, cta, kind == 2);
+        for (int r = g.r0; r < g.r1; r += g.rps) {
+          const int n = min(g.rps, g.r1 - r);
+          const uint32_t bytes = (uint32_t)n * g.row_bytes;
+          mbar_wait(&empty[slot], (round & 1) ^ 1);
+          mbar_arrive_expect_tx(&full[slot], bytes);
+          bulk_g2s(ring + (size_t)slot * MK_SLOT, W + (size_t)r * g.row_bytes, bytes, &full[slot], pol);
+          if (++slot == (uint32_t)nslot) {
+            slot = 0;
+            round++;
+          }
+        }
+      }
+    }
+    return;
+  }
+
+  // ============================ consumers ============================
+  const int ct = threadIdx.x - 32;
+  const int cw = warp - 1;
+  const Q3HConst kc = q3h_const();
+  uint32_t slot = 0, round = 0;  // ring position (same sequence as the producer)
+  for (int p = 0; p < nphase; p++) {
+    const uint8_t* W;
+    int N, K, kind;
+    phase_dims(P, p, &W, &N, &K, &kind);
+    const Geo g = phase_geo(N, K, G, cta, kind == 2);
+    (void)W;
+    // ---- 1. dependency on the previous phase (all CTAs), then one bulk copy of
+    //         the phase's raw input (L2 -> smem on the TMA engine) ----
+    const float* src;
+    int src_n;
+    if (kind == 0 || kind == 2) {
+      src = P.h;
+      src_n = K;
+    } else if (kind == 1) {
+      src = P.qkv + (size_t)(P.lh + P.lkv) * P.hd;  // v rows of my kv heads
+      src_n = P.lkv * P.hd;
+    } else if (kind == 3) {
+      src = P.act;
+      src_n = K;
+    } else {
+      src = P.x_in;
+      src_n = K;
+    }
+    unsigned long long* dbg = P.dbg ? P.dbg + ((size_t)cta * nphase + p) * 8 : nullptr;
+    if (dbg && ct == 0) dbg[0] = gtimer();
+    if (ct == 0) {
+      if (p > 0) {
+        while (ld_acquire_gpu(&P.done[p - 1]) < G) __nanosleep(20);
+      }
+      if (dbg) dbg[1] = gtimer();
+      asm volatile("fence.proxy.async.global;" ::: "memory");  // generic writes -> async-proxy reads
+      mbar_arrive_expect_tx(xbar, (uint32_t)src_n * 4u);
+      bulk_g2s(raw, src, (uint32_t)src_n * 4u, xbar, 0ull, false);
+    }
+    mbar_wait(xbar, p & 1);
+    if (dbg && ct == 0) dbg[2] = gtimer();
+    // ---- 2. stage x for this phase (glue fused here) ----
+    const float4* raw4 = reinterpret_cast<const float4*>(raw);
+    if (kind == 0 || kind == 2) {
+      // a = h / sqrt(mean(h^2) + 1e-5)
+      float ss = 0.f;
+      for (int q = ct; q < (K >> 2); q += MK_CT) {
+        const float4 v = raw4[q];
+        ss = fmaf(v.x, v.x, ss);
+        ss = fmaf(v.y, v.y, ss);
+        ss = fmaf(v.z, v.z, ss);
+        ss = fmaf(v.w, v.w, ss);
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+      if (lane == 0) red[cw] = ss;
+      named_bar_sync(1, MK_CT);
+      float tot = 0.f;
+#pragma unroll
+      for (int w = 0; w < MK_NC; w++) tot += red[w];
+      const float inv = 1.0f / sqrtf(tot / (float)K + 1e-5f);
+      stage_x(K, g.nbp, xstride, xs, bs, [&](int q) {
+        const float4 v = raw4[q];
+        return make_float4(v.x * inv, v.y * inv, v.z * inv, v.w * inv);
+      });
+    } else if (kind == 1) {
+      // ctx head i = v row of kv group floor((h0+i)/per) - k0; hd % 4 == 0
+      const int hd4 = P.hd >> 2, h0 = P.h0, k0 = P.k0, per = P.per;
+      stage_x(K, g.nbp, xstride, xs, bs, [&](int q) {
+        const int i = q / hd4, e = q - i * hd4;
+        return raw4[((h0 + i) / per - k0) * hd4 + e];
+      });
+    } else {
+      stage_x(K, g.nbp, xstride, xs, bs, [&](int q) { return raw4[q]; });
+    }
+    named_bar_sync(1, MK_CT);
+    if (dbg && ct == 0) dbg[3] = gtimer();
+    // ---- 3. stream this CTA's rows from the ring.  Every consumer warp visits
+    //         every slot (wait full -> its units -> arrive empty, count NC);
+    //         the units (R rows x one chunk) of consecutive slots are dealt
+    //         round-robin over the warps: global unit t = sl*U + u -> warp t % NC.
+    {
+      const int nrows = g.r1 - g.r0;
+      const int nslots = (nrows + g.rps - 1) / g.rps;
+      const int gps = g.rps / g.R;                 // row groups per full slot
+      const int U = gps * g.nchunk;                // units per slot
+      const int inv_nc = (65536 + g.nchunk - 1) / g.nchunk;
+      int u0 = cw;                                 // first unit of this warp in slot sl
+      for (int sl = 0; sl < nslots; sl++) {
+#ifndef IFB_MK_NOWAIT
+        mbar_wait(&full[slot], round & 1);
+#endif
+        const int n = min(g.rps, nrows - sl * g.rps);
+        const unsigned char* sbase = ring + (size_t)slot * MK_SLOT;
+        int u = u0;
+        for (; u < U; u += MK_NC) {
+          const int grp = (u * inv_nc) >> 16, c = u - grp * g.nchunk;
+          const int i0 = grp * g.R;
+#ifdef IFB_MK_NOCOMPUTE
+          if (false) {
+#else
+          if (i0 < n) {
+#endif
+            float* pr = part + (size_t)(sl * g.rps + i0) * g.nchunk;
+            const unsigned char* ua = sbase + (size_t)i0 * g.row_bytes;
+            if (MK_RMAX >= 8 && g.R == 8)
+              mk_unit_dispatch<MK_RMAX >= 8 ? 8 : 4, XS>(ua, g.row_bytes, n - i0, c, g.nb, xstride, xs, bs, pr, g.nchunk, kc);
+            else if (g.R == 4)
+              mk_unit_dispatch<4, XS>(ua, g.row_bytes, n - i0, c, g.nb, xstride, xs, bs, pr, g.nchunk, kc);
+            else
+              mk_unit_dispatch<2, XS>(ua, g.row_bytes, n - i0, c, g.nb, xstride, xs, bs, pr, g.nchunk, kc);
+          }
+        }
+        u0 = u - U;  // continue the round-robin in the next slot
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[slot]);
+        if (++slot == (uint32_t)nslot) {
+          slot = 0;
+          round++;
+        }
+      }
+    }
+    named_bar_sync(1, MK_CT);
+    if (dbg && ct == 0) dbg[4] = gtimer();
+    // ---- 4. combine chunks (fixed order) + epilogue ----
+    const int nr = g.r1 - g.r0;
+    if (kind == 2) {
+      // interleaved gate/up rows (2f, 2f+1): act[f] = silu(g) * u
+      for (int rr = ct; rr < nr / 2; rr += MK_CT) {
+        float gg = 0.f, u = 0.f;
+        for (int c = 0; c < g.nchunk; c++) {
+          gg += part[(2 * rr) * g.nchunk + c];
+          u += part[(2 * rr + 1) * g.nchunk + c];
+        }
+        const int f = g.r0 / 2 + rr;
+        P.act[f] = gg / (1.0f + expf(-gg)) * u;
+      }
+    }
+    for (int rr = ct; rr < nr && kind != 2; rr += MK_CT) {
+      float s = 0.f;
+      for (int c = 0; c < g.nchunk; c++) s += part[rr * g.nchunk + c];
+      const int n = g.r0 + rr;
+      if (kind == 0) {
+        P.qkv[n] = s;
+        if (P.last_qkv && p == nphase - 4) P.last_qkv[n] = s;
+      } else if (kind == 1 || kind == 3) {
+        P.h[n] = __ldcg(P.h + n) + s;  // residual (the row is owned by this CTA)
+      } else {
+        P.y_out[n] = P.acc ? P.y_out[n] + s : s;
+      }
+    }
+    if (p + 1 < nphase) {
+      // bar.sync orders every consumer's output stores before thread 0's
+      // gpu-scope release (cumulativity); readers acquire the counter.
+      named_bar_sync(1, MK_CT);
+      if (ct == 0) {
+        __threadfence();
+        red_release_gpu_add(&P.done[p], 1);
+      }
+    }
+    if (dbg && ct == 0) dbg[5] = gtimer();
+  }
+}
+
+// ---------------------------------------------------------------------------
+static int mk_sms() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+static int nbp_of(int K) { return ((K / 64 + 31) / 32) * 32; }
+
+// x row stride (float4 units): >= nbp + 1 for every phase and = 1 (mod 8) so the
+// transposed staging stores are bank-conflict-free.  Common Llama widths are
+// compile-time strides (immediate LDS offsets); others use the runtime stride.
+static int mk_xstride(int nbp_max) { return ((nbp_max + 1 + 7) / 8) * 8 + 1; }
+
+static size_t mk_fixed_smem(int nbp_max, int part_max) {
+  return 2 * MK_MAXSLOT * 8 + 128 + (size_t)16 * 16 * mk_xstride(nbp_max) + (size_t)8 * nbp_max + (size_t)4 * part_max;
+}
+
+static int part_need(int N, int K, int G) {
+  const int rows = (N + G - 1) / G;
+  return rows * ((K / 64 + 31) / 32);
+}
+
+if_status mk_launch(MkParams& P, cudaStream_t st) {
+  const int G = mk_sms();
+  int nbp_max = 0, part_max = 0;
+  if (P.mode == MK_MODE_GEMV) {
+    nbp_max = nbp_of(P.gemv_K);
+    part_max = part_need(P.gemv_N, P.gemv_K, G);
+  } else {
+    const int Ns[4] = {P.nqkv, P.d, 2 * P.lf, P.d}, Ks[4] = {P.d, P.nq, P.d, P.lf};
+    if (P.nq % 64 || P.lf % 64) return IF_ERR_UNSUPPORTED;
+    for (int k = 0; k < 4; k++) {
+      nbp_max = std::max(nbp_max, nbp_of(Ks[k]));
+      part_max = std::max(part_max, part_need(Ns[k], Ks[k], G));
+    }
+  }
+  P.nbp_max = nbp_max;
+  int raw_max = P.mode == MK_MODE_GEMV ? P.gemv_K : std::max(std::max(P.d, P.lkv * P.hd), P.lf);
+  raw_max = (raw_max + 3) & ~3;
+  P.raw_max = raw_max;
+  const size_t fixed = mk_fixed_smem(nbp_max, part_max) + (size_t)4 * raw_max;
+  const size_t budget = 227 * 1024;
+  if (fixed + 2 * (size_t)MK_SLOT > budget) return IF_ERR_UNSUPPORTED;
+  int nslot = (int)((budget - fixed) / MK_SLOT);
+  nslot = std::min(nslot, MK_MAXSLOT);
+  P.nslot = nslot;
+  const size_t smem = (size_t)nslot * MK_SLOT + fixed;
+  P.xstride = mk_xstride(nbp_max);
+  void (*kern)(MkParams);
+  switch (P.xstride) {
+    case 73: kern = decode_mk_kernel<73>; break;    // K <= 4096
+    case 137: kern = decode_mk_kernel<137>; break;  // K <= 8192
+    case 201: kern = decode_mk_kernel<201>; break;  // K <= 12288 (7B: F = 11008)
+    case 233: kern = decode_mk_kernel<233>; break;  // K <= 14336 (13B: F = 13824)
+    case 457: kern = decode_mk_kernel<457>; break;  // K <= 28672 (70B: F = 28672)
+    default: kern = decode_mk_kernel<0>; break;
+  }
+  static void (*configured[8])(MkParams) = {};
+  bool done_cfg = false;
+  for (int i = 0; i < 8 && configured[i]; i++) done_cfg |= configured[i] == kern;
+  if (!done_cfg) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)budget);
+    for (int i = 0; i < 8; i++)
+      if (!configured[i]) {
+        configured[i] = kern;
+        break;
+      }
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(G);
+  cfg.blockDim = dim3(MK_THREADS);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;  // grid-wide phase dependencies need co-residency
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = (P.mode == MK_MODE_GEMV || getenv("IFB_MK_NOCOOP")) ? 0 : 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, P);
+  count_launch();
+  if (e != cudaSuccess) return set_error(IF_ERR_CUDA, "decode_mk: %s", cudaGetErrorString(e));
+  return check_launch("decode_mk");
+}
+
+}  // namespace ifb

@@ -1,0 +1,34 @@
+// decode_mk.cuh — interface of the persistent Q3H_B64 batch-1 decode engine.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/if_b200.h"
+
+namespace ifb {
+
+constexpr int MK_MAXL = 128;  // layers per stage handled by one launch
+enum { MK_MODE_STACK = 0, MK_MODE_GEMV = 1 };
+
+struct MkParams {
+  int mode;
+  int layers;
+  int d, nq, nqkv, lf, hd, lh, lkv, h0, k0, per;
+  float* h;         // [d] residual stream, updated in place
+  float* qkv;       // [nqkv]
+  float* act;       // [lf] silu(g)*u, written by the gate/up epilogue
+  float* last_qkv;  // nullable
+  int* done;        // [4*layers] grid-wide phase counters, zeroed before launch
+  // standalone GEMV (MK_MODE_GEMV): y (+)= W x
+  const float* x_in;
+  float* y_out;
+  int gemv_N, gemv_K, acc;
+  // filled by mk_launch
+  int nslot, nbp_max, raw_max, xstride;
+  unsigned long long* dbg;  // nullable: per-CTA %globaltimer stamps [G][nphase][8] (instrumentation)
+  const uint8_t* w[MK_MAXL][4];  // qkv, o, gu (gate/up rows interleaved), down per layer
+};
+
+if_status mk_launch(MkParams& P, cudaStream_t st);
+
+}  // namespace ifb

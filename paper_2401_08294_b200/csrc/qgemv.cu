@@ -17,6 +17,7 @@
 #include <algorithm>
 
 #include "common.cuh"
+#include "decode_mk.cuh"
 #include "simd.cuh"
 
 namespace ifb {
@@ -230,6 +231,7 @@ __global__ void __launch_bounds__(512) qgemv_q3h64(const uint8_t* __restrict__ W
 }
 
 static int g_num_sms = 0;
+unsigned long long* g_mk_dbg = nullptr;
 static int num_sms() {
   if (!g_num_sms) {
     int dev = 0;
@@ -305,6 +307,21 @@ static if_status qgemv_impl(const char* fn, if_scheme s, const uint8_t* W, int64
   if (s.type == IF_Q3H && s.block == 64 && (reinterpret_cast<uintptr_t>(W) & 31u) == 0 && N < (1ll << 31)) {
     bool done = false;
     if_status r;
+    if (B == 1 && K <= 65536) {
+      // persistent TMA-ring engine (decode_mk.cu), single-phase mode
+      static thread_local MkParams P;  // 4 KB of layer pointers; filled per call
+      P.mode = MK_MODE_GEMV;
+      P.layers = 1;
+      P.w[0][0] = W;
+      P.x_in = x;
+      P.y_out = y;
+      P.gemv_N = (int)N;
+      P.gemv_K = (int)K;
+      P.acc = acc;
+      P.dbg = g_mk_dbg;
+      r = mk_launch(P, st);
+      if (r != IF_ERR_UNSUPPORTED) return r;
+    }
     if (B == 1) r = launch_fast<1, 4>(W, N, K, x, B, y, acc, st, &done);
     else if (B == 2) r = launch_fast<2, 2>(W, N, K, x, B, y, acc, st, &done);
     else r = launch_fast<4, 1>(W, N, K, x, B, y, acc, st, &done);
@@ -319,6 +336,9 @@ static if_status qgemv_impl(const char* fn, if_scheme s, const uint8_t* W, int64
 }  // namespace ifb
 
 using namespace ifb;
+
+// instrumentation hook (not in the public header): per-CTA phase timestamps
+extern "C" void ifx_set_mk_debug(unsigned long long* buf) { ifb::g_mk_dbg = buf; }
 
 extern "C" if_status if_qgemv(if_scheme s, const uint8_t* W, int64_t N, int64_t K, const float* x, int64_t B,
                               float* y, if_stream_t stream) {

@@ -96,3 +96,73 @@ __device__ __forceinline__ uint32_t q3h_view(const uint32_t (&w)[8]) {
 }
 
 }  // namespace ifb
+
+namespace ifb {
+
+// ---------------------------------------------------------------------------
+// Q3H decode, subnormal form (the decode engine's hot loop).
+//
+// A 7-bit pair code c masked out of a word at bit position s, with no
+// exponent bits, IS the binary32 subnormal  cf = c * 2^(s-149)  (s <= 17 keeps
+// the field inside the 23-bit mantissa plus the exponent LSB, where the value
+// stays continuous).  Then
+//   * c * x_o        = cf * X_c,  X_c = x_o * 2^(149-s-64)         (1 FMA, exact product)
+//   * floor(c / 11)  : fma.rm(cf, A_s, 0) with A_s = roundup(1/11) * 2^-s
+//                      rounds the exact product c*roundup(1/11)*2^-149 DOWN
+//                      onto the subnormal grid: the result's bits are
+//                      floor(c/11) -- an exact, unbiased float
+//                      q_e * 2^-149 (checked for all c < 128, s <= 17)
+//   * q_e * xe'      = q_sub * X_q,  X_q = (x_e - 11 x_o) * 2^(149-64)
+// so the pair's dot-product contribution q_e x_e + q_o x_o (identity (*)) costs
+// one LOP3 (mask), one FFMA (floor) and two FFMAs (products) -- and no shift for
+// the 18 codes that already sit at s <= 17 inside a code word; the other 14
+// come from 7 funnel-shifted views (2 codes each).  Accumulators carry 2^-64.
+// FFMA2 lanes pair the same code of two rows (same s -> broadcast constants).
+// ---------------------------------------------------------------------------
+struct Q3HCodeSrc {
+  int view;  // -1: code word `word` directly; else view index
+  int word;  // code-area word (0..6) for direct codes
+  int pos;   // bit position s of the code in its source word/view
+};
+// stream bit of code j is 7j; code-area word w holds stream bits [32w, 32w+32)
+constexpr Q3HCodeSrc kQ3hSrc[32] = {
+    {-1, 0, 0},  {-1, 0, 7},  {-1, 0, 14}, {0, 0, 0},   {0, 0, 7},   {-1, 1, 3},  {-1, 1, 10}, {-1, 1, 17},
+    {1, 0, 0},   {1, 0, 7},   {-1, 2, 6},  {-1, 2, 13}, {2, 0, 0},   {2, 0, 7},   {-1, 3, 2},  {-1, 3, 9},
+    {-1, 3, 16}, {3, 0, 0},   {3, 0, 7},   {-1, 4, 5},  {-1, 4, 12}, {4, 0, 0},   {4, 0, 7},   {-1, 5, 1},
+    {-1, 5, 8},  {-1, 5, 15}, {5, 0, 0},   {5, 0, 7},   {-1, 6, 4},  {-1, 6, 11}, {6, 0, 0},   {6, 0, 7}};
+constexpr int kQ3hViewBit[7] = {21, 56, 84, 119, 147, 182, 210};  // stream bit at view bit 0
+constexpr int kQ3hAccScaleLog2 = 64;                              // accumulators carry 2^-64
+
+// view v of a block's code area (block words w[1..7])
+template <int V>
+__device__ __forceinline__ uint32_t q3h_sview(const uint32_t (&w)[8]) {
+  constexpr int bit = kQ3hViewBit[V];
+  constexpr int wi = 1 + bit / 32, sh = bit % 32;
+  if constexpr (wi + 1 <= 7) {
+    return __funnelshift_r(w[wi], w[wi + 1], sh);
+  } else {
+    return w[wi] >> sh;
+  }
+}
+
+template <int J>
+__device__ __forceinline__ uint32_t q3h_scode_bits(const uint32_t (&w)[8], const uint32_t (&vw)[7]) {
+  constexpr Q3HCodeSrc src = kQ3hSrc[J];
+  constexpr uint32_t mask = 0x7Fu << src.pos;
+  if constexpr (src.view < 0) {
+    return w[1 + src.word] & mask;
+  } else {
+    return vw[src.view] & mask;
+  }
+}
+
+// roundup(1/11) * 2^-s as bits: 1/11 rounds up to 0x3DBA2E8C in binary32
+__host__ __device__ constexpr uint32_t q3h_floor_mult_bits(int s) { return 0x3DBA2E8Cu - ((uint32_t)s << 23); }
+
+__device__ __forceinline__ u64 ffma2_rm(u64 a, u64 b, u64 c) {
+  u64 d;
+  asm("fma.rm.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+
+}  // namespace ifb

@@ -8,9 +8,11 @@
 
 #include "comm.cuh"
 #include "common.cuh"
+#include "decode_mk.cuh"
 #include "qgemm.cuh"
 
 namespace ifb {
+extern unsigned long long* g_mk_dbg;
 
 template <typename T>
 __device__ __forceinline__ T to_out(float v);
@@ -55,13 +57,13 @@ __global__ void vbcast_kernel(const float* __restrict__ qkv, OutT* __restrict__ 
   }
 }
 
-// act[t, f] = silu(g) * u,  [g|u] = gu[t]
+// act[t, f] = silu(g) * u with gate/up rows interleaved: g = gu[t, 2f], u = gu[t, 2f+1]
 template <typename OutT>
 __global__ void silu_mul_kernel(const float* __restrict__ gu, OutT* __restrict__ act, int T, int lf) {
   const int64_t total = (int64_t)T * lf;
   for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total; idx += (int64_t)gridDim.x * blockDim.x) {
     const int64_t t = idx / lf, f = idx - t * lf;
-    const float g = gu[t * 2 * lf + f], u = gu[t * 2 * lf + lf + f];
+    const float g = gu[t * 2 * lf + 2 * f], u = gu[t * 2 * lf + 2 * f + 1];
     act[idx] = to_out<OutT>(g / (1.0f + expf(-g)) * u);
   }
 }
@@ -74,7 +76,7 @@ static int ew_grid(int64_t n) {
 }
 
 struct Local {
-  int lh, lkv, lf, nq, nqkv, d, hd;
+  int lh, lkv, lf, nq, nqkv, d, hd, layers;
 };
 
 static if_status local_dims(const if_stack_shape* s, const if_plan* p, int rank, Local* L) {
@@ -95,6 +97,7 @@ static if_status local_dims(const if_stack_shape* s, const if_plan* p, int rank,
   L->d = s->hidden;
   L->nq = L->lh * s->head_dim;
   L->nqkv = (L->lh + 2 * L->lkv) * s->head_dim;
+  L->layers = a.layer_end - a.layer_begin;
   return IF_OK;
 }
 
@@ -107,6 +110,7 @@ struct WS {
   float* gu;
   float* act;
   float* part;
+  int* done;
   size_t bytes;
 };
 
@@ -125,6 +129,7 @@ static WS carve(void* base, const Local& L, int64_t T) {
   w.gu = take((size_t)T * 2 * L.lf);
   w.act = take((size_t)T * L.lf);
   w.part = take((size_t)T * L.d);
+  w.done = reinterpret_cast<int*>(take((size_t)4 * L.layers));
   w.bytes = off;
   return w;
 }
@@ -173,6 +178,47 @@ extern "C" if_status if_run_stack(const if_stack_shape* shape, const if_plan* pl
     if ((st = comm_recv(comm, h_out, nh, cs))) return st;
   }
   const int nlayers = asg.layer_end - asg.layer_begin;
+  // batch-1 Q3H_B64 decode on one TP rank: the whole stage in ONE persistent launch
+  const bool mk = mode == IF_DECODE && T == 1 && sc.type == IF_Q3H && sc.block == 64 && groups == 1 &&
+                  nlayers <= MK_MAXL && nlayers > 0;
+  if (mk) {
+    static thread_local MkParams P;
+    P.mode = MK_MODE_STACK;
+    P.layers = nlayers;
+    P.d = L.d;
+    P.nq = L.nq;
+    P.nqkv = L.nqkv;
+    P.lf = L.lf;
+    P.hd = L.hd;
+    P.lh = L.lh;
+    P.lkv = L.lkv;
+    P.h0 = asg.head_begin;
+    P.k0 = asg.kv_begin;
+    P.per = per;
+    P.h = h_out;
+    P.qkv = w.qkv;
+    P.act = w.act;
+    P.last_qkv = last_qkv;
+    P.done = w.done;
+    P.dbg = g_mk_dbg;
+    for (int l = 0; l < nlayers; l++) {
+      const if_layer_weights& Wl = stage_layers[l];
+      if (!Wl.wqkv || !Wl.wo || !Wl.wgu || !Wl.wdown) return set_error(IF_ERR_ARG, "if_run_stack: null weights, layer %d", l);
+      P.w[l][0] = Wl.wqkv;
+      P.w[l][1] = Wl.wo;
+      P.w[l][2] = Wl.wgu;
+      P.w[l][3] = Wl.wdown;
+    }
+    if (cudaMemsetAsync(w.done, 0, sizeof(int) * 4 * nlayers, cs) != cudaSuccess) return check_launch("if_run_stack: memset");
+    st = mk_launch(P, cs);
+    if (st != IF_ERR_UNSUPPORTED) {
+      if (st) return st;
+      if (!last) {
+        if ((st = comm_send(comm, h_out, nh, cs))) return st;
+      }
+      return check_launch("if_run_stack");
+    }
+  }
   for (int l = 0; l < nlayers; l++) {
     const if_layer_weights& Wl = stage_layers[l];
     if (!Wl.wqkv || !Wl.wo || !Wl.wgu || !Wl.wdown) return set_error(IF_ERR_ARG, "if_run_stack: null weights, layer %d", l);

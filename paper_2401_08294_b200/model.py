@@ -6,7 +6,7 @@ tensor at a time, so a 70B-shaped stack (34 GB packed) never needs its 274 GB
 fp32 form.  Rank-local shards follow the plan (if_plan_partition):
   wqkv  rows q[h0*hd:h1*hd] | k[k0*hd:k1*hd] | v[k0*hd:k1*hd]    (column shard)
   wo    K-columns [h0*hd, h1*hd) of every row                      (row shard)
-  wgu   rows gate[f0:f1] | up[f0:f1]                                (column shard)
+  wgu   rows gate[f0:f1] and up[f0:f1] interleaved (2f gate, 2f+1 up)  (column shard)
   wdown K-columns [f0, f1)                                          (row shard)
 Shards are exact slices of the unsharded packed tensors (block-aligned splits).
 """
@@ -48,6 +48,22 @@ def col_slice(packed: torch.Tensor, s: Scheme, N: int, K: int, c0: int, c1: int)
     return v.contiguous().view(-1)
 
 
+def interleave_rows(a: torch.Tensor, b: torch.Tensor, rows: int) -> torch.Tensor:
+    """Packed [rows, rb] tensors a, b -> [2*rows, rb] with rows a0, b0, a1, b1, ..."""
+    rb = a.numel() // rows
+    return torch.stack([a.view(rows, rb), b.view(rows, rb)], dim=1).reshape(-1).contiguous()
+
+
+def deinterleave_rows(p, rows2: int):
+    """Inverse of interleave_rows (numpy or torch): [2r, rb] -> concat(even rows, odd rows)."""
+    rb = p.shape[0] // rows2
+    v = p.reshape(rows2 // 2, 2, rb)
+    if isinstance(p, torch.Tensor):
+        return torch.cat([v[:, 0].reshape(-1), v[:, 1].reshape(-1)])
+    import numpy as np
+    return np.concatenate([v[:, 0].reshape(-1), v[:, 1].reshape(-1)])
+
+
 class Stack:
     """Rank-local packed shards of a synthetic stack (all layers of the rank's stage)."""
 
@@ -78,7 +94,7 @@ class Stack:
             del wo_full
             g = quantize_rows(s, l, "gate", F, d, d, f0, f1, scratch, self.dev_status)
             u = quantize_rows(s, l, "up", F, d, d, f0, f1, scratch, self.dev_status)
-            wgu = torch.cat([g, u])
+            wgu = interleave_rows(g, u, f1 - f0)  # row 2f = gate f, row 2f+1 = up f (ABI layout)
             del g, u
             wd_full = quantize_rows(s, l, "down", d, F, d, 0, d, scratch, self.dev_status)
             wdown = col_slice(wd_full, s, d, F, f0, f1) if (f1 - f0) != F else wd_full

@@ -14,7 +14,7 @@ import oracle as O
 import paper_2401_08294_b200 as F
 import synth
 from gpu_util import dev, normwise, torch
-from paper_2401_08294_b200.model import Stack
+from paper_2401_08294_b200.model import Stack, deinterleave_rows
 
 pytestmark = pytest.mark.gpu
 
@@ -41,7 +41,7 @@ def _run(cfg, qtype, bs, T, mode=F.IF_DECODE, want_qkv=True):
 def _oracle(cfg, qtype, bs, stk, h):
     host = [[t.cpu().numpy() for t in layer] for layer in stk.layers]
     return O.stack_f64(dict(cfg, qtype=qtype, block=bs), [l[0] for l in host], [l[1] for l in host],
-                       [l[2] for l in host], [l[3] for l in host], h)
+                       [deinterleave_rows(l[2], 2 * stk.local['lf']) for l in host], [l[3] for l in host], h)
 
 
 @pytest.mark.parametrize("qtype,bs", [(35, 64), (4, 32), (3, 32), (8, 64), (2, 64)])
