@@ -214,7 +214,7 @@ def run_ours(args):
     d = cfg["hidden"]
     h_in = torch.from_numpy(synth.activations(B, d)).to(dev)
     h_out = torch.empty_like(h_in)
-    wsb = torch.empty(F.if_stack_workspace_bytes(shape, plan, rank, B, F.IF_DECODE), dtype=torch.uint8, device=dev)
+    wsb = torch.zeros(F.if_stack_workspace_bytes(shape, plan, rank, B, F.IF_DECODE), dtype=torch.uint8, device=dev)
     stream = torch.cuda.Stream(dev)
 
     def step():

@@ -214,7 +214,9 @@ if_status if_comm_recv_prev(if_comm c, float* buf, int64_t n, if_stream_t stream
  * [T, (lh + 2 lkv) head_dim] of the stage's last layer (nullable).
  * mode IF_DECODE (1 <= T <= 64, qGEMV, fp32 activations) or IF_PREFILL
  * (T <= 4096, qGEMM on tcgen05 with bf16 activations).
- * workspace: device, if_stack_workspace_bytes().  comm may be NULL when
+ * workspace: device, if_stack_workspace_bytes(); ZERO-FILL IT ONCE before the
+ * first call (cudaMemset) and keep it with this (shape, plan, rank): it carries
+ * the decode engine's step epoch across calls.  comm may be NULL when
  * plan->devices == 1.  Never synchronises; graph capturable.
  * ------------------------------------------------------------------------- */
 enum { IF_DECODE = 0, IF_PREFILL = 1 };

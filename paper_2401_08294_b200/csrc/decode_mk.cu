@@ -47,6 +47,7 @@ constexpr int MK_THREADS = (MK_NC + 1) * 32;  // + producer warp
 constexpr int MK_SLOT = 32 * 1024;          // ring slot bytes
 constexpr int MK_MAXSLOT = 8;
 constexpr int MK_CT = MK_NC * 32;           // consumer threads
+constexpr int MK_MAXOWN = 256;              // residual rows owned by one CTA
 
 struct Geo {
   int N, K, nb, nchunk, nbp, row_bytes, r0, r1, rps, R;
@@ -325,7 +326,8 @@ __global__ void __launch_bounds__(MK_THREADS, 1) decode_mk_kernel(const __grid_c
   float4* xs = reinterpret_cast<float4*>(smem + (size_t)nslot * MK_SLOT + 2 * MK_MAXSLOT * 8 + 128);
   float2* bs = reinterpret_cast<float2*>(xs + 16 * xstride);
   float* raw = reinterpret_cast<float*>(bs + P.nbp_max);  // raw phase input (TMA bulk copy)
-  float* part = raw + P.raw_max;
+  float* h_own = raw + P.raw_max;                         // [MK_MAXOWN] this CTA's residual rows
+  float* part = h_own + MK_MAXOWN;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
@@ -374,6 +376,12 @@ __global__ void __launch_bounds__(MK_THREADS, 1) decode_mk_kernel(const __grid_c
   const int cw = warp - 1;
   const Q3HConst kc = q3h_const();
   uint32_t slot = 0, round = 0;  // ring position (same sequence as the producer)
+  if (P.mode == MK_MODE_STACK) {
+    // residual rows of this CTA (the o/down row split) from the stage input
+    const int base = P.d / G, rem = P.d % G;
+    const int o0 = cta * base + min(cta, rem), on = base + (cta < rem ? 1 : 0);
+    for (int i = ct; i < on; i += MK_CT) h_own[i] = P.h[o0 + i];
+  }
   for (int p = 0; p < nphase; p++) {
     const uint8_t* W;
     int N, K, kind;
@@ -515,7 +523,9 @@ __global__ void __launch_bounds__(MK_THREADS, 1) decode_mk_kernel(const __grid_c
         P.qkv[n] = s;
         if (P.last_qkv && p == nphase - 4) P.last_qkv[n] = s;
       } else if (kind == 1 || kind == 3) {
-        P.h[n] = __ldcg(P.h + n) + s;  // residual (the row is owned by this CTA)
+        const float hn = h_own[rr] + s;  // residual on the rows this CTA owns
+        h_own[rr] = hn;
+        P.h[n] = hn;
       } else {
         P.y_out[n] = P.acc ? P.y_out[n] + s : s;
       }
@@ -524,10 +534,7 @@ __global__ void __launch_bounds__(MK_THREADS, 1) decode_mk_kernel(const __grid_c
       // bar.sync orders every consumer's output stores before thread 0's
       // gpu-scope release (cumulativity); readers acquire the counter.
       named_bar_sync(1, MK_CT);
-      if (ct == 0) {
-        __threadfence();
-        red_release_gpu_add(&P.done[p], 1);
-      }
+      if (ct == 0) red_release_gpu_add(&P.done[p], 1);
     }
     if (dbg && ct == 0) dbg[5] = gtimer();
   }
@@ -579,7 +586,8 @@ if_status mk_launch(MkParams& P, cudaStream_t st) {
   int raw_max = P.mode == MK_MODE_GEMV ? P.gemv_K : std::max(std::max(P.d, P.lkv * P.hd), P.lf);
   raw_max = (raw_max + 3) & ~3;
   P.raw_max = raw_max;
-  const size_t fixed = mk_fixed_smem(nbp_max, part_max) + (size_t)4 * raw_max;
+  const size_t fixed = mk_fixed_smem(nbp_max, part_max) + (size_t)4 * raw_max + (size_t)4 * MK_MAXOWN;
+  if (P.mode == MK_MODE_STACK && (P.d + G - 1) / G > MK_MAXOWN) return IF_ERR_UNSUPPORTED;
   const size_t budget = 227 * 1024;
   if (fixed + 2 * (size_t)MK_SLOT > budget) return IF_ERR_UNSUPPORTED;
   int nslot = (int)((budget - fixed) / MK_SLOT);

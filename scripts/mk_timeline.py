@@ -44,7 +44,7 @@ else:
     stk = Stack(cfg, s, plan, 0, dev)
     h = torch.randn(1, cfg["hidden"], device=dev)
     out = torch.empty_like(h)
-    ws = torch.empty(F.if_stack_workspace_bytes(shape, plan, 0, 1, F.IF_DECODE), dtype=torch.uint8, device=dev)
+    ws = torch.zeros(F.if_stack_workspace_bytes(shape, plan, 0, 1, F.IF_DECODE), dtype=torch.uint8, device=dev)
     nph = 4 * cfg["layers"]
     dbg = torch.zeros(G * nph * 8, dtype=torch.int64, device=dev)
     for it in range(3):
@@ -55,11 +55,11 @@ L.ifx_set_mk_debug(None)
 d = dbg.view(G, nph, 8).cpu().numpy().astype(np.float64)
 t0 = d[:, 0, 0].min()
 d = (d - t0) / 1e3  # us
-names = ["start", "dep_ok", "x_ready", "staged", "units_done", "signalled"]
+names = ["start", "dep_ok", "x_ready", "staged", "units_done", "signalled", "combined"]
 print(f"== {' '.join(sys.argv[1:])}")
 for p in range(min(nph, 12)):
     row = []
-    for k in range(6):
+    for k in [0, 1, 2, 3, 4, 6, 5]:
         col = d[:, p, k]
         row.append(f"{names[k]} {col.min():7.2f}/{np.median(col):7.2f}/{col.max():7.2f}")
     print(f"phase {p:3d}: " + " | ".join(row))

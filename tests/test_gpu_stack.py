@@ -32,7 +32,7 @@ def _run(cfg, qtype, bs, T, mode=F.IF_DECODE, want_qkv=True):
     out = torch.empty_like(hd)
     nqkv = (cfg["heads"] + 2 * cfg["kv_heads"]) * cfg["head_dim"]
     qkv = torch.empty(T, nqkv, device=d) if want_qkv else None
-    ws = torch.empty(F.if_stack_workspace_bytes(shape, plan, 0, T, mode), dtype=torch.uint8, device=d)
+    ws = torch.zeros(F.if_stack_workspace_bytes(shape, plan, 0, T, mode), dtype=torch.uint8, device=d)
     F.if_run_stack(shape, plan, 0, None, stk.arr, hd, T, mode, out, qkv, ws)
     torch.cuda.synchronize()
     return stk, h, out.cpu().numpy(), (qkv.cpu().numpy() if want_qkv else None)
@@ -85,3 +85,27 @@ def test_stack_decode_7b_full_size():
     ho, qo = _oracle(cfg, 35, 64, stk, h)
     assert normwise(out, ho) <= 1e-3
     assert normwise(qkv, qo) <= 1e-3
+
+
+def test_stack_decode_repeated_calls_same_workspace():
+    """The decode engine tags its activations with a per-call epoch kept in the
+    workspace: back-to-back calls (as in a graph replay loop) must each produce
+    the oracle's result, including after the input changes."""
+    d = dev()
+    cfg = SMALL
+    s = F.scheme(35, 64)
+    shape = F.stack_shape(*[cfg[k] for k in ("layers", "hidden", "heads", "kv_heads", "head_dim", "ffn")], s)
+    plan = F.if_plan_partition(F.IF_BY_LAYER, shape, 1)
+    stk = Stack(cfg, s, plan, 0, d)
+    ws = torch.zeros(F.if_stack_workspace_bytes(shape, plan, 0, 1, F.IF_DECODE), dtype=torch.uint8, device=d)
+    outs = []
+    for it in range(5):
+        h = synth.activations(1, cfg["hidden"], tid=10 + (it // 2))
+        hd = torch.from_numpy(h).to(d)
+        out = torch.empty_like(hd)
+        F.if_run_stack(shape, plan, 0, None, stk.arr, hd, 1, F.IF_DECODE, out, None, ws)
+        torch.cuda.synchronize()
+        ho, _ = _oracle(cfg, 35, 64, stk, h)
+        assert normwise(out.cpu().numpy(), ho) <= 1e-3, it
+        outs.append(out.cpu().numpy())
+    assert np.array_equal(outs[0], outs[1]) and np.array_equal(outs[2], outs[3])  # deterministic
