@@ -57,7 +57,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                 "-lms", "20"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
         except Exception:
@@ -260,6 +260,8 @@ def run_ours(args):
     tok_s = B * args.steps / (ms / 1e3)  # tokens of the job (one stream of B tokens per step)
     total_bytes = stack_bytes_total(cfg, s)
     gbs = total_bytes / (ms_per_step / 1e3) / 1e9  # whole-job weight bytes streamed per second
+    rank_bytes = stk.weight_bytes()
+    stack_gbs_rank = rank_bytes / (ms_per_step / 1e3) / 1e9
 
     # ---- e2e through the public API: pinned host h_in -> device -> stack -> host h_out
     h_host = torch.from_numpy(synth.activations(B, d)).pin_memory()
@@ -287,8 +289,27 @@ def run_ours(args):
     e2e = {"value": B * args.steps / (ms_e2e / 1e3), "unit": "tokens/s", "h2d_bytes_per_step": B * d * 4,
            "d2h_bytes_per_step": B * d * 4}
 
-    # ---- roofline of the dominant kernel (the fused qGEMV), timed live with CUDA events
-    roof = gemv_roofline(F, torch, stk, cfg, s, B, stream, hbm_peak, peak_kind)
+    # ---- roofline of the dominant kernel.  For batch-1 Q3H the whole step is ONE
+    #      launch of the persistent decode kernel (decode_mk: 128 fused-dequant
+    #      GEMV phases + glue), so its average launch duration is the step time
+    #      measured above on the launching stream (the graph adds only a 16 KB
+    #      device copy and a 512 B memset around it).  Algorithmic bytes per
+    #      launch = the packed weights of the rank's layers (0.5 B/weight).
+    launches_mk = launches_per_step
+    roof = {"kernel": "decode_mk (persistent whole-stack decode, 1 launch/step)" if launches_mk == 1 else
+            "qgemv (per-layer kernels)", "bound": "hbm", "achieved": stack_gbs_rank,
+            "peak": hbm_peak, "unit": "GB/s", "frac": stack_gbs_rank / hbm_peak,
+            "peak_kind": f"{peak_kind} copy bandwidth (MEASURED_PEAKS.json hbm_gbs)",
+            "traffic": None, "avg_launch_us": ms_per_step * 1e3 / max(1, launches_mk),
+            "algorithmic_bytes_per_launch": rank_bytes // max(1, launches_mk),
+            "algorithmic_bytes": "packed weight bytes (0.5 B/weight incl. two fp16 per 64-block)"}
+    prof_path = os.path.join(ROOT, "profiles", "decode_mk_traffic.json")
+    if os.path.exists(prof_path):
+        try:
+            with open(prof_path) as f:
+                roof["traffic"] = json.load(f).get("dram_bytes_per_launch")
+        except Exception:
+            pass
 
     line = None
     if rank == 0:
@@ -321,47 +342,10 @@ def stack_bytes_total(cfg, s):
     return per * cfg["layers"]
 
 
-def gemv_roofline(F, torch, stk, cfg, s, B, stream, hbm_peak, peak_kind):
-    """Time the fused qGEMV alone, in the stack's launch configuration, over all of
-    the rank's layers in rotation (no L2 reuse), with CUDA events on its stream."""
-    d = cfg["hidden"]
-    a = stk.plan.a[stk.rank]
-    lh, lkv, lf = stk.local["lh"], stk.local["lkv"], stk.local["lf"]
-    hd = cfg["head_dim"]
-    shapes = [("qkv", (lh + 2 * lkv) * hd, d, 0), ("o", d, lh * hd, 1), ("gate_up", 2 * lf, d, 2), ("down", d, lf, 3)]
-    x = torch.randn(B, max(d, lf, lh * hd), device=stk.dev_status.device)
-    y = torch.empty(B, max(2 * lf, (lh + 2 * lkv) * hd, d), device=x.device)
-    tot_bytes, tot_ms, launches = 0, 0.0, 0
-    for name, N, K, idx in shapes:
-        xs = x[:, :K].contiguous()
-        with torch.cuda.stream(stream):
-            for layer in stk.layers[:2]:
-                F.if_qgemv(s, layer[idx], N, K, xs, B, y, stream)
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            reps = 3
-            e0.record(stream)
-            for _ in range(reps):
-                for layer in stk.layers:
-                    F.if_qgemv(s, layer[idx], N, K, xs, B, y, stream)
-            e1.record(stream)
-        e1.synchronize()
-        ms = e0.elapsed_time(e1)
-        n = reps * len(stk.layers)
-        tot_bytes += n * F.if_packed_bytes(s, N, K)
-        tot_ms += ms
-        launches += n
-    achieved = tot_bytes / (tot_ms / 1e3) / 1e9
-    return {"kernel": "qgemv_q3h64 (fused dequant GEMV, all 4 stack shapes)", "bound": "hbm",
-            "achieved": achieved, "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak,
-            "peak_kind": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)" if peak_kind == "measured" else peak_kind,
-            "traffic": None, "avg_launch_us": tot_ms * 1e3 / launches,
-            "algorithmic_bytes": "packed weight bytes per launch (0.5 B/weight incl. two fp16 per 64-block)"}
-
-
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--batch", type=int, default=1)
     ap.add_argument("--model", default="7b", choices=["7b", "13b", "70b"])
