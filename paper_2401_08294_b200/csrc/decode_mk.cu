@@ -44,16 +44,20 @@ namespace ifb {
 constexpr int MK_NC = IFB_MK_NC;            // consumer warps
 constexpr int MK_RMAX = IFB_MK_RMAX;        // rows per unit (x reuse)
 constexpr int MK_THREADS = (MK_NC + 1) * 32;  // + producer warp
-constexpr int MK_SLOT = 32 * 1024;          // ring slot bytes
+constexpr int MK_SLOT = 24 * 1024;          // ring slot bytes
 constexpr int MK_MAXSLOT = 8;
 constexpr int MK_CT = MK_NC * 32;           // consumer threads
 constexpr int MK_MAXOWN = 256;              // residual rows owned by one CTA
+constexpr int MK_MAXG = 160;                // >= CTAs in the grid (sum-h^2 partials)
 
 struct Geo {
   int N, K, nb, nchunk, nbp, row_bytes, r0, r1, rps, R;
 };
 
-__device__ __forceinline__ Geo phase_geo(int N, int K, int G, int cta, int pairs) {
+// rows are split over the CTAs in contiguous balanced groups of `unit` rows
+// (4 in stack mode: pairs of outputs for the transformed epilogue writes, and
+// two (gate, up) row pairs = one act pair in the gate/up phase)
+__device__ __forceinline__ Geo phase_geo(int N, int K, int G, int cta, int unit) {
   Geo g;
   g.N = N;
   g.K = K;
@@ -61,15 +65,10 @@ __device__ __forceinline__ Geo phase_geo(int N, int K, int G, int cta, int pairs
   g.nchunk = (g.nb + 31) >> 5;
   g.nbp = g.nchunk << 5;
   g.row_bytes = g.nb * 32;
-  // contiguous balanced row ranges; the gate/up phase splits (gate, up) row pairs
-  const int units = pairs ? N / 2 : N;
+  const int units = N / unit;
   const int base = units / G, rem = units % G;
-  g.r0 = cta * base + min(cta, rem);
-  g.r1 = g.r0 + base + (cta < rem ? 1 : 0);
-  if (pairs) {
-    g.r0 *= 2;
-    g.r1 *= 2;
-  }
+  g.r0 = (cta * base + min(cta, rem)) * unit;
+  g.r1 = g.r0 + (base + (cta < rem ? 1 : 0)) * unit;
   int rps = MK_SLOT / g.row_bytes;
   if (MK_RMAX >= 8 && rps >= 8) {
     g.R = 8;
@@ -268,48 +267,46 @@ __device__ __forceinline__ void mk_unit_dispatch(const unsigned char* slot_rows,
     mk_unit<R, XS, false>(slot_rows, row_bytes, nrows_valid, c, nb, xs_rt, xs, bs, part_rows, nchunk, kc);
 }
 
-// Stage the transformed x of one phase: for the float4 quad q (weights 4q..4q+3,
-// i.e. pairs 2q, 2q+1 of block b = q / 16, JJ = q % 16) write
-//   xs[JJ * xstride + b] = {512 x_o(2JJ), 512 x_o(2JJ+1), xe'(2JJ), xe'(2JJ+1)}
-// (identity (*) of simd.cuh) and bs[b] = {sum x, sum x_odd}.  src4(q) returns the
-// 4 raw inputs of quad q (already scaled).  Consecutive threads read
-// consecutive quads; xstride = nbp + 1 makes the transposed stores
-// conflict-free; a block's 16 quads sit in one half-warp for the block sums.
-// code bit position s_j of pair j (simd.cuh kQ3hSrc), for the per-pair x scaling
-__constant__ int kQ3hPosC[32] = {0, 7, 14, 0, 7, 3, 10, 17, 0, 7, 6, 13, 0, 7, 2, 9,
-                                 16, 0, 7, 5, 12, 0, 7, 1, 8, 15, 0, 7, 4, 11, 0, 7};
+// code bit position s_j of pair j (simd.cuh kQ3hSrc), for the per-pair x scaling;
+// copied to shared memory at kernel start (lanes index it with different j)
+__device__ const int kQ3hPosTab[32] = {0, 7, 14, 0, 7, 3, 10, 17, 0, 7, 6, 13, 0, 7, 2, 9,
+                                       16, 0, 7, 5, 12, 0, 7, 1, 8, 15, 0, 7, 4, 11, 0, 7};
+constexpr int MK_MAXQ = 8;  // staged quads held in registers per consumer thread
 
-// Stage the transformed x of one phase: for the float4 quad q (weights
-// 4q..4q+3 = pairs 2JJ, 2JJ+1 of block b = q / 16, JJ = q % 16) write
+// Stage one quad of x: weights 4q..4q+3 = pairs 2JJ, 2JJ+1 of block b = q / 16,
+// JJ = q % 16:
 //   xs[JJ * xstride + b] = {X_c(2JJ), X_c(2JJ+1), X_q(2JJ), X_q(2JJ+1)}
 //   X_c(j) = x_o(j) * 2^(85 - s_j),   X_q(j) = (x_e(j) - 11 x_o(j)) * 2^85
-// (subnormal-form decode, simd.cuh) and bs[b].x = sum of the block's x.
-// Consecutive threads read consecutive quads; xstride = 1 (mod 8) makes the
-// transposed stores conflict-free; a block's 16 quads sit in one half-warp.
-template <typename Src4>
-__device__ __forceinline__ void stage_x(int K, int nbp, int xstride, float4* xs, float2* bs, Src4 src4) {
-  const int ct = threadIdx.x - 32;  // consumer thread id
-  const int nq = K >> 2, nqp = nbp * 16;
+// (subnormal-form decode, simd.cuh) and bs[b].x = sum of the block's 64 x.
+// xstride = 1 (mod 8) makes the transposed stores conflict-free; a block's 16
+// quads sit in one half-warp (all 32 lanes must call this together).
+__device__ __forceinline__ void stage_quad(int q, float4 v, int xstride, float4* xs, float2* bs, const int* pos) {
+  const int b = q >> 4, jj = q & 15;
   const float s85 = 38685626227668133590597632.0f;  // 2^85
-  for (int q = ct; q < nqp; q += MK_CT) {
-    const int b = q >> 4, jj = q & 15;
-    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (q < nq) v = src4(q);
-    // pairs (v.x, v.y) and (v.z, v.w): x_e = .x/.z, x_o = .y/.w
-    const float c0 = __uint_as_float((uint32_t)(127 + 85 - kQ3hPosC[2 * jj]) << 23);
-    const float c1 = __uint_as_float((uint32_t)(127 + 85 - kQ3hPosC[2 * jj + 1]) << 23);
-    xs[jj * xstride + b] = make_float4(v.y * c0, v.w * c1, fmaf(-11.0f, v.y, v.x) * s85, fmaf(-11.0f, v.w, v.z) * s85);
-    float sx = (v.x + v.y) + (v.z + v.w);
+  const float c0 = __uint_as_float((uint32_t)(127 + 85 - pos[2 * jj]) << 23);
+  const float c1 = __uint_as_float((uint32_t)(127 + 85 - pos[2 * jj + 1]) << 23);
+  // pairs (v.x, v.y) and (v.z, v.w): x_e = .x/.z, x_o = .y/.w
+  xs[jj * xstride + b] = make_float4(v.y * c0, v.w * c1, fmaf(-11.0f, v.y, v.x) * s85, fmaf(-11.0f, v.w, v.z) * s85);
+  float sx = (v.x + v.y) + (v.z + v.w);
 #pragma unroll
-    for (int o = 8; o > 0; o >>= 1) sx += __shfl_xor_sync(0xffffffffu, sx, o);
-    if (jj == 0) bs[b] = make_float2(sx, 0.f);
-  }
+  for (int o = 8; o > 0; o >>= 1) sx += __shfl_xor_sync(0xffffffffu, sx, o);
+  if (jj == 0) bs[b] = make_float2(sx, 0.f);
 }
 
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
   return t;
+}
+
+// Write the transformed pair (x_e, x_o) of element k (k even) of a phase input
+// into a global xs image with the shared-memory layout of stage_quad.
+__device__ __forceinline__ void put_pair(float4* xsg, int xstride, const int* pos, int k, float xe, float xo) {
+  const int b = k >> 6, j = (k >> 1) & 31, jj = j >> 1, comp = j & 1;
+  float* f = reinterpret_cast<float*>(xsg + jj * xstride + b);
+  const float cj = __uint_as_float((uint32_t)(127 + 85 - pos[j]) << 23);  // 2^(85 - s_j)
+  f[comp] = xo * cj;
+  f[2 + comp] = fmaf(-11.0f, xo, xe) * 38685626227668133590597632.0f;  // * 2^85
 }
 
 template <int XS>
@@ -321,13 +318,16 @@ __global__ void __launch_bounds__(MK_THREADS, 1) decode_mk_kernel(const __grid_c
   unsigned char* ring = smem;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)nslot * MK_SLOT);
   uint64_t* empty = full + MK_MAXSLOT;
-  float* red = reinterpret_cast<float*>(empty + MK_MAXSLOT);  // [MK_NC + 1]
+  float* red = reinterpret_cast<float*>(empty + MK_MAXSLOT);  // [MK_NC] + scalars
   uint64_t* xbar = reinterpret_cast<uint64_t*>(red + 30);
   float4* xs = reinterpret_cast<float4*>(smem + (size_t)nslot * MK_SLOT + 2 * MK_MAXSLOT * 8 + 128);
   float2* bs = reinterpret_cast<float2*>(xs + 16 * xstride);
-  float* raw = reinterpret_cast<float*>(bs + P.nbp_max);  // raw phase input (TMA bulk copy)
-  float* h_own = raw + P.raw_max;                         // [MK_MAXOWN] this CTA's residual rows
-  float* part = h_own + MK_MAXOWN;
+  float* raw_sep = reinterpret_cast<float*>(bs + P.nbp_max);  // raw phase input when not staged in place
+  float* raw = P.raw_max ? raw_sep : reinterpret_cast<float*>(xs);  // TMA bulk-copy target
+  float* h_own = raw_sep + P.raw_max;                         // [MK_MAXOWN] this CTA's residual rows
+  int* pos = reinterpret_cast<int*>(h_own + MK_MAXOWN);       // [32] code positions
+  float* ssq_s = reinterpret_cast<float*>(pos + 32);          // [MK_MAXG] sum h^2 partials
+  float* part = ssq_s + MK_MAXG;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
@@ -338,8 +338,11 @@ __global__ void __launch_bounds__(MK_THREADS, 1) decode_mk_kernel(const __grid_c
     mbar_init(xbar, 1);
     fence_mbar_init();
   }
+  if (threadIdx.x < 32) pos[threadIdx.x] = kQ3hPosTab[threadIdx.x];
   __syncthreads();
-  const int nphase = P.mode == MK_MODE_GEMV ? 1 : 4 * P.layers;
+  const bool stack = P.mode == MK_MODE_STACK;
+  const int nphase = stack ? 4 * P.layers : 1;
+  const int unit = stack ? 4 : 1;
 
   if (warp == 0) {
     // ============================ producer ============================
@@ -354,7 +357,7 @@ __global__ void __launch_bounds__(MK_THREADS, 1) decode_mk_kernel(const __grid_c
         const uint8_t* W;
         int N, K, kind;
         phase_dims(P, p, &W, &N, &K, &kind);
-        const Geo g = phase_geo(N, K, G, cta, kind == 2);
+        const Geo g = phase_geo(N, K, G, cta, unit);
         for (int r = g.r0; r < g.r1; r += g.rps) {
           const int n = min(g.rps, g.r1 - r);
           const uint32_t bytes = (uint32_t)n * g.row_bytes;
@@ -376,83 +379,132 @@ __global__ void __launch_bounds__(MK_THREADS, 1) decode_mk_kernel(const __grid_c
   const int cw = warp - 1;
   const Q3HConst kc = q3h_const();
   uint32_t slot = 0, round = 0;  // ring position (same sequence as the producer)
-  if (P.mode == MK_MODE_STACK) {
+  if (stack) {
     // residual rows of this CTA (the o/down row split) from the stage input
-    const int base = P.d / G, rem = P.d % G;
-    const int o0 = cta * base + min(cta, rem), on = base + (cta < rem ? 1 : 0);
-    for (int i = ct; i < on; i += MK_CT) h_own[i] = P.h[o0 + i];
+    const Geo go = phase_geo(P.d, P.nq, G, cta, unit);
+    for (int i = ct; i < go.r1 - go.r0; i += MK_CT) h_own[i] = P.h[go.r0 + i];
   }
   for (int p = 0; p < nphase; p++) {
     const uint8_t* W;
     int N, K, kind;
     phase_dims(P, p, &W, &N, &K, &kind);
-    const Geo g = phase_geo(N, K, G, cta, kind == 2);
+    const Geo g = phase_geo(N, K, G, cta, unit);
     (void)W;
-    // ---- 1. dependency on the previous phase (all CTAs), then one bulk copy of
-    //         the phase's raw input (L2 -> smem on the TMA engine) ----
-    const float* src;
-    int src_n;
-    if (kind == 0 || kind == 2) {
-      src = P.h;
-      src_n = K;
-    } else if (kind == 1) {
-      src = P.qkv + (size_t)(P.lh + P.lkv) * P.hd;  // v rows of my kv heads
-      src_n = P.lkv * P.hd;
-    } else if (kind == 3) {
-      src = P.act;
-      src_n = K;
-    } else {
-      src = P.x_in;
-      src_n = K;
-    }
     unsigned long long* dbg = P.dbg ? P.dbg + ((size_t)cta * nphase + p) * 8 : nullptr;
     if (dbg && ct == 0) dbg[0] = gtimer();
-    if (ct == 0) {
-      if (p > 0) {
+    // Phase input.  Producers (the previous phase's epilogues) already wrote it in
+    // the transformed quad layout into a global xs image: one dependency wait, then
+    // 16 bulk copies (one per quad row JJ) + the sum-h^2 partials for RMSNorm.
+    // The first phase (plain h) and the standalone GEMV stage from raw instead.
+    const bool from_image = stack && p > 0;
+    const bool rms = kind == 0 || kind == 2;
+    float out_scale = 1.f;  // RMSNorm folded into the output: W (s h) = s (W h)
+    if (from_image) {
+      const float4* img = kind == 1 ? P.xs_ctx : (kind == 3 ? P.xs_act : P.xs_h);
+      const uint32_t row_bytes = (uint32_t)g.nbp * 16u;
+      const uint32_t ssq_bytes = rms ? (uint32_t)((G + 3) & ~3) * 4u : 0u;
+      if (ct == 0) {
         while (ld_acquire_gpu(&P.done[p - 1]) < G) __nanosleep(20);
+        if (dbg) dbg[1] = gtimer();
+        asm volatile("fence.proxy.async.global;" ::: "memory");  // generic writes -> async-proxy reads
+        mbar_arrive_expect_tx(xbar, 16u * row_bytes + ssq_bytes);
+        for (int jj = 0; jj < 16; jj++)
+          bulk_g2s(xs + jj * xstride, img + jj * xstride, row_bytes, xbar, 0ull, false);
+        if (rms) bulk_g2s(ssq_s, P.ssq, ssq_bytes, xbar, 0ull, false);
       }
-      if (dbg) dbg[1] = gtimer();
-      asm volatile("fence.proxy.async.global;" ::: "memory");  // generic writes -> async-proxy reads
-      mbar_arrive_expect_tx(xbar, (uint32_t)src_n * 4u);
-      bulk_g2s(raw, src, (uint32_t)src_n * 4u, xbar, 0ull, false);
-    }
-    mbar_wait(xbar, p & 1);
-    if (dbg && ct == 0) dbg[2] = gtimer();
-    // ---- 2. stage x for this phase (glue fused here) ----
-    const float4* raw4 = reinterpret_cast<const float4*>(raw);
-    if (kind == 0 || kind == 2) {
-      // a = h / sqrt(mean(h^2) + 1e-5)
-      float ss = 0.f;
-      for (int q = ct; q < (K >> 2); q += MK_CT) {
-        const float4 v = raw4[q];
-        ss = fmaf(v.x, v.x, ss);
-        ss = fmaf(v.y, v.y, ss);
-        ss = fmaf(v.z, v.z, ss);
-        ss = fmaf(v.w, v.w, ss);
+      mbar_wait(xbar, p & 1);
+      if (dbg && ct == 0) dbg[2] = gtimer();
+      // block sums of x from the image: x_e + x_o = xe' + 12 x_o
+      for (int b = ct; b < g.nbp; b += MK_CT) {
+        float sx = 0.f;
+#pragma unroll 4
+        for (int jj = 0; jj < 16; jj++) {
+          const float4 v = xs[jj * xstride + b];
+          const float c0 = __uint_as_float((uint32_t)(127 - 85 + pos[2 * jj]) << 23);  // 2^(s - 85)
+          const float c1 = __uint_as_float((uint32_t)(127 - 85 + pos[2 * jj + 1]) << 23);
+          sx += (v.z + v.w) * 2.5849394142282115e-26f + 12.0f * (v.x * c0 + v.y * c1);  // 2^-85
+        }
+        bs[b] = make_float2(sx, 0.f);
       }
+      if (rms) {
+        if (cw == 0) {
+          float t = 0.f;
+          for (int c = lane; c < G; c += 32) t += ssq_s[c];
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
-      if (lane == 0) red[cw] = ss;
+          for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+          if (lane == 0) red[16] = t;
+        }
+      }
       named_bar_sync(1, MK_CT);
-      float tot = 0.f;
-#pragma unroll
-      for (int w = 0; w < MK_NC; w++) tot += red[w];
-      const float inv = 1.0f / sqrtf(tot / (float)K + 1e-5f);
-      stage_x(K, g.nbp, xstride, xs, bs, [&](int q) {
-        const float4 v = raw4[q];
-        return make_float4(v.x * inv, v.y * inv, v.z * inv, v.w * inv);
-      });
-    } else if (kind == 1) {
-      // ctx head i = v row of kv group floor((h0+i)/per) - k0; hd % 4 == 0
-      const int hd4 = P.hd >> 2, h0 = P.h0, k0 = P.k0, per = P.per;
-      stage_x(K, g.nbp, xstride, xs, bs, [&](int q) {
-        const int i = q / hd4, e = q - i * hd4;
-        return raw4[((h0 + i) / per - k0) * hd4 + e];
-      });
+      if (rms) out_scale = 1.0f / sqrtf(red[16] / (float)K + 1e-5f);
     } else {
-      stage_x(K, g.nbp, xstride, xs, bs, [&](int q) { return raw4[q]; });
+      // raw input -> registers -> transformed quads (raw may alias xs)
+      const float* src = stack ? P.h : P.x_in;
+      if (ct == 0) {
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+        mbar_arrive_expect_tx(xbar, (uint32_t)K * 4u);
+        bulk_g2s(raw, src, (uint32_t)K * 4u, xbar, 0ull, false);
+      }
+      mbar_wait(xbar, p & 1);
+      if (dbg && ct == 0) dbg[2] = gtimer();
+      const float4* raw4 = reinterpret_cast<const float4*>(raw);
+      const int nq = K >> 2, nqp = g.nbp * 16;
+      float inv = 1.f;
+      if (P.raw_max == 0) {
+        float4 v[MK_MAXQ];
+        float ss = 0.f;
+#pragma unroll
+        for (int i = 0; i < MK_MAXQ; i++) {
+          const int q = ct + i * MK_CT;
+          v[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (q < nq) {
+            v[i] = raw4[q];
+            ss = fmaf(v[i].x, v[i].x, fmaf(v[i].y, v[i].y, fmaf(v[i].z, v[i].z, fmaf(v[i].w, v[i].w, ss))));
+          }
+        }
+        if (rms) {
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+          if (lane == 0) red[cw] = ss;
+        }
+        named_bar_sync(1, MK_CT);  // every raw read is done: xs may now overwrite it
+        if (rms) {
+          float tot = 0.f;
+#pragma unroll
+          for (int w = 0; w < MK_NC; w++) tot += red[w];
+          inv = 1.0f / sqrtf(tot / (float)K + 1e-5f);  // a = h / sqrt(mean(h^2) + 1e-5)
+        }
+#pragma unroll
+        for (int i = 0; i < MK_MAXQ; i++) {
+          if (i * MK_CT + (ct & ~31) < nqp) {  // per-warp (nqp is a multiple of 32)
+            const float4 a = v[i];
+            stage_quad(ct + i * MK_CT, make_float4(a.x * inv, a.y * inv, a.z * inv, a.w * inv), xstride, xs, bs, pos);
+          }
+        }
+      } else {
+        if (rms) {
+          float ss = 0.f;
+          for (int q = ct; q < nq; q += MK_CT) {
+            const float4 v = raw4[q];
+            ss = fmaf(v.x, v.x, fmaf(v.y, v.y, fmaf(v.z, v.z, fmaf(v.w, v.w, ss))));
+          }
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+          if (lane == 0) red[cw] = ss;
+          named_bar_sync(1, MK_CT);
+          float tot = 0.f;
+#pragma unroll
+          for (int w = 0; w < MK_NC; w++) tot += red[w];
+          inv = 1.0f / sqrtf(tot / (float)K + 1e-5f);
+        }
+        for (int q = ct; q < nqp; q += MK_CT) {
+          float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (q < nq) v = raw4[q];
+          stage_quad(q, make_float4(v.x * inv, v.y * inv, v.z * inv, v.w * inv), xstride, xs, bs, pos);
+        }
+      }
+      named_bar_sync(1, MK_CT);
     }
-    named_bar_sync(1, MK_CT);
     if (dbg && ct == 0) dbg[3] = gtimer();
     // ---- 3. stream this CTA's rows from the ring.  Every consumer warp visits
     //         every slot (wait full -> its units -> arrive empty, count NC);
@@ -501,33 +553,79 @@ __global__ void __launch_bounds__(MK_THREADS, 1) decode_mk_kernel(const __grid_c
     }
     named_bar_sync(1, MK_CT);
     if (dbg && ct == 0) dbg[4] = gtimer();
-    // ---- 4. combine chunks (fixed order) + epilogue ----
+    // ---- 4. combine chunks (fixed order) + epilogue.  Outputs feeding the next
+    //         phase are written pre-transformed (put_pair) into its xs image. ----
     const int nr = g.r1 - g.r0;
-    if (kind == 2) {
-      // interleaved gate/up rows (2f, 2f+1): act[f] = silu(g) * u
-      for (int rr = ct; rr < nr / 2; rr += MK_CT) {
-        float gg = 0.f, u = 0.f;
-        for (int c = 0; c < g.nchunk; c++) {
-          gg += part[(2 * rr) * g.nchunk + c];
-          u += part[(2 * rr + 1) * g.nchunk + c];
-        }
-        const int f = g.r0 / 2 + rr;
-        P.act[f] = gg / (1.0f + expf(-gg)) * u;
+    const int nc = g.nchunk;
+    if (!stack) {
+      for (int rr = ct; rr < nr; rr += MK_CT) {
+        float sacc = 0.f;
+        for (int c = 0; c < nc; c++) sacc += part[rr * nc + c];
+        const int n = g.r0 + rr;
+        P.y_out[n] = P.acc ? P.y_out[n] + sacc : sacc;
       }
-    }
-    for (int rr = ct; rr < nr && kind != 2; rr += MK_CT) {
-      float s = 0.f;
-      for (int c = 0; c < g.nchunk; c++) s += part[rr * g.nchunk + c];
-      const int n = g.r0 + rr;
-      if (kind == 0) {
-        P.qkv[n] = s;
-        if (P.last_qkv && p == nphase - 4) P.last_qkv[n] = s;
-      } else if (kind == 1 || kind == 3) {
-        const float hn = h_own[rr] + s;  // residual on the rows this CTA owns
-        h_own[rr] = hn;
-        P.h[n] = hn;
-      } else {
-        P.y_out[n] = P.acc ? P.y_out[n] + s : s;
+    } else if (kind == 2) {
+      // interleaved gate/up rows (2f, 2f+1), two f per thread: act pair
+      for (int rr = 4 * ct; rr < nr; rr += 4 * MK_CT) {
+        float a[2];
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+          float gg = 0.f, u = 0.f;
+          for (int c = 0; c < nc; c++) {
+            gg += part[(rr + 2 * h) * nc + c];
+            u += part[(rr + 2 * h + 1) * nc + c];
+          }
+          gg *= out_scale;
+          u *= out_scale;
+          a[h] = gg / (1.0f + expf(-gg)) * u;
+        }
+        put_pair(P.xs_act, xstride, pos, (g.r0 + rr) / 2, a[0], a[1]);
+      }
+    } else if (kind == 0) {
+      const int v_off = (P.lh + P.lkv) * P.hd;
+      const bool last_layer = p == nphase - 4;
+      for (int rr = 2 * ct; rr < nr; rr += 2 * MK_CT) {
+        float v2[2];
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+          float sacc = 0.f;
+          for (int c = 0; c < nc; c++) sacc += part[(rr + h) * nc + c];
+          v2[h] = sacc * out_scale;
+          if (last_layer && P.last_qkv) P.last_qkv[g.r0 + rr + h] = v2[h];
+        }
+        const int n = g.r0 + rr;
+        if (n >= v_off) {
+          // ctx heads i whose kv group is this v head: scatter the pair
+          const int ev = n - v_off, jv = ev / P.hd, e = ev - jv * P.hd;
+          const int i0 = (jv + P.k0) * P.per - P.h0;
+          for (int i = max(i0, 0); i < min(i0 + P.per, P.lh); i++) put_pair(P.xs_ctx, xstride, pos, i * P.hd + e, v2[0], v2[1]);
+        }
+      }
+    } else {
+      // o / down: residual on the rows this CTA owns; sum h^2 partial for RMSNorm
+      float ss = 0.f;
+      for (int rr = 2 * ct; rr < nr; rr += 2 * MK_CT) {
+        float hn[2];
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+          float sacc = 0.f;
+          for (int c = 0; c < nc; c++) sacc += part[(rr + h) * nc + c];
+          hn[h] = h_own[rr + h] + sacc;
+          h_own[rr + h] = hn[h];
+          ss = fmaf(hn[h], hn[h], ss);
+          if (p == nphase - 1) P.h[g.r0 + rr + h] = hn[h];  // stage output
+        }
+        put_pair(P.xs_h, xstride, pos, g.r0 + rr, hn[0], hn[1]);
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+      if (lane == 0) red[cw] = ss;
+      named_bar_sync(1, MK_CT);
+      if (ct == 0) {
+        float t = 0.f;
+#pragma unroll
+        for (int w = 0; w < MK_NC; w++) t += red[w];
+        P.ssq[cta] = t;
       }
     }
     if (p + 1 < nphase) {
@@ -564,7 +662,7 @@ static size_t mk_fixed_smem(int nbp_max, int part_max) {
 }
 
 static int part_need(int N, int K, int G) {
-  const int rows = (N + G - 1) / G;
+  const int rows = (N + G - 1) / G + 4;
   return rows * ((K / 64 + 31) / 32);
 }
 
@@ -583,11 +681,17 @@ if_status mk_launch(MkParams& P, cudaStream_t st) {
     }
   }
   P.nbp_max = nbp_max;
-  int raw_max = P.mode == MK_MODE_GEMV ? P.gemv_K : std::max(std::max(P.d, P.lkv * P.hd), P.lf);
-  raw_max = (raw_max + 3) & ~3;
+  int raw_need = P.mode == MK_MODE_GEMV ? P.gemv_K : std::max(std::max(P.d, P.lkv * P.hd), P.lf);
+  raw_need = (raw_need + 3) & ~3;
+  // stage in place (raw input aliases xs) when every phase's quads fit in registers
+  const bool inplace = nbp_max * 16 <= MK_MAXQ * MK_CT && (size_t)4 * raw_need <= (size_t)16 * 16 * mk_xstride(nbp_max);
+  const int raw_max = inplace ? 0 : raw_need;
   P.raw_max = raw_max;
-  const size_t fixed = mk_fixed_smem(nbp_max, part_max) + (size_t)4 * raw_max + (size_t)4 * MK_MAXOWN;
-  if (P.mode == MK_MODE_STACK && (P.d + G - 1) / G > MK_MAXOWN) return IF_ERR_UNSUPPORTED;
+  const size_t fixed = mk_fixed_smem(nbp_max, part_max) + (size_t)4 * raw_max + (size_t)4 * MK_MAXOWN + 128 +
+                       (size_t)4 * MK_MAXG;
+  if (P.mode == MK_MODE_STACK && ((P.d + G - 1) / G > MK_MAXOWN || G > MK_MAXG || P.nqkv % 4 || P.d % 4 ||
+                                  P.hd % 2))
+    return IF_ERR_UNSUPPORTED;
   const size_t budget = 227 * 1024;
   if (fixed + 2 * (size_t)MK_SLOT > budget) return IF_ERR_UNSUPPORTED;
   int nslot = (int)((budget - fixed) / MK_SLOT);

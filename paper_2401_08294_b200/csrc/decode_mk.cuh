@@ -19,6 +19,12 @@ struct MkParams {
   float* act;       // [lf] silu(g)*u, written by the gate/up epilogue
   float* last_qkv;  // nullable
   int* done;        // [4*layers] grid-wide phase counters, zeroed before launch
+  // phase inputs pre-transformed by the producing epilogues (xs layout, float4
+  // [16][xstride]) and the per-CTA sum-h^2 partials for RMSNorm
+  float4* xs_h;
+  float4* xs_ctx;
+  float4* xs_act;
+  float* ssq;
   // standalone GEMV (MK_MODE_GEMV): y (+)= W x
   const float* x_in;
   float* y_out;

@@ -6,6 +6,8 @@
 // through comm.cu.
 #include <cuda_bf16.h>
 
+#include <algorithm>
+
 #include "comm.cuh"
 #include "common.cuh"
 #include "decode_mk.cuh"
@@ -111,6 +113,7 @@ struct WS {
   float* act;
   float* part;
   int* done;
+  float* xsimg;  // 3 transformed-input images + sum-h^2 partials (decode engine)
   size_t bytes;
 };
 
@@ -130,6 +133,9 @@ static WS carve(void* base, const Local& L, int64_t T) {
   w.act = take((size_t)T * L.lf);
   w.part = take((size_t)T * L.d);
   w.done = reinterpret_cast<int*>(take((size_t)4 * L.layers));
+  // 3 images of 16 x xstride float4 (xstride <= nbp_max + 9) + 256 floats
+  const size_t nbp_max = (size_t)((std::max(std::max(L.d, L.nq), L.lf) / 64 + 31) / 32) * 32;
+  w.xsimg = take(3 * 16 * (nbp_max + 16) * 4 + 256);
   w.bytes = off;
   return w;
 }
@@ -200,6 +206,14 @@ extern "C" if_status if_run_stack(const if_stack_shape* shape, const if_plan* pl
     P.act = w.act;
     P.last_qkv = last_qkv;
     P.done = w.done;
+    {
+      const int nbp_max = ((std::max(std::max(L.d, L.nq), L.lf) / 64 + 31) / 32) * 32;
+      const size_t img = (size_t)16 * (nbp_max + 16);
+      P.xs_h = reinterpret_cast<float4*>(w.xsimg);
+      P.xs_ctx = P.xs_h + img;
+      P.xs_act = P.xs_ctx + img;
+      P.ssq = reinterpret_cast<float*>(P.xs_act + img);
+    }
     P.dbg = g_mk_dbg;
     for (int l = 0; l < nlayers; l++) {
       const if_layer_weights& Wl = stage_layers[l];

@@ -55,12 +55,12 @@ L.ifx_set_mk_debug(None)
 d = dbg.view(G, nph, 8).cpu().numpy().astype(np.float64)
 t0 = d[:, 0, 0].min()
 d = (d - t0) / 1e3  # us
-names = ["start", "dep_ok", "x_ready", "staged", "units_done", "signalled", "combined"]
+names = ["start", "dep_ok", "x_ready", "staged", "units_done", "signalled", "st_bar", "st_loaded"]
 print(f"== {' '.join(sys.argv[1:])}")
 for p in range(min(nph, 12)):
     row = []
-    for k in [0, 1, 2, 3, 4, 6, 5]:
+    for k in [0, 1, 2, 7, 6, 3, 4, 5]:
         col = d[:, p, k]
-        row.append(f"{names[k]} {col.min():7.2f}/{np.median(col):7.2f}/{col.max():7.2f}")
+        row.append(f"{names[k]} {np.median(col):7.2f}")
     print(f"phase {p:3d}: " + " | ".join(row))
 print("total span (us):", d[:, -1, 5].max())
