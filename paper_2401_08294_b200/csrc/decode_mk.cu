@@ -379,6 +379,7 @@ __global__ void __launch_bounds__(MK_THREADS, 1) decode_mk_kernel(const __grid_c
   const int cw = warp - 1;
   const Q3HConst kc = q3h_const();
   uint32_t slot = 0, round = 0;  // ring position (same sequence as the producer)
+  uint32_t xuse = 0;              // completed phases of the input-copy barrier
   if (stack) {
     // residual rows of this CTA (the o/down row split) from the stage input
     const Geo go = phase_geo(P.d, P.nq, G, cta, unit);
@@ -412,7 +413,8 @@ __global__ void __launch_bounds__(MK_THREADS, 1) decode_mk_kernel(const __grid_c
           bulk_g2s(xs + jj * xstride, img + jj * xstride, row_bytes, xbar, 0ull, false);
         if (rms) bulk_g2s(ssq_s, P.ssq, ssq_bytes, xbar, 0ull, false);
       }
-      mbar_wait(xbar, p & 1);
+      mbar_wait(xbar, xuse & 1);
+      xuse++;
       if (dbg && ct == 0) dbg[2] = gtimer();
       // block sums of x from the image: x_e + x_o = xe' + 12 x_o
       for (int b = ct; b < g.nbp; b += MK_CT) {
@@ -445,7 +447,8 @@ __global__ void __launch_bounds__(MK_THREADS, 1) decode_mk_kernel(const __grid_c
         mbar_arrive_expect_tx(xbar, (uint32_t)K * 4u);
         bulk_g2s(raw, src, (uint32_t)K * 4u, xbar, 0ull, false);
       }
-      mbar_wait(xbar, p & 1);
+      mbar_wait(xbar, xuse & 1);
+      xuse++;
       if (dbg && ct == 0) dbg[2] = gtimer();
       const float4* raw4 = reinterpret_cast<const float4*>(raw);
       const int nq = K >> 2, nqp = g.nbp * 16;
