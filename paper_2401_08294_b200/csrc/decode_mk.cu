@@ -46,9 +46,16 @@ constexpr int MK_RMAX = IFB_MK_RMAX;        // rows per unit (x reuse)
 constexpr int MK_THREADS = (MK_NC + 1) * 32;  // + producer warp
 constexpr int MK_SLOT = 24 * 1024;          // ring slot bytes
 constexpr int MK_MAXSLOT = 8;
+#ifndef IFB_MK_INFLIGHT
+#define IFB_MK_INFLIGHT 3
+#endif
+// slots the producer keeps in flight (issued, not landed).  Landed slots still
+// fill the whole ring; bounding the bytes in flight bounds the queueing delay
+// every other L2 access of this SM (the phase images, the tags) sees behind
+// the weight stream (Little's law: ~3 slots cover the unloaded HBM latency).
+constexpr int MK_INFLIGHT = IFB_MK_INFLIGHT;
 constexpr int MK_CT = MK_NC * 32;           // consumer threads
 constexpr int MK_MAXOWN = 256;              // residual rows owned by one CTA
-constexpr int MK_MAXG = 160;                // >= CTAs in the grid (sum-h^2 partials)
 
 struct Geo {
   int N, K, nb, nchunk, nbp, row_bytes, r0, r1, rps, R;
@@ -299,14 +306,64 @@ __device__ __forceinline__ unsigned long long gtimer() {
   return t;
 }
 
+// ---- phase images: readiness carried by the data itself ------------------------
+// A phase's input vector is written by the previous phase's epilogues, each CTA
+// its own rows, straight into a global "image" in the transformed quad layout of
+// stage_quad.  Every stored float carries the image version's parity in its
+// mantissa LSB (stripped by the reader: values do not depend on it), and the
+// stores are single-copy-atomic 32-bit words, so a reader that sees the
+// expected parity in a word sees that word's final value.  The writer needs no
+// fence: after its epilogue it bumps a relaxed per-phase counter; a reader waits
+// for the counter (every CTA past the phase = every CTA done reading the
+// previous version: 1-bit parity cannot alias), bulk-copies the image and
+// re-reads (ld.relaxed.gpu, L1 bypassed) the rare word whose store had not
+// landed yet.
+__device__ __forceinline__ float4 ld_relaxed_f4(const float4* p) {
+  float4 v;
+  asm volatile("ld.relaxed.gpu.global.v4.f32 {%0,%1,%2,%3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "l"(p)
+               : "memory");
+  return v;
+}
+__device__ __forceinline__ uint32_t ld_relaxed_u32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed_u32(void* p, uint32_t v) {
+  asm volatile("st.relaxed.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+// value with its mantissa LSB replaced by the image parity
+__device__ __forceinline__ uint32_t tagp(float v, uint32_t par) { return (__float_as_uint(v) & ~1u) | par; }
+__device__ __forceinline__ bool par4_ok(float4 v, uint32_t par) {
+  return (((__float_as_uint(v.x) ^ par) | (__float_as_uint(v.y) ^ par) | (__float_as_uint(v.z) ^ par) |
+           (__float_as_uint(v.w) ^ par)) & 1u) == 0u;
+}
+// a wait that never ends is a bug (or a workspace that was not zero-filled):
+// trap after ~2 s instead of hanging the GPU
+struct SpinGuard {
+  uint32_t n = 0;
+  unsigned long long t0 = 0;
+  __device__ __forceinline__ void tick() {
+    if ((++n & 255u) == 0u) {
+      const unsigned long long t = gtimer();
+      if (n == 256u) t0 = t;
+      else if (t - t0 > 2000000000ull) __trap();
+    }
+  }
+};
+
 // Write the transformed pair (x_e, x_o) of element k (k even) of a phase input
-// into a global xs image with the shared-memory layout of stage_quad.
-__device__ __forceinline__ void put_pair(float4* xsg, int xstride, const int* pos, int k, float xe, float xo) {
+// into a global image with the shared-memory layout of stage_quad, tagged with
+// the image parity.
+__device__ __forceinline__ void put_pair(float4* xsg, int xstride, const int* pos, int k, float xe, float xo,
+                                         uint32_t par) {
   const int b = k >> 6, j = (k >> 1) & 31, jj = j >> 1, comp = j & 1;
   float* f = reinterpret_cast<float*>(xsg + jj * xstride + b);
   const float cj = __uint_as_float((uint32_t)(127 + 85 - pos[j]) << 23);  // 2^(85 - s_j)
-  f[comp] = xo * cj;
-  f[2 + comp] = fmaf(-11.0f, xo, xe) * 38685626227668133590597632.0f;  // * 2^85
+  st_relaxed_u32(f + comp, tagp(xo * cj, par));
+  st_relaxed_u32(f + 2 + comp, tagp(fmaf(-11.0f, xo, xe) * 38685626227668133590597632.0f, par));  // * 2^85
 }
 
 template <int XS>
@@ -352,7 +409,7 @@ __global__ void __launch_bounds__(MK_THREADS, 1) decode_mk_kernel(const __grid_c
     if (lane == 0) {
 #endif
       const uint64_t pol = policy_evict_first();
-      uint32_t slot = 0, round = 0;
+      uint32_t slot = 0, round = 0, seq = 0;
       for (int p = 0; p < nphase; p++) {
         const uint8_t* W;
         int N, K, kind;
@@ -361,7 +418,12 @@ __global__ void __launch_bounds__(MK_THREADS, 1) decode_mk_kernel(const __grid_c
         for (int r = g.r0; r < g.r1; r += g.rps) {
           const int n = min(g.rps, g.r1 - r);
           const uint32_t bytes = (uint32_t)n * g.row_bytes;
-          mbar_wait(&empty[slot], (round & 1) ^ 1);
+          if (MK_INFLIGHT < nslot && seq >= (uint32_t)MK_INFLIGHT) {
+            const uint32_t q = seq - MK_INFLIGHT;  // the copy MK_INFLIGHT issues ago must have landed
+            mbar_wait_sleep(&full[q % (uint32_t)nslot], (q / (uint32_t)nslot) & 1);
+          }
+          seq++;
+          mbar_wait_sleep(&empty[slot], (round & 1) ^ 1);
           mbar_arrive_expect_tx(&full[slot], bytes);
           bulk_g2s(ring + (size_t)slot * MK_SLOT, W + (size_t)r * g.row_bytes, bytes, &full[slot], pol);
           if (++slot == (uint32_t)nslot) {
@@ -380,6 +442,10 @@ __global__ void __launch_bounds__(MK_THREADS, 1) decode_mk_kernel(const __grid_c
   const Q3HConst kc = q3h_const();
   uint32_t slot = 0, round = 0;  // ring position (same sequence as the producer)
   uint32_t xuse = 0;              // completed phases of the input-copy barrier
+  // image versions of this launch (decode_mk.cuh): ctx/act are written once per
+  // layer, h (and the sum-h^2 partials) twice; version 0 = the zero-filled workspace
+  const uint32_t ep = stack ? ld_relaxed_u32(P.epoch) : 0u;
+  const uint32_t L2 = 2u * (uint32_t)P.layers;
   if (stack) {
     // residual rows of this CTA (the o/down row split) from the stage input
     const Geo go = phase_geo(P.d, P.nq, G, cta, unit);
@@ -391,52 +457,96 @@ __global__ void __launch_bounds__(MK_THREADS, 1) decode_mk_kernel(const __grid_c
     phase_dims(P, p, &W, &N, &K, &kind);
     const Geo g = phase_geo(N, K, G, cta, unit);
     (void)W;
-    unsigned long long* dbg = P.dbg ? P.dbg + ((size_t)cta * nphase + p) * 8 : nullptr;
-    if (dbg && ct == 0) dbg[0] = gtimer();
+    unsigned long long* dbg = P.dbg ? P.dbg + ((size_t)cta * nphase + p) * 16 : nullptr;
+    if (dbg && ct == 0) { dbg[0] = gtimer(); dbg[8] = clock64(); }
     // Phase input.  Producers (the previous phase's epilogues) already wrote it in
     // the transformed quad layout into a global xs image: one dependency wait, then
     // 16 bulk copies (one per quad row JJ) + the sum-h^2 partials for RMSNorm.
     // The first phase (plain h) and the standalone GEMV stage from raw instead.
     const bool from_image = stack && p > 0;
     const bool rms = kind == 0 || kind == 2;
+    const uint32_t l = (uint32_t)(p >> 2);
     float out_scale = 1.f;  // RMSNorm folded into the output: W (s h) = s (W h)
     if (from_image) {
-      const float4* img = kind == 1 ? P.xs_ctx : (kind == 3 ? P.xs_act : P.xs_h);
-      const uint32_t row_bytes = (uint32_t)g.nbp * 16u;
-      const uint32_t ssq_bytes = rms ? (uint32_t)((G + 3) & ~3) * 4u : 0u;
+      // input image of this phase and the version its writers tag it with
+      const float4* img;
+      uint32_t ver;
+      if (kind == 1) {
+        img = P.xs_ctx, ver = ep * (uint32_t)P.layers + l + 1u;
+      } else if (kind == 3) {
+        img = P.xs_act, ver = ep * (uint32_t)P.layers + l + 1u;
+      } else {
+        img = P.xs_h, ver = ep * L2 + 2u * l + (kind == 2 ? 1u : 0u);  // kind 0: down of layer l-1
+      }
+      const uint32_t par = ver & 1u;
+      // 1. one thread waits until every CTA has finished the previous phase (a
+      //    relaxed counter: no fence on either side -- the data carries its own
+      //    readiness) and copies the whole image (all 16 quad rows, padding
+      //    blocks included: never written, zero) into xs with the TMA engine
       if (ct == 0) {
-        while (ld_acquire_gpu(&P.done[p - 1]) < G) __nanosleep(20);
-        if (dbg) dbg[1] = gtimer();
-        asm volatile("fence.proxy.async.global;" ::: "memory");  // generic writes -> async-proxy reads
-        mbar_arrive_expect_tx(xbar, 16u * row_bytes + ssq_bytes);
-        for (int jj = 0; jj < 16; jj++)
-          bulk_g2s(xs + jj * xstride, img + jj * xstride, row_bytes, xbar, 0ull, false);
-        if (rms) bulk_g2s(ssq_s, P.ssq, ssq_bytes, xbar, 0ull, false);
+        SpinGuard sg;
+        const int target = (int)((ep + 1u) * (uint32_t)G);
+        while ((int)ld_relaxed_u32(reinterpret_cast<const uint32_t*>(P.done + p - 1)) - target < 0) {
+          __nanosleep(20);
+          sg.tick();
+        }
+        if (dbg) { dbg[1] = gtimer(); dbg[9] = clock64(); }
+        const uint32_t row_bytes = (uint32_t)g.nbp * 16u;
+        mbar_arrive_expect_tx(xbar, 16u * row_bytes);
+        for (int jj = 0; jj < 16; jj++) bulk_g2s(xs + jj * xstride, img + jj * xstride, row_bytes, xbar, 0ull, false);
+      }
+      // 2. the sum-h^2 partials (fixed order: deterministic)
+      if (rms && cw == MK_NC - 1) {
+        SpinGuard sg;
+        float t = 0.f;
+        for (int c = lane; c < G; c += 32) {
+          uint32_t v = ld_relaxed_u32(reinterpret_cast<const uint32_t*>(P.ssq) + c);
+          while ((v ^ par) & 1u) {
+            __nanosleep(20);
+            sg.tick();
+            v = ld_relaxed_u32(reinterpret_cast<const uint32_t*>(P.ssq) + c);
+          }
+          t += __uint_as_float(v & ~1u);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+        if (lane == 0) red[16] = t;
       }
       mbar_wait(xbar, xuse & 1);
       xuse++;
-      if (dbg && ct == 0) dbg[2] = gtimer();
-      // block sums of x from the image: x_e + x_o = xe' + 12 x_o
-      for (int b = ct; b < g.nbp; b += MK_CT) {
+      if (dbg && ct == 0) { dbg[6] = gtimer(); dbg[14] = clock64(); }
+      // 3. one thread per block b: its 16 quads -- check every word's parity
+      //    (re-read the rare late one from L2), strip it, and form the block sum
+      //    of x (x_e + x_o = xe' + 12 x_o in transformed terms)
+      for (int b = ct; b < g.nb; b += MK_CT) {
+        float4 v[16];
+#pragma unroll
+        for (int jj = 0; jj < 16; jj++) v[jj] = xs[jj * xstride + b];
         float sx = 0.f;
-#pragma unroll 4
+#pragma unroll
         for (int jj = 0; jj < 16; jj++) {
-          const float4 v = xs[jj * xstride + b];
-          const float c0 = __uint_as_float((uint32_t)(127 - 85 + pos[2 * jj]) << 23);  // 2^(s - 85)
-          const float c1 = __uint_as_float((uint32_t)(127 - 85 + pos[2 * jj + 1]) << 23);
-          sx += (v.z + v.w) * 2.5849394142282115e-26f + 12.0f * (v.x * c0 + v.y * c1);  // 2^-85
+          if (!par4_ok(v[jj], par)) {
+            SpinGuard sg;
+            do {
+              if (dbg) atomicAdd(reinterpret_cast<unsigned long long*>(dbg + 7), 1ull);
+              sg.tick();
+              v[jj] = ld_relaxed_f4(img + jj * xstride + b);
+            } while (!par4_ok(v[jj], par));
+          }
+          const float4 w = make_float4(__uint_as_float(__float_as_uint(v[jj].x) & ~1u),
+                                       __uint_as_float(__float_as_uint(v[jj].y) & ~1u),
+                                       __uint_as_float(__float_as_uint(v[jj].z) & ~1u),
+                                       __uint_as_float(__float_as_uint(v[jj].w) & ~1u));
+          xs[jj * xstride + b] = w;
+          constexpr float kS85 = 2.5849394142282115e-26f;  // 2^-85
+          const float c0 = __uint_as_float((uint32_t)(127 - 85 + kQ3hSrc[2 * jj].pos) << 23);  // 2^(s - 85)
+          const float c1 = __uint_as_float((uint32_t)(127 - 85 + kQ3hSrc[2 * jj + 1].pos) << 23);
+          sx += (w.z + w.w) * kS85 + 12.0f * (w.x * c0 + w.y * c1);
         }
         bs[b] = make_float2(sx, 0.f);
       }
-      if (rms) {
-        if (cw == 0) {
-          float t = 0.f;
-          for (int c = lane; c < G; c += 32) t += ssq_s[c];
-#pragma unroll
-          for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
-          if (lane == 0) red[16] = t;
-        }
-      }
+      for (int b = g.nb + ct; b < g.nbp; b += MK_CT) bs[b] = make_float2(0.f, 0.f);
+      if (dbg && ct == 0) { dbg[2] = gtimer(); dbg[10] = clock64(); }
       named_bar_sync(1, MK_CT);
       if (rms) out_scale = 1.0f / sqrtf(red[16] / (float)K + 1e-5f);
     } else {
@@ -449,7 +559,7 @@ __global__ void __launch_bounds__(MK_THREADS, 1) decode_mk_kernel(const __grid_c
       }
       mbar_wait(xbar, xuse & 1);
       xuse++;
-      if (dbg && ct == 0) dbg[2] = gtimer();
+      if (dbg && ct == 0) { dbg[2] = gtimer(); dbg[10] = clock64(); }
       const float4* raw4 = reinterpret_cast<const float4*>(raw);
       const int nq = K >> 2, nqp = g.nbp * 16;
       float inv = 1.f;
@@ -508,7 +618,7 @@ __global__ void __launch_bounds__(MK_THREADS, 1) decode_mk_kernel(const __grid_c
       }
       named_bar_sync(1, MK_CT);
     }
-    if (dbg && ct == 0) dbg[3] = gtimer();
+    if (dbg && ct == 0) { dbg[3] = gtimer(); dbg[11] = clock64(); }
     // ---- 3. stream this CTA's rows from the ring.  Every consumer warp visits
     //         every slot (wait full -> its units -> arrive empty, count NC);
     //         the units (R rows x one chunk) of consecutive slots are dealt
@@ -522,7 +632,7 @@ __global__ void __launch_bounds__(MK_THREADS, 1) decode_mk_kernel(const __grid_c
       int u0 = cw;                                 // first unit of this warp in slot sl
       for (int sl = 0; sl < nslots; sl++) {
 #ifndef IFB_MK_NOWAIT
-        mbar_wait(&full[slot], round & 1);
+        mbar_wait_sleep(&full[slot], round & 1);
 #endif
         const int n = min(g.rps, nrows - sl * g.rps);
         const unsigned char* sbase = ring + (size_t)slot * MK_SLOT;
@@ -555,7 +665,7 @@ __global__ void __launch_bounds__(MK_THREADS, 1) decode_mk_kernel(const __grid_c
       }
     }
     named_bar_sync(1, MK_CT);
-    if (dbg && ct == 0) dbg[4] = gtimer();
+    if (dbg && ct == 0) { dbg[4] = gtimer(); dbg[12] = clock64(); }
     // ---- 4. combine chunks (fixed order) + epilogue.  Outputs feeding the next
     //         phase are written pre-transformed (put_pair) into its xs image. ----
     const int nr = g.r1 - g.r0;
@@ -582,11 +692,12 @@ __global__ void __launch_bounds__(MK_THREADS, 1) decode_mk_kernel(const __grid_c
           u *= out_scale;
           a[h] = gg / (1.0f + expf(-gg)) * u;
         }
-        put_pair(P.xs_act, xstride, pos, (g.r0 + rr) / 2, a[0], a[1]);
+        put_pair(P.xs_act, xstride, pos, (g.r0 + rr) / 2, a[0], a[1], (ep * (uint32_t)P.layers + l + 1u) & 1u);
       }
     } else if (kind == 0) {
       const int v_off = (P.lh + P.lkv) * P.hd;
       const bool last_layer = p == nphase - 4;
+      const uint32_t vctx = ep * (uint32_t)P.layers + l + 1u;
       for (int rr = 2 * ct; rr < nr; rr += 2 * MK_CT) {
         float v2[2];
 #pragma unroll
@@ -601,11 +712,13 @@ __global__ void __launch_bounds__(MK_THREADS, 1) decode_mk_kernel(const __grid_c
           // ctx heads i whose kv group is this v head: scatter the pair
           const int ev = n - v_off, jv = ev / P.hd, e = ev - jv * P.hd;
           const int i0 = (jv + P.k0) * P.per - P.h0;
-          for (int i = max(i0, 0); i < min(i0 + P.per, P.lh); i++) put_pair(P.xs_ctx, xstride, pos, i * P.hd + e, v2[0], v2[1]);
+          for (int i = max(i0, 0); i < min(i0 + P.per, P.lh); i++)
+            put_pair(P.xs_ctx, xstride, pos, i * P.hd + e, v2[0], v2[1], vctx & 1u);
         }
       }
     } else {
       // o / down: residual on the rows this CTA owns; sum h^2 partial for RMSNorm
+      const uint32_t vh = ep * L2 + 2u * l + (kind == 1 ? 1u : 2u);
       float ss = 0.f;
       for (int rr = 2 * ct; rr < nr; rr += 2 * MK_CT) {
         float hn[2];
@@ -618,7 +731,7 @@ __global__ void __launch_bounds__(MK_THREADS, 1) decode_mk_kernel(const __grid_c
           ss = fmaf(hn[h], hn[h], ss);
           if (p == nphase - 1) P.h[g.r0 + rr + h] = hn[h];  // stage output
         }
-        put_pair(P.xs_h, xstride, pos, g.r0 + rr, hn[0], hn[1]);
+        put_pair(P.xs_h, xstride, pos, g.r0 + rr, hn[0], hn[1], vh & 1u);
       }
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
@@ -628,17 +741,18 @@ __global__ void __launch_bounds__(MK_THREADS, 1) decode_mk_kernel(const __grid_c
         float t = 0.f;
 #pragma unroll
         for (int w = 0; w < MK_NC; w++) t += red[w];
-        P.ssq[cta] = t;
+        st_relaxed_u32(P.ssq + cta, tagp(t, vh & 1u));
       }
     }
-    if (p + 1 < nphase) {
-      // bar.sync orders every consumer's output stores before thread 0's
-      // gpu-scope release (cumulativity); readers acquire the counter.
-      named_bar_sync(1, MK_CT);
-      if (ct == 0) red_release_gpu_add(&P.done[p], 1);
-    }
-    if (dbg && ct == 0) dbg[5] = gtimer();
+    // signal "finished reading this phase's input, outputs issued": a relaxed
+    // add, no fence -- readers check every word's parity anyway (the rare late
+    // word is re-read).  Counters grow by G per launch (no reset).
+    if (stack && p + 1 < nphase && ct == 0) red_relaxed_gpu_add(P.done + p, 1);
+    if (dbg && ct == 0) { dbg[5] = gtimer(); dbg[13] = clock64(); }
   }
+  // every CTA read the epoch before writing its first image (which CTA 0's last
+  // phase has consumed), so the next launch may see the new one
+  if (stack && cta == 0 && ct == 0) st_relaxed_u32(P.epoch, ep + 1u);
 }
 
 // ---------------------------------------------------------------------------

@@ -8,6 +8,7 @@
 namespace ifb {
 
 constexpr int MK_MAXL = 128;  // layers per stage handled by one launch
+constexpr int MK_MAXG = 160;  // >= CTAs in the grid (one per SM)
 enum { MK_MODE_STACK = 0, MK_MODE_GEMV = 1 };
 
 struct MkParams {
@@ -18,7 +19,11 @@ struct MkParams {
   float* qkv;       // [nqkv]
   float* act;       // [lf] silu(g)*u, written by the gate/up epilogue
   float* last_qkv;  // nullable
-  int* done;        // [4*layers] grid-wide phase counters, zeroed before launch
+  // Phase dependencies without fences (see decode_mk.cu, "images"): done[p]
+  // counts CTAs past phase p over all launches (G per launch), epoch = completed
+  // launches.  Both live in the caller's workspace, zero-filled once before use.
+  int* done;  // [4 * MK_MAXL]
+  uint32_t* epoch;
   // phase inputs pre-transformed by the producing epilogues (xs layout, float4
   // [16][xstride]) and the per-CTA sum-h^2 partials for RMSNorm
   float4* xs_h;

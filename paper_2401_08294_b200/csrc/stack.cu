@@ -112,7 +112,7 @@ struct WS {
   float* gu;
   float* act;
   float* part;
-  int* done;
+  int* done;  // decode engine: phase counters [4 * MK_MAXL] + epoch
   float* xsimg;  // 3 transformed-input images + sum-h^2 partials (decode engine)
   size_t bytes;
 };
@@ -132,7 +132,7 @@ static WS carve(void* base, const Local& L, int64_t T) {
   w.gu = take((size_t)T * 2 * L.lf);
   w.act = take((size_t)T * L.lf);
   w.part = take((size_t)T * L.d);
-  w.done = reinterpret_cast<int*>(take((size_t)4 * L.layers));
+  w.done = reinterpret_cast<int*>(take((size_t)4 * MK_MAXL + 32));
   // 3 images of 16 x xstride float4 (xstride <= nbp_max + 9) + 256 floats
   const size_t nbp_max = (size_t)((std::max(std::max(L.d, L.nq), L.lf) / 64 + 31) / 32) * 32;
   w.xsimg = take(3 * 16 * (nbp_max + 16) * 4 + 256);
@@ -206,6 +206,7 @@ extern "C" if_status if_run_stack(const if_stack_shape* shape, const if_plan* pl
     P.act = w.act;
     P.last_qkv = last_qkv;
     P.done = w.done;
+    P.epoch = reinterpret_cast<uint32_t*>(w.done + 4 * MK_MAXL);
     {
       const int nbp_max = ((std::max(std::max(L.d, L.nq), L.lf) / 64 + 31) / 32) * 32;
       const size_t img = (size_t)16 * (nbp_max + 16);
@@ -223,7 +224,6 @@ extern "C" if_status if_run_stack(const if_stack_shape* shape, const if_plan* pl
       P.w[l][2] = Wl.wgu;
       P.w[l][3] = Wl.wdown;
     }
-    if (cudaMemsetAsync(w.done, 0, sizeof(int) * 4 * nlayers, cs) != cudaSuccess) return check_launch("if_run_stack: memset");
     st = mk_launch(P, cs);
     if (st != IF_ERR_UNSUPPORTED) {
       if (st) return st;
