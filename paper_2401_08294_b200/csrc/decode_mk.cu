@@ -539,8 +539,8 @@ __global__ void __launch_bounds__(MK_THREADS, 1) decode_mk_kernel(const __grid_c
                                        __uint_as_float(__float_as_uint(v[jj].w) & ~1u));
           xs[jj * xstride + b] = w;
           constexpr float kS85 = 2.5849394142282115e-26f;  // 2^-85
-          const float c0 = __uint_as_float((uint32_t)(127 - 85 + kQ3hSrc[2 * jj].pos) << 23);  // 2^(s - 85)
-          const float c1 = __uint_as_float((uint32_t)(127 - 85 + kQ3hSrc[2 * jj + 1].pos) << 23);
+          const float c0 = __uint_as_float((uint32_t)(127 - 85 + pos[2 * jj]) << 23);  // 2^(s - 85)
+          const float c1 = __uint_as_float((uint32_t)(127 - 85 + pos[2 * jj + 1]) << 23);
           sx += (w.z + w.w) * kS85 + 12.0f * (w.x * c0 + w.y * c1);
         }
         bs[b] = make_float2(sx, 0.f);

@@ -3,7 +3,7 @@
 #include <cstdio>
 #include "../../paper_2401_08294_b200/csrc/decode_mk.cu"
 
-template <int R, int NW>
+template <int R, int NW, int SYNC>
 __global__ void __launch_bounds__(NW * 32, 1) unit_bench(float* out, int iters) {
   extern __shared__ __align__(1024) unsigned char sm[];
   unsigned char* ring = sm;                       // 32 KB of rows
@@ -22,14 +22,15 @@ __global__ void __launch_bounds__(NW * 32, 1) unit_bench(float* out, int iters) 
     const int uu = u % units;
     const int grp = uu / 2, c = uu % 2;
     ifb::mk_unit<R, 73, true>(ring + grp * R * 2048, 2048, R, c, 64, 73, xs, bs, part + (w & 7) * 64, 2, kc);
+    if (SYNC && (it % SYNC) == SYNC - 1) __syncthreads();  // waves: every warp starts together
   }
   __syncthreads();
   if (threadIdx.x == 0) out[blockIdx.x] = part[0];
 }
 
-template <int R, int NW>
+template <int R, int NW, int SYNC = 0>
 void run(float* out) {
-  auto k = unit_bench<R, NW>;
+  auto k = unit_bench<R, NW, SYNC>;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
   int iters = 2000;
   k<<<148, NW * 32, 64 * 1024>>>(out, 10);
@@ -41,13 +42,13 @@ void run(float* out) {
   cudaEventSynchronize(b);
   float ms; cudaEventElapsedTime(&ms, a, b);
   double weights = 148.0 * NW * iters * R * 32 * 64;
-  printf("R=%d warps=%2d: %.3f ms  %.1f weights/clk/SM (@1.965GHz)  = %.0f GB/s Q3H-equivalent  err=%s\n", R, NW, ms,
+  printf("sync=%d R=%d warps=%2d: %.3f ms  %.1f weights/clk/SM (@1.965GHz)  = %.0f GB/s Q3H-equivalent  err=%s\n", SYNC, R, NW, ms,
          weights / 148 / (ms * 1e-3 * 1.965e9), weights * 0.5 / (ms * 1e-3) / 1e9, cudaGetErrorString(cudaGetLastError()));
 }
 
 int main() {
   float* out;
   cudaMalloc(&out, 148 * 4);
-  run<4, 8>(out); run<4, 12>(out); run<4, 16>(out); run<8, 8>(out); run<8, 12>(out); run<2, 16>(out);
+  run<4, 16>(out); run<4, 16, 1>(out); run<4, 16, 3>(out); run<4, 15, 1>(out); run<8, 12>(out); run<8, 12, 1>(out);
   return 0;
 }
