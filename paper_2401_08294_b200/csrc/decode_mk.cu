@@ -515,37 +515,40 @@ __global__ void __launch_bounds__(MK_THREADS, 1) decode_mk_kernel(const __grid_c
       mbar_wait(xbar, xuse & 1);
       xuse++;
       if (dbg && ct == 0) { dbg[6] = gtimer(); dbg[14] = clock64(); }
-      // 3. one thread per block b: its 16 quads -- check every word's parity
+      // 3. four threads per block b, four quads each: check every word's parity
       //    (re-read the rare late one from L2), strip it, and form the block sum
       //    of x (x_e + x_o = xe' + 12 x_o in transformed terms)
-      for (int b = ct; b < g.nb; b += MK_CT) {
-        float4 v[16];
-#pragma unroll
-        for (int jj = 0; jj < 16; jj++) v[jj] = xs[jj * xstride + b];
+      for (int t0 = cw * 32; t0 < 4 * g.nbp; t0 += MK_CT) {
+        const int t = t0 + lane, b = t >> 2, j4 = t & 3;
         float sx = 0.f;
+        if (b < g.nb) {
+          float4 v[4];
 #pragma unroll
-        for (int jj = 0; jj < 16; jj++) {
-          if (!par4_ok(v[jj], par)) {
-            SpinGuard sg;
-            do {
-              if (dbg) atomicAdd(reinterpret_cast<unsigned long long*>(dbg + 7), 1ull);
-              sg.tick();
-              v[jj] = ld_relaxed_f4(img + jj * xstride + b);
-            } while (!par4_ok(v[jj], par));
+          for (int i = 0; i < 4; i++) v[i] = xs[(4 * j4 + i) * xstride + b];
+#pragma unroll
+          for (int i = 0; i < 4; i++) {
+            const int jj = 4 * j4 + i;
+            float4 q = v[i];
+            if (!par4_ok(q, par)) {
+              SpinGuard sg;
+              do {
+                if (dbg) atomicAdd(reinterpret_cast<unsigned long long*>(dbg + 7), 1ull);
+                sg.tick();
+                q = ld_relaxed_f4(img + jj * xstride + b);
+              } while (!par4_ok(q, par));
+            }
+            const float4 w = make_float4(__uint_as_float(__float_as_uint(q.x) & ~1u), __uint_as_float(__float_as_uint(q.y) & ~1u),
+                                         __uint_as_float(__float_as_uint(q.z) & ~1u), __uint_as_float(__float_as_uint(q.w) & ~1u));
+            xs[jj * xstride + b] = w;
+            const float c0 = __uint_as_float((uint32_t)(127 - 85 + pos[2 * jj]) << 23);  // 2^(s - 85)
+            const float c1 = __uint_as_float((uint32_t)(127 - 85 + pos[2 * jj + 1]) << 23);
+            sx += (w.z + w.w) * 2.5849394142282115e-26f + 12.0f * (w.x * c0 + w.y * c1);
           }
-          const float4 w = make_float4(__uint_as_float(__float_as_uint(v[jj].x) & ~1u),
-                                       __uint_as_float(__float_as_uint(v[jj].y) & ~1u),
-                                       __uint_as_float(__float_as_uint(v[jj].z) & ~1u),
-                                       __uint_as_float(__float_as_uint(v[jj].w) & ~1u));
-          xs[jj * xstride + b] = w;
-          constexpr float kS85 = 2.5849394142282115e-26f;  // 2^-85
-          const float c0 = __uint_as_float((uint32_t)(127 - 85 + pos[2 * jj]) << 23);  // 2^(s - 85)
-          const float c1 = __uint_as_float((uint32_t)(127 - 85 + pos[2 * jj + 1]) << 23);
-          sx += (w.z + w.w) * kS85 + 12.0f * (w.x * c0 + w.y * c1);
         }
-        bs[b] = make_float2(sx, 0.f);
+        sx += __shfl_xor_sync(0xffffffffu, sx, 1);
+        sx += __shfl_xor_sync(0xffffffffu, sx, 2);
+        if (j4 == 0 && b < g.nbp) bs[b] = make_float2(sx, 0.f);
       }
-      for (int b = g.nb + ct; b < g.nbp; b += MK_CT) bs[b] = make_float2(0.f, 0.f);
       if (dbg && ct == 0) { dbg[2] = gtimer(); dbg[10] = clock64(); }
       named_bar_sync(1, MK_CT);
       if (rms) out_scale = 1.0f / sqrtf(red[16] / (float)K + 1e-5f);
