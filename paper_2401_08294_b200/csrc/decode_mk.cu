@@ -36,7 +36,7 @@
 namespace ifb {
 
 #ifndef IFB_MK_NC
-#define IFB_MK_NC 15
+#define IFB_MK_NC 16
 #endif
 #ifndef IFB_MK_RMAX
 #define IFB_MK_RMAX 4

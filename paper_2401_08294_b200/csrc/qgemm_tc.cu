@@ -1,22 +1,30 @@
-// qgemm_tc.cu — a5: prefill GEMM with fused dequantization on the 5th-gen
-// tensor cores (tcgen05 + TMEM + TMA), P:94:
-//     Y[m, n] (+)= sum_k W'[n, k] X[m, k]       X bf16, W' -> bf16, fp32 accumulate
-//
-// CTA tile: 128 output columns (weight rows n) x 256 output rows (activations m,
-// two 128-row UMMA tiles, i.e. two 128x128 fp32 accumulators = 256 TMEM
-// columns), K in steps of 64 (one Q3H_B64 block per weight row).  Optional
-// split-K over gridDim.z (partials combined with red.global.add.v4.f32).
+// qgemm_tc.cu — fused-dequant GEMM on the 5th-gen tensor cores (tcgen05 +
+// TMEM + TMA), P:93-94:
+//     Y[m, n] (+)= sum_k W'[n, k] X[m, k]        fp32 accumulate
+// Two uses of one kernel template:
+//  * a5 prefill (DEC = false): X bf16 [M, K] by TMA (SWIZZLE_128B tensor map),
+//    W' -> bf16, two 128-row UMMA M tiles per CTA (256 TMEM columns).
+//  * a4 batched decode (DEC = true, 2 <= B <= 64): x fp32 [B, K] is split
+//    into fp16 hi + lo (x = hi + lo to ~22 bits) by a converter warp straight
+//    into the UMMA A tile (rows 0..63 hi, 64..127 lo), W' -> fp16, one M tile;
+//    the epilogue adds the lo rows to the hi rows.  Error: fp16 rounding of W'
+//    only (Q17), well inside the 1e-3 decode gate.
+// CTA tile: 128 weight rows (UMMA N) x K in steps of 64 (one Q3H_B64 block per
+// row), optional split-K over gridDim.z (partials combined with red.add).
 // Warp roles (8 warps):
-//   warp 0  TMA producer: X tiles [128 rows x 64 k] bf16, SWIZZLE_128B tensor map
-//   warp 1  TMEM allocator + single-thread tcgen05.mma issuer (kind::f16, bf16)
-//   warps 2-5  dequantizers: weight row r = thread, Eq. 2 -> bf16,
-//           written straight into the UMMA canonical K-major SW128 layout,
-//           fence.proxy.async, mbarrier arrive
+//   warp 0  X producer (TMA, or the fp32 -> fp16 hi/lo converter)
+//   warp 1  TMEM allocator + single-thread tcgen05.mma issuer (kind::f16)
+//   warps 2-5  dequantizers, one weight row per thread: the row's packed bytes
+//           for stage i + PD are prefetched with cp.async (a shared-memory
+//           ring, rows padded to an odd number of 16-byte chunks: conflict-
+//           free), Eq. 2 -> 16-bit, written straight into the UMMA
+//           canonical K-major SW128 layout, fence.proxy.async, mbarrier arrive
 //   warps 2-5  epilogue: tcgen05.ld 32x32b (TMEM lane quarter = warp % 4)
-// Pipeline: 4 stages, full barriers (A: TMA tx bytes; B: 128 dequant arrivals),
-// empty barriers armed by tcgen05.commit.
+// Pipeline: full barriers (A: TMA tx bytes or converter arrival; B: 128
+// dequant arrivals), empty barriers armed by tcgen05.commit.
 #include <cuda.h>
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 #include <cudaTypedefs.h>
 
 #include "common.cuh"
@@ -27,15 +35,30 @@ namespace ifb {
 
 constexpr int TC_BN = 128;     // weight rows per CTA (UMMA N)
 constexpr int TC_BM = 128;     // activation rows per UMMA tile (UMMA M)
-constexpr int TC_MT = 2;       // UMMA M tiles per CTA
 constexpr int TC_BK = 64;      // K per stage
-constexpr int TC_STAGES = 4;
 constexpr int TC_THREADS = 256;
 constexpr int TC_A_BYTES = TC_BM * TC_BK * 2;  // 16 KB per M tile
 constexpr int TC_B_BYTES = TC_BN * TC_BK * 2;  // 16 KB
-constexpr int TC_STAGE_BYTES = TC_MT * TC_A_BYTES + TC_B_BYTES;
-constexpr int TC_SMEM = TC_STAGES * TC_STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
-constexpr int TC_TMEM_COLS = TC_MT * TC_BN;  // 256
+constexpr int TC_PK = 8;   // packed-weight ring slots (stages of raw bytes per row)
+constexpr int TC_PD = 6;   // cp.async prefetch distance (stages)
+
+template <bool DEC>
+struct TcCfg {
+  static constexpr int MT = DEC ? 1 : 2;          // UMMA M tiles per CTA
+  static constexpr int STAGES = DEC ? 4 : 3;
+  static constexpr int STAGE_BYTES = MT * TC_A_BYTES + TC_B_BYTES;
+  static constexpr int TMEM_COLS = MT * TC_BN;
+};
+// raw bytes of one row per stage (64 weights), and the padded ring stride:
+// a multiple of 16 with an odd 16-byte chunk count (conflict-free LDS.128)
+__host__ __device__ constexpr int tc_sb(int qt, int bs) { return (TC_BK / bs) * q_block_bytes(qt, bs); }
+__host__ __device__ constexpr int tc_sbpad(int qt, int bs) {
+  return ((tc_sb(qt, bs) + 15) / 16) % 2 ? ((tc_sb(qt, bs) + 15) / 16) * 16 : ((tc_sb(qt, bs) + 15) / 16 + 1) * 16;
+}
+template <bool DEC>
+__host__ __device__ constexpr int tc_smem(int qt, int bs) {
+  return TcCfg<DEC>::STAGES * TcCfg<DEC>::STAGE_BYTES + TC_PK * TC_BN * tc_sbpad(qt, bs) + 1024 /*align*/ + 256;
+}
 
 // ---- tcgen05 / TMA PTX wrappers ----------------------------------------------
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int x, int y, uint64_t* bar) {
@@ -59,9 +82,12 @@ __device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr) {
   return d;
 }
 
-// kind::f16 instruction descriptor: D f32, A/B bf16, both K-major, M = 128, N = 128
+// kind::f16 instruction descriptor: D f32, A/B bf16 (or fp16), both K-major
 __host__ __device__ constexpr uint32_t umma_idesc_bf16(int M, int N) {
   return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+__host__ __device__ constexpr uint32_t umma_idesc_f16(int M, int N) {
+  return (1u << 4) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
 }
 
 __device__ __forceinline__ void umma_bf16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc, bool acc) {
@@ -93,24 +119,81 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float a, float b) {
   __nv_bfloat162 v = __floats2bfloat162_rn(a, b);  // .x = a (low half), .y = b
   return *reinterpret_cast<uint32_t*>(&v);
 }
+__device__ __forceinline__ uint32_t pack_f16x2(float a, float b) {
+  __half2 v = __floats2half2_rn(a, b);
+  return *reinterpret_cast<uint32_t*>(&v);
+}
+template <bool F16>
+__device__ __forceinline__ uint32_t pack16x2(float a, float b) {
+  if constexpr (F16) return pack_f16x2(a, b);
+  else return pack_bf16x2(a, b);
+}
 
-// Dequantize weight row n, weights [k0, k0 + 64), into 128 bytes of bf16 in the
-// SW128 K-major layout at row r of the B tile (zeros beyond N or K).
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async4(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+// Prefetch the SB raw bytes of weight row n for K-stage ks (64 weights) into its
+// ring row (zeros are produced later by dequant_row for rows/stages out of range).
 template <int QT, int BS>
-__device__ __forceinline__ void dequant_row(const uint8_t* __restrict__ W, int64_t nb, int64_t n, int64_t N,
-                                           int64_t k0, int64_t K, unsigned char* btile, int r) {
+__device__ __forceinline__ void prefetch_row(const uint8_t* __restrict__ W, int64_t nb, int64_t n, int64_t N,
+                                             int64_t ks, int64_t K, unsigned char* dst) {
+  constexpr int SB = tc_sb(QT, BS);
+  if (n >= N || ks * TC_BK >= K) return;
+  const uint8_t* src = W + (n * nb + ks * (TC_BK / BS)) * q_block_bytes(QT, BS);
+  if (SB % 16 == 0 && (reinterpret_cast<uintptr_t>(src) & 15u) == 0) {
+#pragma unroll
+    for (int i = 0; i < SB / 16; i++) cp_async16(dst + 16 * i, src + 16 * i);
+  } else {
+#pragma unroll
+    for (int i = 0; i < SB / 4; i++) cp_async4(dst + 4 * i, src + 4 * i);
+  }
+}
+
+// Dequantize weight row n, weights [k0, k0 + 64), from its raw bytes in the ring
+// into 128 bytes of 16-bit values in the SW128 K-major layout at row r of the
+// B tile (zeros beyond N or K).
+template <int QT, int BS, bool F16>
+__device__ __forceinline__ void dequant_row(const unsigned char* raw, int64_t n, int64_t N, int64_t k0, int64_t K,
+                                           unsigned char* btile, int r) {
   constexpr int D = q_levels(QT);
   constexpr int C = q_width(QT);
   constexpr int NC = q_ncodes(QT, BS);
   constexpr int BB = q_block_bytes(QT, BS);
   constexpr int NW = q_block_words(QT, BS);
-  uint32_t out[32];  // 64 bf16
+  constexpr int SB = tc_sb(QT, BS);
+  constexpr int SBW = (SB + 15) / 16 * 4;  // words read (whole 16-byte chunks)
+  uint32_t out[32];  // 64 16-bit values
+  if (n < N && k0 < K) {
+    uint32_t words[SBW + 1];
 #pragma unroll
-  for (int sub = 0; sub < TC_BK / BS; sub++) {
-    const int64_t kk = k0 + sub * BS;
-    if (n < N && kk < K) {
+    for (int i = 0; i < SBW / 4; i++) {
+      const uint4 v = *reinterpret_cast<const uint4*>(raw + 16 * i);
+      words[4 * i] = v.x, words[4 * i + 1] = v.y, words[4 * i + 2] = v.z, words[4 * i + 3] = v.w;
+    }
+    words[SBW] = 0u;
+#pragma unroll
+    for (int sub = 0; sub < TC_BK / BS; sub++) {
+      // block sub starts at byte sub * BB (a multiple of 2): word-aligned or a halfword in
+      const int boff = sub * BB;
       uint32_t w[NW + 1];
-      load_block_words<BB, NW>(W + (n * nb + kk / BS) * BB, w);
+#pragma unroll
+      for (int i = 0; i <= NW; i++) {
+        const int wi = boff / 4 + i;
+        const uint32_t a = wi < SBW ? words[wi] : 0u, b = wi + 1 <= SBW ? words[wi + 1] : 0u;
+        w[i] = (boff & 3) ? __funnelshift_r(a, b, 16) : a;
+      }
+      if (BB % 4) w[NW] = 0u;
+      // mask the bytes past the block (BB % 4 == 2: the last word's high half)
+      if constexpr (BB % 4 != 0) w[NW - 1] &= 0xFFFFu;
       const float lo = half_bits_to_float(w[0] & 0xFFFFu);
       const float hi = half_bits_to_float(w[0] >> 16);
       const float step = __fdiv_rn(__fsub_rn(hi, lo), (float)D);
@@ -120,19 +203,19 @@ __device__ __forceinline__ void dequant_row(const uint8_t* __restrict__ W, int64
         if constexpr (QT == 35) {
           const uint32_t q1 = (v * 187u) >> 11;  // floor(v/11) for v < 128
           const uint32_t q2 = v - 11u * q1;      // v mod 11
-          out[sub * (BS / 2) + j] = pack_bf16x2(__fmaf_rn((float)q1, step, lo), __fmaf_rn((float)q2, step, lo));
+          out[sub * (BS / 2) + j] = pack16x2<F16>(__fmaf_rn((float)q1, step, lo), __fmaf_rn((float)q2, step, lo));
         } else {
           const float wp = __fmaf_rn((float)v, step, lo);
           if (j & 1)
-            out[sub * (BS / 2) + j / 2] |= pack_bf16x2(0.f, wp) & 0xFFFF0000u;
+            out[sub * (BS / 2) + j / 2] |= pack16x2<F16>(0.f, wp) & 0xFFFF0000u;
           else
-            out[sub * (BS / 2) + j / 2] = pack_bf16x2(wp, 0.f) & 0x0000FFFFu;
+            out[sub * (BS / 2) + j / 2] = pack16x2<F16>(wp, 0.f) & 0x0000FFFFu;
         }
       }
-    } else {
-#pragma unroll
-      for (int j = 0; j < BS / 2; j++) out[sub * (BS / 2) + j] = 0u;
     }
+  } else {
+#pragma unroll
+    for (int j = 0; j < 32; j++) out[j] = 0u;
   }
   // 8 chunks of 16 B; chunk c of row r lives at chunk (c ^ (r % 8)) of the row (SW128)
   unsigned char* rowp = btile + (r >> 3) * 1024 + (r & 7) * 128;
@@ -143,39 +226,105 @@ __device__ __forceinline__ void dequant_row(const uint8_t* __restrict__ W, int64
   }
 }
 
-template <int QT, int BS>
+// Decode mode: x fp32 [B, K] -> fp16 hi (rows 0..63) + lo (rows 64..127) of the
+// A tile for K-stage ks, SW128 K-major.  Rows of tokens >= B stay zero (zeroed
+// once).  TC_CONV warps: item = (token, 8-element chunk), loads issued first.
+constexpr int TC_CONV = 3;  // converter warps (0, 6, 7)
+__device__ __forceinline__ void convert_x_tile(const float* __restrict__ x, int B, int64_t K, int64_t ks,
+                                               unsigned char* atile, int cidx) {
+  const int lane = threadIdx.x & 31;
+  const int64_t k0 = ks * TC_BK;
+  const int nitem = B * 8;
+  for (int t0 = cidx * 32; t0 < nitem; t0 += TC_CONV * 32 * 4) {
+    float4 va[4], vb[4];
+#pragma unroll
+    for (int u = 0; u < 4; u++) {
+      const int t = t0 + u * TC_CONV * 32 + lane;
+      const int m = t >> 3, c = t & 7;
+      const int64_t k = k0 + 8 * c;
+      va[u] = vb[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (t < nitem) {
+        if (k + 8 <= K) {
+          va[u] = __ldg(reinterpret_cast<const float4*>(x + (int64_t)m * K + k));
+          vb[u] = __ldg(reinterpret_cast<const float4*>(x + (int64_t)m * K + k + 4));
+        } else {
+          float v[8];
+#pragma unroll
+          for (int i = 0; i < 8; i++) v[i] = k + i < K ? x[(int64_t)m * K + k + i] : 0.f;
+          va[u] = make_float4(v[0], v[1], v[2], v[3]);
+          vb[u] = make_float4(v[4], v[5], v[6], v[7]);
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 4; u++) {
+      const int t = t0 + u * TC_CONV * 32 + lane;
+      if (t >= nitem) continue;
+      const int m = t >> 3, c = t & 7;
+      const float v[8] = {va[u].x, va[u].y, va[u].z, va[u].w, vb[u].x, vb[u].y, vb[u].z, vb[u].w};
+      uint32_t h[4], l[4];
+#pragma unroll
+      for (int i = 0; i < 4; i++) {
+        const __half2 hh = __floats2half2_rn(v[2 * i], v[2 * i + 1]);
+        const float2 hf = __half22float2(hh);
+        const __half2 ll = __floats2half2_rn(v[2 * i] - hf.x, v[2 * i + 1] - hf.y);
+        h[i] = *reinterpret_cast<const uint32_t*>(&hh);
+        l[i] = *reinterpret_cast<const uint32_t*>(&ll);
+      }
+      const int mh = m, ml = 64 + m;
+      *reinterpret_cast<uint4*>(atile + (mh >> 3) * 1024 + (mh & 7) * 128 + ((c ^ (mh & 7)) << 4)) =
+          make_uint4(h[0], h[1], h[2], h[3]);
+      *reinterpret_cast<uint4*>(atile + (ml >> 3) * 1024 + (ml & 7) * 128 + ((c ^ (ml & 7)) << 4)) =
+          make_uint4(l[0], l[1], l[2], l[3]);
+    }
+  }
+}
+
+template <int QT, int BS, bool DEC>
 __global__ void __launch_bounds__(TC_THREADS, 1)
-    qgemm_tc_kernel(const __grid_constant__ CUtensorMap xmap, const uint8_t* __restrict__ W, int64_t N, int64_t K,
-                    int64_t M, float* __restrict__ Y, int ksteps_per_split, int atomic_out) {
+    qgemm_tc_kernel(const __grid_constant__ CUtensorMap xmap, const float* __restrict__ xdec, const uint8_t* __restrict__ W,
+                    int64_t N, int64_t K, int64_t M, float* __restrict__ Y, int ksteps_per_split, int atomic_out) {
+  using Cfg = TcCfg<DEC>;
+  constexpr int MT = Cfg::MT, STAGES = Cfg::STAGES, STAGE_BYTES = Cfg::STAGE_BYTES;
+  constexpr int SBPAD = tc_sbpad(QT, BS);
   extern __shared__ unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* a_full = reinterpret_cast<uint64_t*>(smem + TC_STAGES * TC_STAGE_BYTES);
-  uint64_t* b_full = a_full + TC_STAGES;
-  uint64_t* empty = b_full + TC_STAGES;
-  uint64_t* acc_full = empty + TC_STAGES;
+  unsigned char* pring = smem + STAGES * STAGE_BYTES;  // [TC_PK][TC_BN][SBPAD] raw weight bytes
+  uint64_t* a_full = reinterpret_cast<uint64_t*>(pring + TC_PK * TC_BN * SBPAD);
+  uint64_t* b_full = a_full + STAGES;
+  uint64_t* empty = b_full + STAGES;
+  uint64_t* acc_full = empty + STAGES;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_full + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t n0 = (int64_t)blockIdx.x * TC_BN;
-  const int64_t m0 = (int64_t)blockIdx.y * (TC_BM * TC_MT);
+  const int64_t m0 = (int64_t)blockIdx.y * (TC_BM * MT);
   const int64_t nb = K / BS;
   const int ktotal = (int)((K + TC_BK - 1) / TC_BK);
   const int ks0 = blockIdx.z * ksteps_per_split;
   const int ks1 = min(ktotal, ks0 + ksteps_per_split);
-  const int nks = ks1 - ks0;
+  const int nks = max(ks1 - ks0, 0);
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < TC_STAGES; s++) {
-      mbar_init(&a_full[s], 1);
+    for (int s = 0; s < STAGES; s++) {
+      mbar_init(&a_full[s], DEC ? TC_CONV : 1);
       mbar_init(&b_full[s], 128);
       mbar_init(&empty[s], 1);
     }
     mbar_init(acc_full, 1);
     fence_mbar_init();
   }
+  if constexpr (DEC) {
+    // A tiles: rows of tokens >= B are never written by the converter -> zero them
+    for (int i = threadIdx.x; i < STAGES * TC_A_BYTES / 16; i += blockDim.x) {
+      const int s = i / (TC_A_BYTES / 16), o = i % (TC_A_BYTES / 16);
+      reinterpret_cast<uint4*>(smem + s * STAGE_BYTES)[o] = make_uint4(0u, 0u, 0u, 0u);
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                 "n"(TC_TMEM_COLS)
+                 "n"(Cfg::TMEM_COLS)
                  : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
@@ -184,37 +333,48 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  if (warp == 0) {
-    // ---------------- TMA producer: X tiles ----------------
-    if (lane == 0) {
+  if (warp == 0 || (DEC && warp >= 6)) {
+    if constexpr (DEC) {
+      // ---------------- converters: x fp32 -> fp16 hi/lo A tiles ----------------
+      const int cidx = warp == 0 ? 0 : warp - 5;
+      for (int i = 0; i < nks; i++) {
+        const int s = i % STAGES;
+        mbar_wait(&empty[s], ((i / STAGES) & 1) ^ 1);
+        convert_x_tile(xdec, (int)M, K, ks0 + i, smem + s * STAGE_BYTES, cidx);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> tensor core reads
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&a_full[s]);
+      }
+    } else if (lane == 0) {
+      // ---------------- TMA producer: X tiles ----------------
       asm volatile("prefetch.tensormap [%0];" ::"l"(&xmap) : "memory");
       for (int i = 0; i < nks; i++) {
-        const int s = i % TC_STAGES;
-        mbar_wait(&empty[s], ((i / TC_STAGES) & 1) ^ 1);
-        mbar_arrive_expect_tx(&a_full[s], TC_MT * TC_A_BYTES);
-        unsigned char* st = smem + s * TC_STAGE_BYTES;
-        for (int mt = 0; mt < TC_MT; mt++)
+        const int s = i % STAGES;
+        mbar_wait(&empty[s], ((i / STAGES) & 1) ^ 1);
+        mbar_arrive_expect_tx(&a_full[s], MT * TC_A_BYTES);
+        unsigned char* st = smem + s * STAGE_BYTES;
+        for (int mt = 0; mt < MT; mt++)
           tma_load_2d(st + mt * TC_A_BYTES, &xmap, (ks0 + i) * TC_BK, (int)(m0 + mt * TC_BM), &a_full[s]);
       }
     }
   } else if (warp == 1) {
     // ---------------- MMA issuer (one thread) ----------------
     if (lane == 0) {
-      constexpr uint32_t idesc = umma_idesc_bf16(TC_BM, TC_BN);
+      constexpr uint32_t idesc = DEC ? umma_idesc_f16(TC_BM, TC_BN) : umma_idesc_bf16(TC_BM, TC_BN);
       for (int i = 0; i < nks; i++) {
-        const int s = i % TC_STAGES;
-        const uint32_t par = (i / TC_STAGES) & 1;
+        const int s = i % STAGES;
+        const uint32_t par = (i / STAGES) & 1;
         mbar_wait(&a_full[s], par);
         mbar_wait(&b_full[s], par);
         tc_fence_after();
-        const uint32_t st = smem_u32(smem + s * TC_STAGE_BYTES);
-        const uint64_t bdesc0 = umma_desc_sw128(st + TC_MT * TC_A_BYTES);
+        const uint32_t st = smem_u32(smem + s * STAGE_BYTES);
+        const uint64_t bdesc0 = umma_desc_sw128(st + MT * TC_A_BYTES);
 #pragma unroll
-        for (int mt = 0; mt < TC_MT; mt++) {
+        for (int mt = 0; mt < MT; mt++) {
           const uint64_t adesc0 = umma_desc_sw128(st + mt * TC_A_BYTES);
 #pragma unroll
           for (int kk = 0; kk < TC_BK / 16; kk++) {
-            // advance 16 bf16 = 32 bytes along K inside the 128-byte swizzle row
+            // advance 16 elements = 32 bytes along K inside the 128-byte swizzle row
             umma_bf16(tmem + mt * TC_BN, adesc0 + (uint64_t)(kk * 2), bdesc0 + (uint64_t)(kk * 2), idesc,
                       (i > 0) || (kk > 0));
           }
@@ -226,14 +386,25 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   } else if (warp < 6) {
     // ---------------- dequantizers: one weight row per thread ----------------
     const int r = threadIdx.x - 64;  // 0..127
+    const int64_t n = n0 + r;
+    unsigned char* myring = pring + r * SBPAD;
+#pragma unroll
+    for (int i = 0; i < TC_PD; i++) {
+      if (i < nks) prefetch_row<QT, BS>(W, nb, n, N, ks0 + i, K, myring + (i % TC_PK) * TC_BN * SBPAD);
+      cp_async_commit();
+    }
     for (int i = 0; i < nks; i++) {
-      const int s = i % TC_STAGES;
-      mbar_wait(&empty[s], ((i / TC_STAGES) & 1) ^ 1);
-      unsigned char* btile = smem + s * TC_STAGE_BYTES + TC_MT * TC_A_BYTES;
-      dequant_row<QT, BS>(W, nb, n0 + r, N, (int64_t)(ks0 + i) * TC_BK, K, btile, r);
+      const int s = i % STAGES;
+      if (i + TC_PD < nks) prefetch_row<QT, BS>(W, nb, n, N, ks0 + i + TC_PD, K, myring + ((i + TC_PD) % TC_PK) * TC_BN * SBPAD);
+      cp_async_commit();
+      cp_async_wait<TC_PD>();  // stage i's bytes have landed (own copies only: no barrier needed)
+      mbar_wait(&empty[s], ((i / STAGES) & 1) ^ 1);
+      unsigned char* btile = smem + s * STAGE_BYTES + MT * TC_A_BYTES;
+      dequant_row<QT, BS, DEC>(myring + (i % TC_PK) * TC_BN * SBPAD, n, N, (int64_t)(ks0 + i) * TC_BK, K, btile, r);
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> tensor core reads
       mbar_arrive(&b_full[s]);
     }
+    cp_async_wait<0>();
   }
 
   // ---------------- epilogue: TMEM -> registers -> global ----------------
@@ -241,36 +412,66 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     mbar_wait(acc_full, 0);
     tc_fence_after();
     const int q = warp & 3;  // TMEM lane quarter this warp may access
-#pragma unroll
-    for (int mt = 0; mt < TC_MT; mt++) {
-      const int64_t m = m0 + mt * TC_BM + q * 32 + lane;
+    if constexpr (DEC) {
+      // lanes 64..127 hold the lo rows: quarters 2, 3 hand them to quarters 0, 1
+      float* xch = reinterpret_cast<float*>(smem);  // [64 tokens][32 cols], stage 0 (idle now)
 #pragma unroll
       for (int cc = 0; cc < TC_BN / 32; cc++) {
         uint32_t rr[32];
-        tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + mt * TC_BN + cc * 32, rr);
-        const int64_t nbase = n0 + cc * 32;
-        if (m < M && nks > 0) {
-          float* yrow = Y + m * N + nbase;
-          if (nbase + 32 <= N && (N % 4) == 0) {
+        tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + cc * 32, rr);
+        if (q >= 2) {
 #pragma unroll
-            for (int j = 0; j < 32; j += 4) {
-              if (atomic_out) {
-                asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(yrow + j), "f"(__uint_as_float(rr[j])),
-                             "f"(__uint_as_float(rr[j + 1])), "f"(__uint_as_float(rr[j + 2])), "f"(__uint_as_float(rr[j + 3]))
-                             : "memory");
-              } else {
-                *reinterpret_cast<float4*>(yrow + j) = make_float4(__uint_as_float(rr[j]), __uint_as_float(rr[j + 1]),
-                                                                   __uint_as_float(rr[j + 2]), __uint_as_float(rr[j + 3]));
+          for (int j = 0; j < 32; j++) xch[((q - 2) * 32 + lane) * 33 + j] = __uint_as_float(rr[j]);
+        }
+        named_bar_sync(2, 128);
+        if (q < 2) {
+          const int64_t m = q * 32 + lane;
+          const int64_t nbase = n0 + cc * 32;
+          if (m < M && nks > 0) {
+            float* yrow = Y + m * N + nbase;
+            for (int j = 0; j < 32; j++) {
+              const float v = __uint_as_float(rr[j]) + xch[(q * 32 + lane) * 33 + j];
+              if (nbase + j < N) {
+                if (atomic_out) atomicAdd(yrow + j, v);
+                else yrow[j] = v;
               }
             }
-          } else {
-            for (int j = 0; j < 32; j++)
-              if (nbase + j < N) {
-                if (atomic_out)
-                  atomicAdd(yrow + j, __uint_as_float(rr[j]));
-                else
-                  yrow[j] = __uint_as_float(rr[j]);
+          }
+        }
+        named_bar_sync(2, 128);
+      }
+    } else {
+#pragma unroll
+      for (int mt = 0; mt < MT; mt++) {
+        const int64_t m = m0 + mt * TC_BM + q * 32 + lane;
+#pragma unroll
+        for (int cc = 0; cc < TC_BN / 32; cc++) {
+          uint32_t rr[32];
+          tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + mt * TC_BN + cc * 32, rr);
+          const int64_t nbase = n0 + cc * 32;
+          if (m < M && nks > 0) {
+            float* yrow = Y + m * N + nbase;
+            if (nbase + 32 <= N && (N % 4) == 0) {
+#pragma unroll
+              for (int j = 0; j < 32; j += 4) {
+                if (atomic_out) {
+                  asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(yrow + j), "f"(__uint_as_float(rr[j])),
+                               "f"(__uint_as_float(rr[j + 1])), "f"(__uint_as_float(rr[j + 2])), "f"(__uint_as_float(rr[j + 3]))
+                               : "memory");
+                } else {
+                  *reinterpret_cast<float4*>(yrow + j) = make_float4(__uint_as_float(rr[j]), __uint_as_float(rr[j + 1]),
+                                                                     __uint_as_float(rr[j + 2]), __uint_as_float(rr[j + 3]));
+                }
               }
+            } else {
+              for (int j = 0; j < 32; j++)
+                if (nbase + j < N) {
+                  if (atomic_out)
+                    atomicAdd(yrow + j, __uint_as_float(rr[j]));
+                  else
+                    yrow[j] = __uint_as_float(rr[j]);
+                }
+            }
           }
         }
       }
@@ -280,7 +481,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(TC_TMEM_COLS) : "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(Cfg::TMEM_COLS) : "memory");
   }
 }
 
@@ -309,6 +510,45 @@ static int tc_sms() {
   return n;
 }
 
+// split K until the grid covers the SMs (partials combined with red.add)
+static int tc_splits(int tiles, int ktotal) {
+  int splits = 1;
+  while (tiles * splits < tc_sms() && ktotal / (splits * 2) >= 8) splits *= 2;
+  return splits;
+}
+
+template <bool DEC>
+static if_status tc_run(if_scheme s, const CUtensorMap& map, const float* xdec, const uint8_t* W, int64_t N, int64_t K,
+                        int64_t M, float* Y, int accumulate, cudaStream_t st) {
+  // the cp.async weight prefetch needs 4-byte aligned rows (Q3H_B32 with an odd
+  // number of blocks per row is 2-byte aligned: SIMT path)
+  const int64_t row_bytes = K / s.block * q_block_bytes(s.type, s.block);
+  if ((row_bytes & 3) || (reinterpret_cast<uintptr_t>(W) & 3u)) return IF_ERR_UNSUPPORTED;
+  const int ntile = (int)((N + TC_BN - 1) / TC_BN);
+  const int mtile = DEC ? 1 : (int)((M + TC_BM * TcCfg<DEC>::MT - 1) / (TC_BM * TcCfg<DEC>::MT));
+  const int ktotal = (int)((K + TC_BK - 1) / TC_BK);
+  const int splits = tc_splits(ntile * mtile, ktotal);
+  const int kper = (ktotal + splits - 1) / splits;
+  const int atomic_out = (splits > 1) || accumulate;
+  if (splits > 1 && !accumulate) {
+    if (cudaMemsetAsync(Y, 0, sizeof(float) * M * N, st) != cudaSuccess) return check_launch("qgemm_tc memset");
+  }
+  return dispatch_scheme(s, [&]<int QT, int BS>() -> if_status {
+    auto kern = qgemm_tc_kernel<QT, BS, DEC>;
+    constexpr int smem = tc_smem<DEC>(QT, BS);
+    static_assert(smem <= 227 * 1024, "shared memory");
+    static bool configured = false;
+    if (!configured) {
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      configured = true;
+    }
+    dim3 grid(ntile, mtile, splits);
+    kern<<<grid, TC_THREADS, smem, st>>>(map, xdec, W, N, K, M, Y, kper, atomic_out);
+    count_launch();
+    return check_launch(DEC ? "qgemv_tc" : "qgemm_tc");
+  });
+}
+
 if_status qgemm_tc_launch(if_scheme s, const uint8_t* W, int64_t N, int64_t K, const __nv_bfloat16* X, int64_t M,
                           float* Y, int accumulate, cudaStream_t st) {
   // TMA needs the X row pitch (K * 2 bytes) to be a multiple of 16 and a 16-byte aligned base
@@ -324,29 +564,16 @@ if_status qgemm_tc_launch(if_scheme s, const uint8_t* W, int64_t N, int64_t K, c
                          estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (cr != CUDA_SUCCESS) return set_error(IF_ERR_CUDA, "qgemm_tc: cuTensorMapEncodeTiled failed (%d)", (int)cr);
-  const int ntile = (int)((N + TC_BN - 1) / TC_BN);
-  const int mtile = (int)((M + TC_BM * TC_MT - 1) / (TC_BM * TC_MT));
-  const int ktotal = (int)((K + TC_BK - 1) / TC_BK);
-  // split K until the grid covers the SMs (partials combined with red.add)
-  int splits = 1;
-  while (ntile * mtile * splits < tc_sms() && ktotal / (splits * 2) >= 8) splits *= 2;
-  const int kper = (ktotal + splits - 1) / splits;
-  const int atomic_out = (splits > 1) || accumulate;
-  if (splits > 1 && !accumulate) {
-    if (cudaMemsetAsync(Y, 0, sizeof(float) * M * N, st) != cudaSuccess) return check_launch("qgemm_tc memset");
-  }
-  return dispatch_scheme(s, [&]<int QT, int BS>() -> if_status {
-    auto kern = qgemm_tc_kernel<QT, BS>;
-    static bool configured = false;
-    if (!configured) {
-      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM);
-      configured = true;
-    }
-    dim3 grid(ntile, mtile, splits);
-    kern<<<grid, TC_THREADS, TC_SMEM, st>>>(map, W, N, K, M, Y, kper, atomic_out);
-    count_launch();
-    return check_launch("qgemm_tc");
-  });
+  return tc_run<false>(s, map, nullptr, W, N, K, M, Y, accumulate, st);
+}
+
+if_status qgemv_tc_launch(if_scheme s, const uint8_t* W, int64_t N, int64_t K, const float* x, int64_t B, float* Y,
+                          int accumulate, cudaStream_t st) {
+  if (B < 1 || B > 64 || K % 8 != 0 || (reinterpret_cast<uintptr_t>(x) & 15u) || N > (int64_t)1 << 30)
+    return IF_ERR_UNSUPPORTED;
+  CUtensorMap map;  // unused in decode mode
+  memset(&map, 0, sizeof(map));
+  return tc_run<true>(s, map, x, W, N, K, B, Y, accumulate, st);
 }
 
 }  // namespace ifb

@@ -18,6 +18,7 @@
 
 #include "common.cuh"
 #include "decode_mk.cuh"
+#include "qgemm.cuh"
 #include "simd.cuh"
 
 namespace ifb {
@@ -303,6 +304,11 @@ static if_status qgemv_impl(const char* fn, if_scheme s, const uint8_t* W, int64
       if (cudaMemsetAsync(y, 0, sizeof(float) * N * B, st) != cudaSuccess) return check_launch(fn);
     }
     return IF_OK;
+  }
+  if (B >= 2) {
+    // batched decode: the tensor cores (fp16 W', fp16 hi/lo x), weights streamed once
+    if_status r = qgemv_tc_launch(s, W, N, K, x, B, y, acc, st);
+    if (r != IF_ERR_UNSUPPORTED) return r;
   }
   if (s.type == IF_Q3H && s.block == 64 && (reinterpret_cast<uintptr_t>(W) & 31u) == 0 && N < (1ll << 31)) {
     bool done = false;
