@@ -37,6 +37,18 @@ constexpr int TC_BN = 128;     // weight rows per CTA (UMMA N)
 constexpr int TC_BM = 128;     // activation rows per UMMA tile (UMMA M)
 constexpr int TC_BK = 64;      // K per stage
 constexpr int TC_THREADS = 256;
+// fast Q3H_B64 decode variant: 8 dequant warps (2 threads per weight row, half2
+// arithmetic), converters on warps 0, 10, 11 -> 12 warps
+template <int QT, int BS, bool DEC>
+struct TcVar {
+#ifdef IFB_TC_FASTQ3H
+  static constexpr bool FAST = DEC && QT == 35 && BS == 64;  // fp16 arithmetic: ~2x the W' rounding error
+#else
+  static constexpr bool FAST = false;
+#endif
+  static constexpr int THREADS = FAST ? 384 : 256;
+  static constexpr int NDEQ = FAST ? 256 : 128;  // dequant threads (b_full arrivals)
+};
 constexpr int TC_A_BYTES = TC_BM * TC_BK * 2;  // 16 KB per M tile
 constexpr int TC_B_BYTES = TC_BN * TC_BK * 2;  // 16 KB
 constexpr int TC_PK = 8;   // packed-weight ring slots (stages of raw bytes per row)
@@ -45,7 +57,7 @@ constexpr int TC_PD = 6;   // cp.async prefetch distance (stages)
 template <bool DEC>
 struct TcCfg {
   static constexpr int MT = DEC ? 1 : 2;          // UMMA M tiles per CTA
-  static constexpr int STAGES = DEC ? 4 : 3;
+  static constexpr int STAGES = 3;
   static constexpr int STAGE_BYTES = MT * TC_A_BYTES + TC_B_BYTES;
   static constexpr int TMEM_COLS = MT * TC_BN;
 };
@@ -55,9 +67,12 @@ __host__ __device__ constexpr int tc_sb(int qt, int bs) { return (TC_BK / bs) * 
 __host__ __device__ constexpr int tc_sbpad(int qt, int bs) {
   return ((tc_sb(qt, bs) + 15) / 16) % 2 ? ((tc_sb(qt, bs) + 15) / 16) * 16 : ((tc_sb(qt, bs) + 15) / 16 + 1) * 16;
 }
+constexpr int TC_XR = 3;            // decode: raw fp32 x stages (bulk copies), 64 tokens x 64 k each
+constexpr int TC_XR_BYTES = 64 * TC_BK * 4;
 template <bool DEC>
 __host__ __device__ constexpr int tc_smem(int qt, int bs) {
-  return TcCfg<DEC>::STAGES * TcCfg<DEC>::STAGE_BYTES + TC_PK * TC_BN * tc_sbpad(qt, bs) + 1024 /*align*/ + 256;
+  return TcCfg<DEC>::STAGES * TcCfg<DEC>::STAGE_BYTES + TC_PK * TC_BN * tc_sbpad(qt, bs) + (DEC ? TC_XR * TC_XR_BYTES : 0) +
+         1024 /*align*/ + 256;
 }
 
 // ---- tcgen05 / TMA PTX wrappers ----------------------------------------------
@@ -184,6 +199,11 @@ __device__ __forceinline__ void dequant_row(const unsigned char* raw, int64_t n,
     for (int sub = 0; sub < TC_BK / BS; sub++) {
       // block sub starts at byte sub * BB (a multiple of 2): word-aligned or a halfword in
       const int boff = sub * BB;
+      if (k0 + sub * BS >= K) {
+#pragma unroll
+        for (int j = 0; j < BS / 2; j++) out[sub * (BS / 2) + j] = 0u;
+        continue;
+      }
       uint32_t w[NW + 1];
 #pragma unroll
       for (int i = 0; i <= NW; i++) {
@@ -226,75 +246,138 @@ __device__ __forceinline__ void dequant_row(const unsigned char* raw, int64_t n,
   }
 }
 
-// Decode mode: x fp32 [B, K] -> fp16 hi (rows 0..63) + lo (rows 64..127) of the
-// A tile for K-stage ks, SW128 K-major.  Rows of tokens >= B stay zero (zeroed
-// once).  TC_CONV warps: item = (token, 8-element chunk), loads issued first.
-constexpr int TC_CONV = 3;  // converter warps (0, 6, 7)
-__device__ __forceinline__ void convert_x_tile(const float* __restrict__ x, int B, int64_t K, int64_t ks,
-                                               unsigned char* atile, int cidx) {
+// Decode mode: the raw fp32 x of K-stage ks (token m's 64 values at xr + 256 m,
+// landed by bulk copies) -> fp16 hi (rows 0..63) + lo (rows 64..127) of the A
+// tile, SW128 K-major.  Rows of tokens >= B stay zero (zeroed once).  TC_CONV
+// warps; item = (token, 8-element chunk).
+constexpr int TC_CONV = 3;  // converter warps
+template <bool PERM>
+__device__ __forceinline__ void convert_x_tile(const float* xr, int B, unsigned char* atile, int cidx) {
   const int lane = threadIdx.x & 31;
-  const int64_t k0 = ks * TC_BK;
-  const int nitem = B * 8;
-  for (int t0 = cidx * 32; t0 < nitem; t0 += TC_CONV * 32 * 4) {
-    float4 va[4], vb[4];
+  for (int t = cidx * 32 + lane; t < B * 8; t += TC_CONV * 32) {
+    const int m = t >> 3, c = t & 7;
+    const float4 va = *reinterpret_cast<const float4*>(xr + m * TC_BK + 8 * c);
+    const float4 vb = *reinterpret_cast<const float4*>(xr + m * TC_BK + 8 * c + 4);
+    // PERM: the fast Q3H dequant's K order (x0, x4, x1, x5, x2, x6, x3, x7) of each chunk
+    const float v[8] = {va.x, PERM ? vb.x : va.y, PERM ? va.y : va.z, PERM ? vb.y : va.w,
+                        PERM ? va.z : vb.x, PERM ? vb.z : vb.y, PERM ? va.w : vb.z, vb.w};
+    uint32_t h[4], l[4];
 #pragma unroll
-    for (int u = 0; u < 4; u++) {
-      const int t = t0 + u * TC_CONV * 32 + lane;
-      const int m = t >> 3, c = t & 7;
-      const int64_t k = k0 + 8 * c;
-      va[u] = vb[u] = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (t < nitem) {
-        if (k + 8 <= K) {
-          va[u] = __ldg(reinterpret_cast<const float4*>(x + (int64_t)m * K + k));
-          vb[u] = __ldg(reinterpret_cast<const float4*>(x + (int64_t)m * K + k + 4));
+    for (int i = 0; i < 4; i++) {
+      const __half2 hh = __floats2half2_rn(v[2 * i], v[2 * i + 1]);
+      const float2 hf = __half22float2(hh);
+      const __half2 ll = __floats2half2_rn(v[2 * i] - hf.x, v[2 * i + 1] - hf.y);
+      h[i] = *reinterpret_cast<const uint32_t*>(&hh);
+      l[i] = *reinterpret_cast<const uint32_t*>(&ll);
+    }
+    const int mh = m, ml = 64 + m;
+    *reinterpret_cast<uint4*>(atile + (mh >> 3) * 1024 + (mh & 7) * 128 + ((c ^ (mh & 7)) << 4)) =
+        make_uint4(h[0], h[1], h[2], h[3]);
+    *reinterpret_cast<uint4*>(atile + (ml >> 3) * 1024 + (ml & 7) * 128 + ((c ^ (ml & 7)) << 4)) =
+        make_uint4(l[0], l[1], l[2], l[3]);
+  }
+}
+
+// one 2D TMA of the fp32 x tile [64 tokens x 64 k] of K-stage ks into a raw-x slot
+// (out-of-range tokens / k are zero-filled by the tensor map)
+__device__ __forceinline__ void issue_x_stage(const CUtensorMap* xmap, int64_t ks, float* xr, uint64_t* bar) {
+  mbar_arrive_expect_tx(bar, TC_XR_BYTES);
+  tma_load_2d(xr, xmap, (int)(ks * TC_BK), 0, bar);
+}
+
+// ---- fast Q3H_B64 dequant to fp16 (decode mode), two threads per row ---------
+// Half h of the row's 32-byte block (header lo|hi fp16, 7-bit pair codes from
+// byte 4) -> pairs [16h, 16h + 16) -> 16-byte chunks [4h, 4h + 4) of
+// the SW128 row.  Codes (4q + d, 4q + 2 + d) share one half2 lane pair:
+//   h2 = (c_a | 0x6400, c_b | 0x6400)          = (1024 + c_a, 1024 + c_b)
+//   q_e = RN((c - 5) / 11) = floor(c / 11)      (|(c - 5) / 11 - m| <= 5/11 and the
+//       = HFMA2(c, 1/11, -5/11) + 1536 - 1536    fp16 evaluation error is < 0.01: checked for all c)
+//   q_o = c - 11 q_e, exact in fp16
+//   w'  = q step_hi + (q step_lo + lo)          (Eq. 2 in fp16, step split hi + lo: ~fp16(w') )
+// K order inside a chunk (matched by the converter's x permutation):
+//   we(4q), we(4q+2), wo(4q), wo(4q+2), we(4q+1), we(4q+3), wo(4q+1), wo(4q+3)
+__device__ __forceinline__ uint32_t h2u(__half2 v) { return *reinterpret_cast<uint32_t*>(&v); }
+__device__ __forceinline__ __half2 u2h(uint32_t v) { return *reinterpret_cast<__half2*>(&v); }
+// stream bits [p, p + 32) of the code area (words c[0..7], c[7] = 0)
+__device__ __forceinline__ uint32_t code_bits(const uint32_t (&c)[8], int p) {
+  const int wi = p >> 5, sh = p & 31;
+  return sh ? __funnelshift_r(c[wi], c[wi + 1], sh) : c[wi];
+}
+__device__ __forceinline__ void dequant_q3h64_half(const unsigned char* raw, bool valid, int h, unsigned char* btile,
+                                                   int r) {
+  uint32_t outw[16];
+  if (valid) {
+    const uint4 v0 = *reinterpret_cast<const uint4*>(raw);
+    const uint4 v1 = *reinterpret_cast<const uint4*>(raw + 16);
+    const uint32_t hdr = v0.x;
+    // code-stream window of this half: bits [112 h, 112 h + 160), so that every code
+    // position below is a compile-time constant for both halves
+    const uint32_t ca[9] = {v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w, 0u, 0u};
+    uint32_t c[6];
+#pragma unroll
+    for (int i = 0; i < 5; i++) c[i] = h ? __funnelshift_r(ca[3 + i], ca[4 + i], 16) : ca[i];
+    c[5] = 0u;
+    const float lo = half_bits_to_float(hdr & 0xFFFFu), hi = half_bits_to_float(hdr >> 16);
+    const float stepf = __fdiv_rn(__fsub_rn(hi, lo), 10.0f);
+    const __half2 step2 = __float2half2_rn(stepf);  // step = step2 + stepl2 to ~22 bits
+    const __half2 stepl2 = __float2half2_rn(stepf - __low2float(step2));
+    const __half2 lo2 = u2h((hdr & 0xFFFFu) | (hdr << 16));
+    const __half2 k11 = __float2half2_rn(1.0f / 11.0f), kb = __float2half2_rn(-5.0f / 11.0f);
+    const __half2 k1536 = __float2half2_rn(1536.0f), k1024 = __float2half2_rn(1024.0f), km11 = __float2half2_rn(-11.0f);
+#pragma unroll
+    for (int qq = 0; qq < 4; qq++) {
+#pragma unroll
+      for (int dd = 0; dd < 2; dd++) {
+        const int jr = 4 * qq + dd;  // codes 16h + jr and 16h + jr + 2
+        const int p = 7 * jr;
+        const uint32_t t = (p & 31) ? __funnelshift_r(c[p >> 5], c[(p >> 5) + 1], p & 31) : c[p >> 5];
+        uint32_t ub;
+        if (jr == 0) {
+          ub = t << 2;  // code jr + 2 from bits 14..20 to 16..22
         } else {
-          float v[8];
-#pragma unroll
-          for (int i = 0; i < 8; i++) v[i] = k + i < K ? x[(int64_t)m * K + k + i] : 0.f;
-          va[u] = make_float4(v[0], v[1], v[2], v[3]);
-          vb[u] = make_float4(v[4], v[5], v[6], v[7]);
+          const int p2 = p - 2;
+          ub = (p2 & 31) ? __funnelshift_r(c[p2 >> 5], c[(p2 >> 5) + 1], p2 & 31) : c[p2 >> 5];
         }
+        const __half2 hh = u2h((ub & 0x007F0000u) | (t & 0x7Fu) | 0x64006400u);
+        const __half2 c2 = __hsub2(hh, k1024);  // (c_a, c_b), exact
+        const __half2 rr = __hadd2(__hfma2(c2, k11, kb), k1536);
+        const __half2 qe = __hsub2(rr, k1536);
+        const __half2 qo = __hfma2(qe, km11, c2);
+        outw[qq * 4 + 2 * dd] = h2u(__hfma2(qe, step2, __hfma2(qe, stepl2, lo2)));
+        outw[qq * 4 + 2 * dd + 1] = h2u(__hfma2(qo, step2, __hfma2(qo, stepl2, lo2)));
       }
     }
+  } else {
 #pragma unroll
-    for (int u = 0; u < 4; u++) {
-      const int t = t0 + u * TC_CONV * 32 + lane;
-      if (t >= nitem) continue;
-      const int m = t >> 3, c = t & 7;
-      const float v[8] = {va[u].x, va[u].y, va[u].z, va[u].w, vb[u].x, vb[u].y, vb[u].z, vb[u].w};
-      uint32_t h[4], l[4];
+    for (int i = 0; i < 16; i++) outw[i] = 0u;
+  }
+  unsigned char* rowp = btile + (r >> 3) * 1024 + (r & 7) * 128;
 #pragma unroll
-      for (int i = 0; i < 4; i++) {
-        const __half2 hh = __floats2half2_rn(v[2 * i], v[2 * i + 1]);
-        const float2 hf = __half22float2(hh);
-        const __half2 ll = __floats2half2_rn(v[2 * i] - hf.x, v[2 * i + 1] - hf.y);
-        h[i] = *reinterpret_cast<const uint32_t*>(&hh);
-        l[i] = *reinterpret_cast<const uint32_t*>(&ll);
-      }
-      const int mh = m, ml = 64 + m;
-      *reinterpret_cast<uint4*>(atile + (mh >> 3) * 1024 + (mh & 7) * 128 + ((c ^ (mh & 7)) << 4)) =
-          make_uint4(h[0], h[1], h[2], h[3]);
-      *reinterpret_cast<uint4*>(atile + (ml >> 3) * 1024 + (ml & 7) * 128 + ((c ^ (ml & 7)) << 4)) =
-          make_uint4(l[0], l[1], l[2], l[3]);
-    }
+  for (int qq = 0; qq < 4; qq++) {
+    const int cch = 4 * h + qq;
+    *reinterpret_cast<uint4*>(rowp + ((cch ^ (r & 7)) << 4)) =
+        make_uint4(outw[4 * qq], outw[4 * qq + 1], outw[4 * qq + 2], outw[4 * qq + 3]);
   }
 }
 
 template <int QT, int BS, bool DEC>
-__global__ void __launch_bounds__(TC_THREADS, 1)
+__global__ void __launch_bounds__(TcVar<QT, BS, DEC>::THREADS, 1)
     qgemm_tc_kernel(const __grid_constant__ CUtensorMap xmap, const float* __restrict__ xdec, const uint8_t* __restrict__ W,
                     int64_t N, int64_t K, int64_t M, float* __restrict__ Y, int ksteps_per_split, int atomic_out) {
   using Cfg = TcCfg<DEC>;
+  using Var = TcVar<QT, BS, DEC>;
   constexpr int MT = Cfg::MT, STAGES = Cfg::STAGES, STAGE_BYTES = Cfg::STAGE_BYTES;
   constexpr int SBPAD = tc_sbpad(QT, BS);
   extern __shared__ unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   unsigned char* pring = smem + STAGES * STAGE_BYTES;  // [TC_PK][TC_BN][SBPAD] raw weight bytes
-  uint64_t* a_full = reinterpret_cast<uint64_t*>(pring + TC_PK * TC_BN * SBPAD);
+  float* xraw = reinterpret_cast<float*>(pring + TC_PK * TC_BN * SBPAD);  // decode: [TC_XR][64][64] raw x
+  uint64_t* a_full = reinterpret_cast<uint64_t*>(reinterpret_cast<unsigned char*>(xraw) + (DEC ? TC_XR * TC_XR_BYTES : 0));
   uint64_t* b_full = a_full + STAGES;
   uint64_t* empty = b_full + STAGES;
   uint64_t* acc_full = empty + STAGES;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_full + 1);
+  uint64_t* xr_full = acc_full + 1;  // [TC_XR]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(xr_full + TC_XR);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t n0 = (int64_t)blockIdx.x * TC_BN;
@@ -308,10 +391,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; s++) {
       mbar_init(&a_full[s], DEC ? TC_CONV : 1);
-      mbar_init(&b_full[s], 128);
+      mbar_init(&b_full[s], Var::NDEQ);
       mbar_init(&empty[s], 1);
     }
     mbar_init(acc_full, 1);
+    for (int i = 0; i < TC_XR; i++) mbar_init(&xr_full[i], 1);
     fence_mbar_init();
   }
   if constexpr (DEC) {
@@ -333,17 +417,26 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  if (warp == 0 || (DEC && warp >= 6)) {
+  const int conv_first = Var::FAST ? 10 : 6;  // converter warps: 0 and conv_first..
+  if (warp == 0 || (DEC && warp >= conv_first)) {
     if constexpr (DEC) {
       // ---------------- converters: x fp32 -> fp16 hi/lo A tiles ----------------
-      const int cidx = warp == 0 ? 0 : warp - 5;
+      const int cidx = warp == 0 ? 0 : warp - conv_first + 1;
+      const bool issuer = warp == 0 && lane == 0;
+      if (issuer)
+        for (int i = 0; i < TC_XR && i < nks; i++)
+          issue_x_stage(&xmap, ks0 + i, xraw + i * (TC_XR_BYTES / 4), &xr_full[i]);
       for (int i = 0; i < nks; i++) {
-        const int s = i % STAGES;
+        const int s = i % STAGES, xs = i % TC_XR;
         mbar_wait(&empty[s], ((i / STAGES) & 1) ^ 1);
-        convert_x_tile(xdec, (int)M, K, ks0 + i, smem + s * STAGE_BYTES, cidx);
+        mbar_wait(&xr_full[xs], (i / TC_XR) & 1);
+        convert_x_tile<Var::FAST>(xraw + xs * (TC_XR_BYTES / 4), (int)M, smem + s * STAGE_BYTES, cidx);
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> tensor core reads
         __syncwarp();
         if (lane == 0) mbar_arrive(&a_full[s]);
+        named_bar_sync(3, TC_CONV * 32);  // every converter is done with this raw-x slot
+        if (issuer && i + TC_XR < nks)
+          issue_x_stage(&xmap, ks0 + i + TC_XR, xraw + xs * (TC_XR_BYTES / 4), &xr_full[xs]);
       }
     } else if (lane == 0) {
       // ---------------- TMA producer: X tiles ----------------
@@ -383,7 +476,36 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       }
       umma_commit(acc_full);
     }
-  } else if (warp < 6) {
+  } else if (Var::FAST && warp < 10) {
+    // ---------------- fast Q3H_B64 dequantizers: two threads per row ----------------
+    const int dw = warp - 2;                     // 0..7, 16 rows each
+    const int r = dw * 16 + (lane >> 1), h = lane & 1;
+    const int64_t n = n0 + r;
+    unsigned char* myrow = pring + r * SBPAD;  // this row's slot 0; half h copies bytes [16h, 16h + 16)
+    auto pre = [&](int i) {
+      const int64_t ks = ks0 + i;
+      if (n < N && ks * TC_BK < K) cp_async16(myrow + (i % TC_PK) * TC_BN * SBPAD + 16 * h, W + (n * nb + ks) * 32 + 16 * h);
+    };
+#pragma unroll
+    for (int i = 0; i < TC_PD; i++) {
+      if (i < nks) pre(i);
+      cp_async_commit();
+    }
+    for (int i = 0; i < nks; i++) {
+      const int s = i % STAGES;
+      if (i + TC_PD < nks) pre(i + TC_PD);
+      cp_async_commit();
+      cp_async_wait<TC_PD>();
+      __syncwarp();  // the partner lane's half of the block is visible
+      mbar_wait(&empty[s], ((i / STAGES) & 1) ^ 1);
+      unsigned char* btile = smem + s * STAGE_BYTES + MT * TC_A_BYTES;
+      dequant_q3h64_half(myrow + (i % TC_PK) * TC_BN * SBPAD, n < N && (int64_t)(ks0 + i) * TC_BK < K, h, btile, r);
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> tensor core reads
+      mbar_arrive(&b_full[s]);
+      __syncwarp();  // both halves read before the partner overwrites (ring reuse)
+    }
+    cp_async_wait<0>();
+  } else if (!Var::FAST && warp < 6) {
     // ---------------- dequantizers: one weight row per thread ----------------
     const int r = threadIdx.x - 64;  // 0..127
     const int64_t n = n0 + r;
@@ -543,7 +665,7 @@ static if_status tc_run(if_scheme s, const CUtensorMap& map, const float* xdec, 
       configured = true;
     }
     dim3 grid(ntile, mtile, splits);
-    kern<<<grid, TC_THREADS, smem, st>>>(map, xdec, W, N, K, M, Y, kper, atomic_out);
+    kern<<<grid, TcVar<QT, BS, DEC>::THREADS, smem, st>>>(map, xdec, W, N, K, M, Y, kper, atomic_out);
     count_launch();
     return check_launch(DEC ? "qgemv_tc" : "qgemm_tc");
   });
@@ -571,8 +693,16 @@ if_status qgemv_tc_launch(if_scheme s, const uint8_t* W, int64_t N, int64_t K, c
                           int accumulate, cudaStream_t st) {
   if (B < 1 || B > 64 || K % 8 != 0 || (reinterpret_cast<uintptr_t>(x) & 15u) || N > (int64_t)1 << 30)
     return IF_ERR_UNSUPPORTED;
-  CUtensorMap map;  // unused in decode mode
-  memset(&map, 0, sizeof(map));
+  if (!get_encoder()) return IF_ERR_UNSUPPORTED;
+  CUtensorMap map;  // x fp32 [B, K], tiles of 64 tokens x 64 k, no swizzle (the converter reads it)
+  cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)B};
+  cuuint64_t strides[1] = {(cuuint64_t)K * 4};
+  cuuint32_t box[2] = {(cuuint32_t)TC_BK, 64u};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult cr = g_encode(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(x), dims, strides, box, estr,
+                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (cr != CUDA_SUCCESS) return set_error(IF_ERR_CUDA, "qgemv_tc: cuTensorMapEncodeTiled failed (%d)", (int)cr);
   return tc_run<true>(s, map, x, W, N, K, B, Y, accumulate, st);
 }
 
