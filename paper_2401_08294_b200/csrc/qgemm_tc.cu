@@ -23,6 +23,8 @@
 // Pipeline: full barriers (A: TMA tx bytes or converter arrival; B: 128
 // dequant arrivals), empty barriers armed by tcgen05.commit.
 #include <cuda.h>
+
+#include <algorithm>
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 #include <cudaTypedefs.h>
@@ -54,25 +56,31 @@ constexpr int TC_B_BYTES = TC_BN * TC_BK * 2;  // 16 KB
 constexpr int TC_PK = 8;   // packed-weight ring slots (stages of raw bytes per row)
 constexpr int TC_PD = 6;   // cp.async prefetch distance (stages)
 
-template <bool DEC>
-struct TcCfg {
-  static constexpr int MT = DEC ? 1 : 2;          // UMMA M tiles per CTA
-  static constexpr int STAGES = 3;
-  static constexpr int STAGE_BYTES = MT * TC_A_BYTES + TC_B_BYTES;
-  static constexpr int TMEM_COLS = MT * TC_BN;
-};
 // raw bytes of one row per stage (64 weights), and the padded ring stride:
 // a multiple of 16 with an odd 16-byte chunk count (conflict-free LDS.128)
 __host__ __device__ constexpr int tc_sb(int qt, int bs) { return (TC_BK / bs) * q_block_bytes(qt, bs); }
 __host__ __device__ constexpr int tc_sbpad(int qt, int bs) {
   return ((tc_sb(qt, bs) + 15) / 16) % 2 ? ((tc_sb(qt, bs) + 15) / 16) * 16 : ((tc_sb(qt, bs) + 15) / 16 + 1) * 16;
 }
-constexpr int TC_XR = 3;            // decode: raw fp32 x stages (bulk copies), 64 tokens x 64 k each
-constexpr int TC_XR_BYTES = 64 * TC_BK * 4;
+template <bool DEC, int SBPAD = 48>
+struct TcCfg {
+  static constexpr int MT = DEC ? 1 : 2;          // UMMA M tiles per CTA
+  static constexpr int STAGES = (DEC && SBPAD <= 48) ? 4 : 3;
+  static constexpr int STAGE_BYTES = MT * TC_A_BYTES + TC_B_BYTES;
+  static constexpr int TMEM_COLS = MT * TC_BN;
+};
+// decode: raw fp32 x ring, 48 KB of slots of Bpad tokens x 64 k (Bpad = B rounded
+// up to 8/16/32/64): 24 slots at B <= 8 ... 3 at B = 64 (deep L2 prefetch)
+constexpr int TC_XRING = 48 * 1024;
+constexpr int TC_XRMAX = 16;
+__host__ __device__ constexpr int tc_bpad(int B) { return B <= 8 ? 8 : B <= 16 ? 16 : B <= 32 ? 32 : 64; }
+__host__ __device__ constexpr int tc_nxr(int B) {
+  return TC_XRING / (tc_bpad(B) * TC_BK * 4) < TC_XRMAX ? TC_XRING / (tc_bpad(B) * TC_BK * 4) : TC_XRMAX;
+}
 template <bool DEC>
 __host__ __device__ constexpr int tc_smem(int qt, int bs) {
-  return TcCfg<DEC>::STAGES * TcCfg<DEC>::STAGE_BYTES + TC_PK * TC_BN * tc_sbpad(qt, bs) + (DEC ? TC_XR * TC_XR_BYTES : 0) +
-         1024 /*align*/ + 256;
+  return (tc_sbpad(qt, bs) <= 48 ? TcCfg<DEC, 48>::STAGES : TcCfg<DEC, 64>::STAGES) * TcCfg<DEC>::STAGE_BYTES +
+         TC_PK * TC_BN * tc_sbpad(qt, bs) + (DEC ? TC_XRING : 0) + 1024 /*align*/ + 512;
 }
 
 // ---- tcgen05 / TMA PTX wrappers ----------------------------------------------
@@ -252,7 +260,7 @@ __device__ __forceinline__ void dequant_row(const unsigned char* raw, int64_t n,
 // warps; item = (token, 8-element chunk).
 constexpr int TC_CONV = 3;  // converter warps
 template <bool PERM>
-__device__ __forceinline__ void convert_x_tile(const float* xr, int B, unsigned char* atile, int cidx) {
+__device__ __forceinline__ void convert_x_tile(const float* xr, int B, unsigned char* atile, int cidx, int lo_off = 64) {
   const int lane = threadIdx.x & 31;
   for (int t = cidx * 32 + lane; t < B * 8; t += TC_CONV * 32) {
     const int m = t >> 3, c = t & 7;
@@ -270,7 +278,7 @@ __device__ __forceinline__ void convert_x_tile(const float* xr, int B, unsigned 
       h[i] = *reinterpret_cast<const uint32_t*>(&hh);
       l[i] = *reinterpret_cast<const uint32_t*>(&ll);
     }
-    const int mh = m, ml = 64 + m;
+    const int mh = m, ml = lo_off + m;
     *reinterpret_cast<uint4*>(atile + (mh >> 3) * 1024 + (mh & 7) * 128 + ((c ^ (mh & 7)) << 4)) =
         make_uint4(h[0], h[1], h[2], h[3]);
     *reinterpret_cast<uint4*>(atile + (ml >> 3) * 1024 + (ml & 7) * 128 + ((c ^ (ml & 7)) << 4)) =
@@ -278,10 +286,10 @@ __device__ __forceinline__ void convert_x_tile(const float* xr, int B, unsigned 
   }
 }
 
-// one 2D TMA of the fp32 x tile [64 tokens x 64 k] of K-stage ks into a raw-x slot
-// (out-of-range tokens / k are zero-filled by the tensor map)
-__device__ __forceinline__ void issue_x_stage(const CUtensorMap* xmap, int64_t ks, float* xr, uint64_t* bar) {
-  mbar_arrive_expect_tx(bar, TC_XR_BYTES);
+// one 2D TMA of the fp32 x tile [Bpad tokens x 64 k] of K-stage ks into a raw-x
+// slot (out-of-range tokens / k are zero-filled by the tensor map)
+__device__ __forceinline__ void issue_x_stage(const CUtensorMap* xmap, int64_t ks, float* xr, uint64_t* bar, int bpad) {
+  mbar_arrive_expect_tx(bar, (uint32_t)(bpad * TC_BK * 4));
   tma_load_2d(xr, xmap, (int)(ks * TC_BK), 0, bar);
 }
 
@@ -364,20 +372,20 @@ template <int QT, int BS, bool DEC>
 __global__ void __launch_bounds__(TcVar<QT, BS, DEC>::THREADS, 1)
     qgemm_tc_kernel(const __grid_constant__ CUtensorMap xmap, const float* __restrict__ xdec, const uint8_t* __restrict__ W,
                     int64_t N, int64_t K, int64_t M, float* __restrict__ Y, int ksteps_per_split, int atomic_out) {
-  using Cfg = TcCfg<DEC>;
+  using Cfg = TcCfg<DEC, tc_sbpad(QT, BS)>;
   using Var = TcVar<QT, BS, DEC>;
   constexpr int MT = Cfg::MT, STAGES = Cfg::STAGES, STAGE_BYTES = Cfg::STAGE_BYTES;
   constexpr int SBPAD = tc_sbpad(QT, BS);
   extern __shared__ unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   unsigned char* pring = smem + STAGES * STAGE_BYTES;  // [TC_PK][TC_BN][SBPAD] raw weight bytes
-  float* xraw = reinterpret_cast<float*>(pring + TC_PK * TC_BN * SBPAD);  // decode: [TC_XR][64][64] raw x
-  uint64_t* a_full = reinterpret_cast<uint64_t*>(reinterpret_cast<unsigned char*>(xraw) + (DEC ? TC_XR * TC_XR_BYTES : 0));
+  float* xraw = reinterpret_cast<float*>(pring + TC_PK * TC_BN * SBPAD);  // decode: [nxr][Bpad][64] raw x
+  uint64_t* a_full = reinterpret_cast<uint64_t*>(reinterpret_cast<unsigned char*>(xraw) + (DEC ? TC_XRING : 0));
   uint64_t* b_full = a_full + STAGES;
   uint64_t* empty = b_full + STAGES;
   uint64_t* acc_full = empty + STAGES;
-  uint64_t* xr_full = acc_full + 1;  // [TC_XR]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(xr_full + TC_XR);
+  uint64_t* xr_full = acc_full + 1;  // [TC_XRMAX]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(xr_full + TC_XRMAX);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t n0 = (int64_t)blockIdx.x * TC_BN;
@@ -395,7 +403,7 @@ __global__ void __launch_bounds__(TcVar<QT, BS, DEC>::THREADS, 1)
       mbar_init(&empty[s], 1);
     }
     mbar_init(acc_full, 1);
-    for (int i = 0; i < TC_XR; i++) mbar_init(&xr_full[i], 1);
+    for (int i = 0; i < TC_XRMAX; i++) mbar_init(&xr_full[i], 1);
     fence_mbar_init();
   }
   if constexpr (DEC) {
@@ -423,20 +431,19 @@ __global__ void __launch_bounds__(TcVar<QT, BS, DEC>::THREADS, 1)
       // ---------------- converters: x fp32 -> fp16 hi/lo A tiles ----------------
       const int cidx = warp == 0 ? 0 : warp - conv_first + 1;
       const bool issuer = warp == 0 && lane == 0;
+      const int bpad = tc_bpad((int)M), nxr = tc_nxr((int)M), xslot = bpad * TC_BK;
       if (issuer)
-        for (int i = 0; i < TC_XR && i < nks; i++)
-          issue_x_stage(&xmap, ks0 + i, xraw + i * (TC_XR_BYTES / 4), &xr_full[i]);
+        for (int i = 0; i < nxr && i < nks; i++) issue_x_stage(&xmap, ks0 + i, xraw + i * xslot, &xr_full[i], bpad);
       for (int i = 0; i < nks; i++) {
-        const int s = i % STAGES, xs = i % TC_XR;
+        const int s = i % STAGES, xs = i % nxr;
         mbar_wait(&empty[s], ((i / STAGES) & 1) ^ 1);
-        mbar_wait(&xr_full[xs], (i / TC_XR) & 1);
-        convert_x_tile<Var::FAST>(xraw + xs * (TC_XR_BYTES / 4), (int)M, smem + s * STAGE_BYTES, cidx);
+        mbar_wait(&xr_full[xs], (i / nxr) & 1);
+        convert_x_tile<Var::FAST>(xraw + xs * xslot, (int)M, smem + s * STAGE_BYTES, cidx);
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> tensor core reads
         __syncwarp();
         if (lane == 0) mbar_arrive(&a_full[s]);
         named_bar_sync(3, TC_CONV * 32);  // every converter is done with this raw-x slot
-        if (issuer && i + TC_XR < nks)
-          issue_x_stage(&xmap, ks0 + i + TC_XR, xraw + xs * (TC_XR_BYTES / 4), &xr_full[xs]);
+        if (issuer && i + nxr < nks) issue_x_stage(&xmap, ks0 + i + nxr, xraw + xs * xslot, &xr_full[xs], bpad);
       }
     } else if (lane == 0) {
       // ---------------- TMA producer: X tiles ----------------
@@ -607,6 +614,273 @@ __global__ void __launch_bounds__(TcVar<QT, BS, DEC>::THREADS, 1)
   }
 }
 
+// ---- Q3H_B64 half-row dequant, exact Eq. 2 in fp32 (-> fp16), no I2F ----------
+// Thread half h of a row decodes pairs [16h, 16h + 16) (chunks [4h, 4h + 4)) in
+// natural K order.  Per pair: c as a float via the 2^23 magic, q_e = floor(c/11)
+// by an FFMA rounding down onto the 2^23 grid, q_o = c - 11 q_e,
+// w' = fma(q, step, lo): all full-rate FMA/ALU ops.
+__device__ __forceinline__ void dequant_q3h64_half_f32(const unsigned char* raw, bool valid, int h, unsigned char* tile,
+                                                       int r) {
+  uint32_t outw[16];
+  if (valid) {
+    const uint4 v0 = *reinterpret_cast<const uint4*>(raw);
+    const uint4 v1 = *reinterpret_cast<const uint4*>(raw + 16);
+    const uint32_t hdr = v0.x;
+    const uint32_t ca[9] = {v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w, 0u, 0u};
+    uint32_t c[6];  // code-stream bits [112 h, 112 h + 160): compile-time positions for both halves
+#pragma unroll
+    for (int i = 0; i < 5; i++) c[i] = h ? __funnelshift_r(ca[3 + i], ca[4 + i], 16) : ca[i];
+    c[5] = 0u;
+    const float lo = half_bits_to_float(hdr & 0xFFFFu), hi = half_bits_to_float(hdr >> 16);
+    const float step = __fdiv_rn(__fsub_rn(hi, lo), 10.0f);
+    const float M23 = 8388608.0f, r11 = 0.0909090936183929443359375f;  // 2^23, roundup(1/11)
+#pragma unroll
+    for (int jr = 0; jr < 16; jr++) {
+      const int p = 7 * jr;
+      const uint32_t t = (p & 31) ? __funnelshift_r(c[p >> 5], c[(p >> 5) + 1], p & 31) : c[p >> 5];
+      const float cf = __uint_as_float((t & 0x7Fu) | 0x4B000000u) - M23;      // c, exact
+      const float qe = __fmaf_rd(cf, r11, M23) - M23;                            // floor(c / 11)
+      const float qo = __fmaf_rn(qe, -11.0f, cf);                                // c mod 11
+      outw[jr] = pack_f16x2(__fmaf_rn(qe, step, lo), __fmaf_rn(qo, step, lo));
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < 16; i++) outw[i] = 0u;
+  }
+  unsigned char* rowp = tile + (r >> 3) * 1024 + (r & 7) * 128;
+#pragma unroll
+  for (int qq = 0; qq < 4; qq++) {
+    const int cch = 4 * h + qq;
+    *reinterpret_cast<uint4*>(rowp + ((cch ^ (r & 7)) << 4)) =
+        make_uint4(outw[4 * qq], outw[4 * qq + 1], outw[4 * qq + 2], outw[4 * qq + 3]);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// a4 batched decode, weights on the UMMA M side: D[n, j] = sum_k W'[n, k] X[j, k]
+// with M = 128 weight rows and N = 2 Bp columns (x hi of token t in column t,
+// x lo in column Bp + t, Bp = B rounded up to 8/16/32/64; N >= 16).  The x tile
+// is tiny (N rows), so the pipeline holds up to 8 stages; each epilogue thread
+// owns one weight row and adds its hi and lo columns (no exchange), and the y
+// stores are coalesced along n.
+constexpr int TCD_MAXST = 8;
+constexpr int TCD_XRING = 32 * 1024;
+__host__ __device__ constexpr int tcd_ncols(int B) { return 2 * tc_bpad(B) < 16 ? 16 : 2 * tc_bpad(B); }
+__host__ __device__ constexpr int tcd_stage_bytes(int B) { return TC_B_BYTES + tcd_ncols(B) * 128; }
+__host__ __device__ constexpr int tcd_nxr(int B) {
+  return TCD_XRING / (tc_bpad(B) * TC_BK * 4) < TC_XRMAX ? TCD_XRING / (tc_bpad(B) * TC_BK * 4) : TC_XRMAX;
+}
+
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+// epilogue of the decode kernel (warps 2-5): lane = weight row, y[t, n] = D[n, t] + D[n, bp + t]
+__device__ __forceinline__ void qgemv_epilogue(uint32_t tmem, uint64_t* acc_full, float* __restrict__ Y, int64_t N,
+                                               int B, int bp, int64_t n0, int nks, int atomic_out, int warp, int lane) {
+  mbar_wait(acc_full, 0);
+  tc_fence_after();
+  const int q = warp & 3;  // TMEM lane quarter
+  const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16);
+  const int64_t nn = n0 + q * 32 + lane;
+  for (int t0 = 0; t0 < B; t0 += 16) {
+    uint32_t hv[16], lv[16];
+    tmem_ld16(tbase + t0, hv);
+    tmem_ld16(tbase + bp + t0, lv);  // bp = 8: columns 8..23 (16..23 unused, allocated)
+    if (nn < N && nks > 0) {
+#pragma unroll
+      for (int j = 0; j < 16; j++) {
+        if (t0 + j < B) {
+          const float v = __uint_as_float(hv[j]) + __uint_as_float(lv[j]);
+          float* dst = Y + (int64_t)(t0 + j) * N + nn;
+          if (atomic_out) atomicAdd(dst, v);
+          else *dst = v;
+        }
+      }
+    }
+  }
+  tc_fence_before();
+}
+
+// the 8-warp Q3H_B64 dequant loop: warp w in 2..9 owns rows [16 (w - 2), +16), lane
+// pair (2i, 2i + 1) = the two halves of row 16 (w - 2) + i; each half copies its
+// 16 bytes of the block with cp.async, and __syncwarp makes the partner's visible
+template <int QT, int BS>
+__device__ __forceinline__ void qgemv_fast_deq(const uint8_t* __restrict__ W, int64_t N, int64_t K, int64_t nb,
+                                               int64_t n0, int ks0, int nks, int stages, int stage_bytes,
+                                               unsigned char* smem, unsigned char* pring, uint64_t* empty,
+                                               uint64_t* b_full, int warp, int lane) {
+  constexpr int SBPAD = tc_sbpad(QT, BS);
+  const int lst = 31 - __clz(stages);
+  const int r = (warp - 2) * 16 + (lane >> 1), h = lane & 1;
+  const int64_t n = n0 + r;
+  unsigned char* myrow = pring + r * SBPAD;
+  auto pre = [&](int i) {
+    const int64_t ks = ks0 + i;
+    if (n < N && ks * TC_BK < K) cp_async16(myrow + (i % TC_PK) * TC_BN * SBPAD + 16 * h, W + (n * nb + ks) * 32 + 16 * h);
+  };
+#pragma unroll
+  for (int i = 0; i < TC_PD; i++) {
+    if (i < nks) pre(i);
+    cp_async_commit();
+  }
+  for (int i = 0; i < nks; i++) {
+    const int s = (i & (stages - 1));
+    if (i + TC_PD < nks) pre(i + TC_PD);
+    cp_async_commit();
+    cp_async_wait<TC_PD>();
+    __syncwarp();  // the partner lane's half of the block is visible
+    mbar_wait(&empty[s], ((i >> lst) & 1) ^ 1);
+    dequant_q3h64_half_f32(myrow + (i % TC_PK) * TC_BN * SBPAD, n < N && (int64_t)(ks0 + i) * TC_BK < K, h,
+                           smem + s * stage_bytes, r);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> tensor core reads
+    mbar_arrive(&b_full[s]);
+    __syncwarp();  // both halves read before the ring slot is refilled
+  }
+  cp_async_wait<0>();
+}
+
+template <int QT, int BS>
+struct TcdVar {
+  static constexpr bool FAST = QT == 35 && BS == 64;  // 8 dequant warps, two threads per row
+  static constexpr int THREADS = FAST ? 384 : 256;
+  static constexpr int NDEQ = FAST ? 256 : 128;
+  static constexpr int CONV1 = FAST ? 10 : 6;  // first converter warp after warp 0
+};
+
+template <int QT, int BS>
+__global__ void __launch_bounds__(TcdVar<QT, BS>::THREADS, 1)
+    qgemv_tc_kernel(const __grid_constant__ CUtensorMap xmap, const uint8_t* __restrict__ W, int64_t N, int64_t K,
+                    int B, float* __restrict__ Y, int ksteps_per_split, int atomic_out, int stages) {
+  constexpr int SBPAD = tc_sbpad(QT, BS);
+  using V = TcdVar<QT, BS>;
+  const int bp = tc_bpad(B), ncols = tcd_ncols(B), stage_bytes = tcd_stage_bytes(B);
+  const int nxr = tcd_nxr(B), xslot = bp * TC_BK;
+  const int lst = 31 - __clz(stages), lxr = 31 - __clz(nxr);  // both powers of two
+  extern __shared__ unsigned char smem_raw[];
+  unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // stage s: W' tile (A, 128 rows) at smem + s * stage_bytes, x tile (B, ncols rows) right after
+  unsigned char* pring = smem + stages * stage_bytes;                       // [TC_PK][128][SBPAD]
+  float* xraw = reinterpret_cast<float*>(pring + TC_PK * TC_BN * SBPAD);   // [nxr][bp][64]
+  uint64_t* a_full = reinterpret_cast<uint64_t*>(reinterpret_cast<unsigned char*>(xraw) + TCD_XRING);  // x ready
+  uint64_t* b_full = a_full + TCD_MAXST;  // W' ready
+  uint64_t* empty = b_full + TCD_MAXST;
+  uint64_t* acc_full = empty + TCD_MAXST;
+  uint64_t* xr_full = acc_full + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(xr_full + TC_XRMAX);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t n0 = (int64_t)blockIdx.x * TC_BN;
+  const int64_t nb = K / BS;
+  const int ktotal = (int)((K + TC_BK - 1) / TC_BK);
+  const int ks0 = blockIdx.z * ksteps_per_split;
+  const int nks = max(min(ktotal, ks0 + ksteps_per_split) - ks0, 0);
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < stages; s++) {
+      mbar_init(&a_full[s], TC_CONV);
+      mbar_init(&b_full[s], V::NDEQ);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(acc_full, 1);
+    for (int i = 0; i < TC_XRMAX; i++) mbar_init(&xr_full[i], 1);
+    fence_mbar_init();
+  }
+  // x tiles: rows of tokens >= B (hi and lo) are never written -> zero them once
+  for (int s = 0; s < stages; s++)
+    for (int i = threadIdx.x; i < ncols * 8; i += blockDim.x)
+      reinterpret_cast<uint4*>(smem + s * stage_bytes + TC_B_BYTES)[i] = make_uint4(0u, 0u, 0u, 0u);
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)), "n"(128)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0 || warp >= V::CONV1) {
+    // ---------------- converters: raw fp32 x (2D TMA ring) -> fp16 hi/lo x tiles ----------------
+    const int cidx = warp == 0 ? 0 : warp - V::CONV1 + 1;
+    const bool issuer = warp == 0 && lane == 0;
+    if (issuer)
+      for (int i = 0; i < nxr && i < nks; i++) issue_x_stage(&xmap, ks0 + i, xraw + i * xslot, &xr_full[i], bp);
+    for (int i = 0; i < nks; i++) {
+      const int s = (i & (stages - 1)), xs = (i & (nxr - 1));
+      mbar_wait(&empty[s], ((i >> lst) & 1) ^ 1);
+      mbar_wait(&xr_full[xs], (i >> lxr) & 1);
+      convert_x_tile<false>(xraw + xs * xslot, B, smem + s * stage_bytes + TC_B_BYTES, cidx, bp);
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> tensor core reads
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&a_full[s]);
+      named_bar_sync(3, TC_CONV * 32);  // every converter is done with this raw-x slot
+      if (issuer && i + nxr < nks) issue_x_stage(&xmap, ks0 + i + nxr, xraw + xs * xslot, &xr_full[xs], bp);
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer (one thread): A = W' (M = 128), B = x (N = ncols) ----------------
+    if (lane == 0) {
+      const uint32_t idesc = umma_idesc_f16(TC_BN, ncols);
+      for (int i = 0; i < nks; i++) {
+        const int s = (i & (stages - 1));
+        const uint32_t par = (i >> lst) & 1;
+        mbar_wait(&a_full[s], par);
+        mbar_wait(&b_full[s], par);
+        tc_fence_after();
+        const uint32_t st = smem_u32(smem + s * stage_bytes);
+        const uint64_t adesc0 = umma_desc_sw128(st), bdesc0 = umma_desc_sw128(st + TC_B_BYTES);
+#pragma unroll
+        for (int kk = 0; kk < TC_BK / 16; kk++)
+          umma_bf16(tmem, adesc0 + (uint64_t)(kk * 2), bdesc0 + (uint64_t)(kk * 2), idesc, (i > 0) || (kk > 0));
+        umma_commit(&empty[s]);
+      }
+      umma_commit(acc_full);
+    }
+  } else if (V::FAST && warp >= 6) {
+    // ---------------- Q3H_B64 dequantizers, second half of the 8 warps ----------------
+    // (warps 2-9: 16 rows each, lane pairs = the two halves of a row; warps 2-5
+    //  run the epilogue below after the same loop)
+    qgemv_fast_deq<QT, BS>(W, N, K, nb, n0, ks0, nks, stages, stage_bytes, smem, pring, empty, b_full, warp, lane);
+  } else if (V::FAST) {
+    qgemv_fast_deq<QT, BS>(W, N, K, nb, n0, ks0, nks, stages, stage_bytes, smem, pring, empty, b_full, warp, lane);
+    qgemv_epilogue(tmem, acc_full, Y, N, B, bp, n0, nks, atomic_out, warp, lane);
+  } else {
+    // ---------------- dequantizers: one weight row per thread (Eq. 2 in fp32, -> fp16) ----------------
+    const int r = threadIdx.x - 64;  // 0..127
+    const int64_t n = n0 + r;
+    unsigned char* myring = pring + r * SBPAD;
+#pragma unroll
+    for (int i = 0; i < TC_PD; i++) {
+      if (i < nks) prefetch_row<QT, BS>(W, nb, n, N, ks0 + i, K, myring + (i % TC_PK) * TC_BN * SBPAD);
+      cp_async_commit();
+    }
+    for (int i = 0; i < nks; i++) {
+      const int s = (i & (stages - 1));
+      if (i + TC_PD < nks) prefetch_row<QT, BS>(W, nb, n, N, ks0 + i + TC_PD, K, myring + ((i + TC_PD) % TC_PK) * TC_BN * SBPAD);
+      cp_async_commit();
+      cp_async_wait<TC_PD>();
+      mbar_wait(&empty[s], ((i >> lst) & 1) ^ 1);
+      dequant_row<QT, BS, true>(myring + (i % TC_PK) * TC_BN * SBPAD, n, N, (int64_t)(ks0 + i) * TC_BK, K,
+                                smem + s * stage_bytes, r);
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> tensor core reads
+      mbar_arrive(&b_full[s]);
+    }
+    cp_async_wait<0>();
+    qgemv_epilogue(tmem, acc_full, Y, N, B, bp, n0, nks, atomic_out, warp, lane);
+  }
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(128) : "memory");
+  }
+}
+
 // ---------------------------------------------------------------------------
 static PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
 
@@ -693,17 +967,44 @@ if_status qgemv_tc_launch(if_scheme s, const uint8_t* W, int64_t N, int64_t K, c
                           int accumulate, cudaStream_t st) {
   if (B < 1 || B > 64 || K % 8 != 0 || (reinterpret_cast<uintptr_t>(x) & 15u) || N > (int64_t)1 << 30)
     return IF_ERR_UNSUPPORTED;
+  const int64_t row_bytes = K / s.block * q_block_bytes(s.type, s.block);
+  if ((row_bytes & 3) || (reinterpret_cast<uintptr_t>(W) & 3u)) return IF_ERR_UNSUPPORTED;
   if (!get_encoder()) return IF_ERR_UNSUPPORTED;
-  CUtensorMap map;  // x fp32 [B, K], tiles of 64 tokens x 64 k, no swizzle (the converter reads it)
+  CUtensorMap map;  // x fp32 [B, K], tiles of Bpad tokens x 64 k, no swizzle (the converter reads it)
   cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)B};
   cuuint64_t strides[1] = {(cuuint64_t)K * 4};
-  cuuint32_t box[2] = {(cuuint32_t)TC_BK, 64u};
+  cuuint32_t box[2] = {(cuuint32_t)TC_BK, (cuuint32_t)tc_bpad((int)B)};
   cuuint32_t estr[2] = {1, 1};
   CUresult cr = g_encode(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(x), dims, strides, box, estr,
                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (cr != CUDA_SUCCESS) return set_error(IF_ERR_CUDA, "qgemv_tc: cuTensorMapEncodeTiled failed (%d)", (int)cr);
-  return tc_run<true>(s, map, x, W, N, K, B, Y, accumulate, st);
+  const int ntile = (int)((N + TC_BN - 1) / TC_BN);
+  const int ktotal = (int)((K + TC_BK - 1) / TC_BK);
+  const int splits = tc_splits(ntile, ktotal);
+  const int kper = (ktotal + splits - 1) / splits;
+  const int atomic_out = (splits > 1) || accumulate;
+  if (splits > 1 && !accumulate) {
+    if (cudaMemsetAsync(Y, 0, sizeof(float) * B * N, st) != cudaSuccess) return check_launch("qgemv_tc memset");
+  }
+  return dispatch_scheme(s, [&]<int QT, int BS>() -> if_status {
+    auto kern = qgemv_tc_kernel<QT, BS>;
+    constexpr int fixed = TC_PK * TC_BN * tc_sbpad(QT, BS) + TCD_XRING + 1024 + 512;
+    const int sb = tcd_stage_bytes((int)B);
+    int stages = std::min(TCD_MAXST, (227 * 1024 - fixed) / sb);
+    stages = stages >= 8 ? 8 : stages >= 4 ? 4 : stages >= 2 ? 2 : 0;  // a power of two (shift/mask indexing)
+    if (stages < 2) return IF_ERR_UNSUPPORTED;
+    const int smem = stages * sb + fixed;
+    static bool configured = false;
+    if (!configured) {
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+      configured = true;
+    }
+    dim3 grid(ntile, 1, splits);
+    kern<<<grid, TcdVar<QT, BS>::THREADS, smem, st>>>(map, W, N, K, (int)B, Y, kper, atomic_out, stages);
+    count_launch();
+    return check_launch("qgemv_tc");
+  });
 }
 
 }  // namespace ifb
