@@ -185,7 +185,9 @@ extern "C" if_status if_run_stack(const if_stack_shape* shape, const if_plan* pl
   }
   const int nlayers = asg.layer_end - asg.layer_begin;
   // batch-1 Q3H_B64 decode on one TP rank: the whole stage in ONE persistent launch
-  const bool mk = mode == IF_DECODE && T == 1 && sc.type == IF_Q3H && sc.block == 64 && groups == 1 &&
+  // (batch 2..6: one engine launch per token beats the tensor-core path, whose
+  //  per-launch cost dominates at small B; both stream the weights from HBM)
+  const bool mk = mode == IF_DECODE && T <= 6 && sc.type == IF_Q3H && sc.block == 64 && groups == 1 &&
                   nlayers <= MK_MAXL && nlayers > 0;
   if (mk) {
     static thread_local MkParams P;
@@ -224,7 +226,12 @@ extern "C" if_status if_run_stack(const if_stack_shape* shape, const if_plan* pl
       P.w[l][2] = Wl.wgu;
       P.w[l][3] = Wl.wdown;
     }
-    st = mk_launch(P, cs);
+    for (int64_t t = 0; t < T; t++) {
+      P.h = h_out + t * L.d;
+      P.last_qkv = last_qkv ? last_qkv + t * L.nqkv : nullptr;
+      st = mk_launch(P, cs);
+      if (st) break;
+    }
     if (st != IF_ERR_UNSUPPORTED) {
       if (st) return st;
       if (!last) {
