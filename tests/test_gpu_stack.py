@@ -45,10 +45,22 @@ def _oracle(cfg, qtype, bs, stk, h):
 
 
 @pytest.mark.parametrize("qtype,bs", [(35, 64), (4, 32), (3, 32), (8, 64), (2, 64)])
-@pytest.mark.parametrize("T", [1, 4])
+@pytest.mark.parametrize("T", [1, 4, 7, 16])
 def test_stack_decode_small(qtype, bs, T):
+    """T <= 6 (Q3H_B64): the persistent engine once per token; T >= 7: the tensor-core
+    batched qGEMV (fp16 W', fp16 hi/lo x, Q23) -- both held to 1e-3."""
     stk, h, out, qkv = _run(SMALL, qtype, bs, T)
     ho, qo = _oracle(SMALL, qtype, bs, stk, h)
+    assert normwise(out, ho) <= 1e-3
+    assert normwise(qkv, qo) <= 1e-3
+
+
+def test_stack_decode_batch64_7b_layer():
+    """Batch 64 (the top of the decode range, BASELINE configs[4] batch sweep) on one
+    7B-shaped layer: the tensor-core decode path at full width."""
+    cfg = dict(synth.LLAMA["7b"], layers=1)
+    stk, h, out, qkv = _run(cfg, 35, 64, 64)
+    ho, qo = _oracle(cfg, 35, 64, stk, h)
     assert normwise(out, ho) <= 1e-3
     assert normwise(qkv, qo) <= 1e-3
 
