@@ -12,9 +12,10 @@ HBM (no flush needed).  The step is replayed from a CUDA graph.
   python bench.py [--gpus N] [--steps K] [--warmup W] [--batch B] [--model 7b]
   python bench.py --impl reference ...     (the CPU oracle)
 
-N > 1 (torchrun, one process per GPU): the same stack partitioned by tensor
-(default) or --strategy layer|hybrid, merges through the peer-memory
-communicator; value = tokens/s of the job, time = max over ranks.
+N > 1 (torchrun, one process per GPU): the same stack partitioned by layer
+(default: each stage one persistent engine launch, hand-off through the
+peer-memory communicator) or --strategy tensor|hybrid (per-layer kernels +
+peer-memory merges); value = tokens/s of the job, time = max over ranks.
 """
 from __future__ import annotations
 
@@ -182,12 +183,20 @@ def run_ours(args):
     from paper_2401_08294_b200.model import Stack
 
     ws, rank, local = dist_env()
+    # IFB_BENCH_SHARE_GPU=1: every rank on cuda:0, gloo plumbing (a functional check
+    # of the N-rank path on a 1-GPU box; its timing is not a scaling number)
+    share = os.environ.get("IFB_BENCH_SHARE_GPU") == "1"
+    if share:
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     dist = None
     if ws > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=dev)
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
     hbm_peak, bf16_peak, peak_kind = peaks()
     cfg = synth.LLAMA[args.model]
     s = F.scheme("Q3H", 64)
@@ -235,6 +244,7 @@ def run_ours(args):
     torch.cuda.synchronize()
 
     def barrier():
+        torch.cuda.synchronize()
         if dist:
             dist.barrier()
         torch.cuda.synchronize()
@@ -253,7 +263,7 @@ def run_ours(args):
     barrier()
     ms = e0.elapsed_time(e1)
     if dist:
-        t = torch.tensor([ms], device=dev)
+        t = torch.tensor([ms], device="cpu" if share else dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
     ms_per_step = ms / args.steps
@@ -283,7 +293,7 @@ def run_ours(args):
     f1.synchronize()
     ms_e2e = f0.elapsed_time(f1)
     if dist:
-        t = torch.tensor([ms_e2e], device=dev)
+        t = torch.tensor([ms_e2e], device="cpu" if share else dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms_e2e = float(t.item())
     e2e = {"value": B * args.steps / (ms_e2e / 1e3), "unit": "tokens/s", "h2d_bytes_per_step": B * d * 4,
@@ -349,7 +359,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--batch", type=int, default=1)
     ap.add_argument("--model", default="7b", choices=["7b", "13b", "70b"])
-    ap.add_argument("--strategy", default="tensor", choices=["tensor", "layer", "hybrid"])
+    # N > 1 default: by layer -- every stage runs the persistent decode engine; by
+    # tensor / hybrid run the per-layer kernels + peer-memory merges
+    ap.add_argument("--strategy", default="layer", choices=["tensor", "layer", "hybrid"])
     ap.add_argument("--stages", type=int, default=0)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")

@@ -38,10 +38,14 @@ for it in range(4):
     torch.cuda.synchronize()
     print("launch us", e0.elapsed_time(e1) * 1e3)
 L.ifx_set_mk_debug(None)
-dd = dbg.view(G, nph, 16).cpu().numpy().astype(np.float64)
+raw = dbg.view(G, nph, 16).cpu().numpy()
+dd = np.zeros(raw.shape)
+dd[:, :, :8] = (raw[:, :, :8] - raw[:, 0, 0].min()).astype(np.float64)
+dd[:, :, 8:] = (raw[:, :, 8:] - raw[:, 0, 8].min()).astype(np.float64)
 d = dd[:, :, :8].copy()
 ck = dd[:, :, 8:] / 1965.0  # us at max clock
-d = (d - d[:, 0, 0].min()) / 1e3
+d = d / 1e3
+d[:, 0, 1] = d[:, 0, 0]  # phase 0 has no dependency stamp
 print("total span", d[:, -1, 5].max() - d[:, 0, 0].min())
 kinds = ["qkv", "o", "gu", "down"]
 rows = {k: [] for k in range(4)}
