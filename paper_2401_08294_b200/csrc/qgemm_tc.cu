@@ -43,12 +43,9 @@ constexpr int TC_THREADS = 256;
 // arithmetic), converters on warps 0, 10, 11 -> 12 warps
 template <int QT, int BS, bool DEC>
 struct TcVar {
-#ifdef IFB_TC_FASTQ3H
-  static constexpr bool FAST = DEC && QT == 35 && BS == 64;  // fp16 arithmetic: ~2x the W' rounding error
-#else
-  static constexpr bool FAST = false;
-#endif
-  static constexpr int THREADS = FAST ? 384 : 256;
+  // prefill Q3H_B64: 8 dequant warps (two threads per weight row, exact fp32 Eq. 2)
+  static constexpr bool FAST = !DEC && QT == 35 && BS == 64;
+  static constexpr int THREADS = FAST ? 320 : 256;
   static constexpr int NDEQ = FAST ? 256 : 128;  // dequant threads (b_full arrivals)
 };
 constexpr int TC_A_BYTES = TC_BM * TC_BK * 2;  // 16 KB per M tile
@@ -293,73 +290,41 @@ __device__ __forceinline__ void issue_x_stage(const CUtensorMap* xmap, int64_t k
   tma_load_2d(xr, xmap, (int)(ks * TC_BK), 0, bar);
 }
 
-// ---- fast Q3H_B64 dequant to fp16 (decode mode), two threads per row ---------
-// Half h of the row's 32-byte block (header lo|hi fp16, 7-bit pair codes from
-// byte 4) -> pairs [16h, 16h + 16) -> 16-byte chunks [4h, 4h + 4) of
-// the SW128 row.  Codes (4q + d, 4q + 2 + d) share one half2 lane pair:
-//   h2 = (c_a | 0x6400, c_b | 0x6400)          = (1024 + c_a, 1024 + c_b)
-//   q_e = RN((c - 5) / 11) = floor(c / 11)      (|(c - 5) / 11 - m| <= 5/11 and the
-//       = HFMA2(c, 1/11, -5/11) + 1536 - 1536    fp16 evaluation error is < 0.01: checked for all c)
-//   q_o = c - 11 q_e, exact in fp16
-//   w'  = q step_hi + (q step_lo + lo)          (Eq. 2 in fp16, step split hi + lo: ~fp16(w') )
-// K order inside a chunk (matched by the converter's x permutation):
-//   we(4q), we(4q+2), wo(4q), wo(4q+2), we(4q+1), we(4q+3), wo(4q+1), wo(4q+3)
-__device__ __forceinline__ uint32_t h2u(__half2 v) { return *reinterpret_cast<uint32_t*>(&v); }
-__device__ __forceinline__ __half2 u2h(uint32_t v) { return *reinterpret_cast<__half2*>(&v); }
-// stream bits [p, p + 32) of the code area (words c[0..7], c[7] = 0)
-__device__ __forceinline__ uint32_t code_bits(const uint32_t (&c)[8], int p) {
-  const int wi = p >> 5, sh = p & 31;
-  return sh ? __funnelshift_r(c[wi], c[wi + 1], sh) : c[wi];
-}
-__device__ __forceinline__ void dequant_q3h64_half(const unsigned char* raw, bool valid, int h, unsigned char* btile,
-                                                   int r) {
+// ---- Q3H_B64 half-row dequant, exact Eq. 2 in fp32 (-> fp16 / bf16), no I2F -------
+// Thread half h of a row decodes pairs [16h, 16h + 16) (chunks [4h, 4h + 4)) in
+// natural K order.  Per pair: c as a float via the 2^23 magic, q_e = floor(c/11)
+// by an FFMA rounding down onto the 2^23 grid (P:132), q_o = c - 11 q_e (P:133),
+// w' = fma(q, step, lo) (P:110-113): all full-rate FMA/ALU ops.
+template <bool BF16>
+__device__ __forceinline__ void dequant_q3h64_half_f32(const unsigned char* raw, bool valid, int h, unsigned char* tile,
+                                                       int r) {
   uint32_t outw[16];
   if (valid) {
     const uint4 v0 = *reinterpret_cast<const uint4*>(raw);
     const uint4 v1 = *reinterpret_cast<const uint4*>(raw + 16);
     const uint32_t hdr = v0.x;
-    // code-stream window of this half: bits [112 h, 112 h + 160), so that every code
-    // position below is a compile-time constant for both halves
     const uint32_t ca[9] = {v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w, 0u, 0u};
-    uint32_t c[6];
+    uint32_t c[6];  // code-stream bits [112 h, 112 h + 160): compile-time positions for both halves
 #pragma unroll
     for (int i = 0; i < 5; i++) c[i] = h ? __funnelshift_r(ca[3 + i], ca[4 + i], 16) : ca[i];
     c[5] = 0u;
     const float lo = half_bits_to_float(hdr & 0xFFFFu), hi = half_bits_to_float(hdr >> 16);
-    const float stepf = __fdiv_rn(__fsub_rn(hi, lo), 10.0f);
-    const __half2 step2 = __float2half2_rn(stepf);  // step = step2 + stepl2 to ~22 bits
-    const __half2 stepl2 = __float2half2_rn(stepf - __low2float(step2));
-    const __half2 lo2 = u2h((hdr & 0xFFFFu) | (hdr << 16));
-    const __half2 k11 = __float2half2_rn(1.0f / 11.0f), kb = __float2half2_rn(-5.0f / 11.0f);
-    const __half2 k1536 = __float2half2_rn(1536.0f), k1024 = __float2half2_rn(1024.0f), km11 = __float2half2_rn(-11.0f);
+    const float step = __fdiv_rn(__fsub_rn(hi, lo), 10.0f);
+    const float M23 = 8388608.0f, r11 = 0.0909090936183929443359375f;  // 2^23, roundup(1/11)
 #pragma unroll
-    for (int qq = 0; qq < 4; qq++) {
-#pragma unroll
-      for (int dd = 0; dd < 2; dd++) {
-        const int jr = 4 * qq + dd;  // codes 16h + jr and 16h + jr + 2
-        const int p = 7 * jr;
-        const uint32_t t = (p & 31) ? __funnelshift_r(c[p >> 5], c[(p >> 5) + 1], p & 31) : c[p >> 5];
-        uint32_t ub;
-        if (jr == 0) {
-          ub = t << 2;  // code jr + 2 from bits 14..20 to 16..22
-        } else {
-          const int p2 = p - 2;
-          ub = (p2 & 31) ? __funnelshift_r(c[p2 >> 5], c[(p2 >> 5) + 1], p2 & 31) : c[p2 >> 5];
-        }
-        const __half2 hh = u2h((ub & 0x007F0000u) | (t & 0x7Fu) | 0x64006400u);
-        const __half2 c2 = __hsub2(hh, k1024);  // (c_a, c_b), exact
-        const __half2 rr = __hadd2(__hfma2(c2, k11, kb), k1536);
-        const __half2 qe = __hsub2(rr, k1536);
-        const __half2 qo = __hfma2(qe, km11, c2);
-        outw[qq * 4 + 2 * dd] = h2u(__hfma2(qe, step2, __hfma2(qe, stepl2, lo2)));
-        outw[qq * 4 + 2 * dd + 1] = h2u(__hfma2(qo, step2, __hfma2(qo, stepl2, lo2)));
-      }
+    for (int jr = 0; jr < 16; jr++) {
+      const int p = 7 * jr;
+      const uint32_t t = (p & 31) ? __funnelshift_r(c[p >> 5], c[(p >> 5) + 1], p & 31) : c[p >> 5];
+      const float cf = __uint_as_float((t & 0x7Fu) | 0x4B000000u) - M23;      // c, exact
+      const float qe = __fmaf_rd(cf, r11, M23) - M23;                            // floor(c / 11)
+      const float qo = __fmaf_rn(qe, -11.0f, cf);                                // c mod 11
+      outw[jr] = pack16x2<!BF16>(__fmaf_rn(qe, step, lo), __fmaf_rn(qo, step, lo));
     }
   } else {
 #pragma unroll
     for (int i = 0; i < 16; i++) outw[i] = 0u;
   }
-  unsigned char* rowp = btile + (r >> 3) * 1024 + (r & 7) * 128;
+  unsigned char* rowp = tile + (r >> 3) * 1024 + (r & 7) * 128;
 #pragma unroll
   for (int qq = 0; qq < 4; qq++) {
     const int cch = 4 * h + qq;
@@ -425,7 +390,7 @@ __global__ void __launch_bounds__(TcVar<QT, BS, DEC>::THREADS, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  const int conv_first = Var::FAST ? 10 : 6;  // converter warps: 0 and conv_first..
+  const int conv_first = 6;  // decode-mode converter warps: 0 and 6, 7
   if (warp == 0 || (DEC && warp >= conv_first)) {
     if constexpr (DEC) {
       // ---------------- converters: x fp32 -> fp16 hi/lo A tiles ----------------
@@ -438,7 +403,7 @@ __global__ void __launch_bounds__(TcVar<QT, BS, DEC>::THREADS, 1)
         const int s = i % STAGES, xs = i % nxr;
         mbar_wait(&empty[s], ((i / STAGES) & 1) ^ 1);
         mbar_wait(&xr_full[xs], (i / nxr) & 1);
-        convert_x_tile<Var::FAST>(xraw + xs * xslot, (int)M, smem + s * STAGE_BYTES, cidx);
+        convert_x_tile<false>(xraw + xs * xslot, (int)M, smem + s * STAGE_BYTES, cidx);
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> tensor core reads
         __syncwarp();
         if (lane == 0) mbar_arrive(&a_full[s]);
@@ -484,11 +449,10 @@ __global__ void __launch_bounds__(TcVar<QT, BS, DEC>::THREADS, 1)
       umma_commit(acc_full);
     }
   } else if (Var::FAST && warp < 10) {
-    // ---------------- fast Q3H_B64 dequantizers: two threads per row ----------------
-    const int dw = warp - 2;                     // 0..7, 16 rows each
-    const int r = dw * 16 + (lane >> 1), h = lane & 1;
+    // ---------------- Q3H_B64 dequantizers: two threads per row (warps 2-9) ----------------
+    const int r = (warp - 2) * 16 + (lane >> 1), h = lane & 1;
     const int64_t n = n0 + r;
-    unsigned char* myrow = pring + r * SBPAD;  // this row's slot 0; half h copies bytes [16h, 16h + 16)
+    unsigned char* myrow = pring + r * SBPAD;  // half h copies bytes [16h, 16h + 16) of the block
     auto pre = [&](int i) {
       const int64_t ks = ks0 + i;
       if (n < N && ks * TC_BK < K) cp_async16(myrow + (i % TC_PK) * TC_BN * SBPAD + 16 * h, W + (n * nb + ks) * 32 + 16 * h);
@@ -505,11 +469,11 @@ __global__ void __launch_bounds__(TcVar<QT, BS, DEC>::THREADS, 1)
       cp_async_wait<TC_PD>();
       __syncwarp();  // the partner lane's half of the block is visible
       mbar_wait(&empty[s], ((i / STAGES) & 1) ^ 1);
-      unsigned char* btile = smem + s * STAGE_BYTES + MT * TC_A_BYTES;
-      dequant_q3h64_half(myrow + (i % TC_PK) * TC_BN * SBPAD, n < N && (int64_t)(ks0 + i) * TC_BK < K, h, btile, r);
+      dequant_q3h64_half_f32<true>(myrow + (i % TC_PK) * TC_BN * SBPAD, n < N && (int64_t)(ks0 + i) * TC_BK < K, h,
+                                   smem + s * STAGE_BYTES + MT * TC_A_BYTES, r);
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> tensor core reads
       mbar_arrive(&b_full[s]);
-      __syncwarp();  // both halves read before the partner overwrites (ring reuse)
+      __syncwarp();  // both halves read before the ring slot is refilled
     }
     cp_async_wait<0>();
   } else if (!Var::FAST && warp < 6) {
@@ -614,48 +578,6 @@ __global__ void __launch_bounds__(TcVar<QT, BS, DEC>::THREADS, 1)
   }
 }
 
-// ---- Q3H_B64 half-row dequant, exact Eq. 2 in fp32 (-> fp16), no I2F ----------
-// Thread half h of a row decodes pairs [16h, 16h + 16) (chunks [4h, 4h + 4)) in
-// natural K order.  Per pair: c as a float via the 2^23 magic, q_e = floor(c/11)
-// by an FFMA rounding down onto the 2^23 grid (P:132), q_o = c - 11 q_e (P:133),
-// w' = fma(q, step, lo) (P:110-113): all full-rate FMA/ALU ops.
-__device__ __forceinline__ void dequant_q3h64_half_f32(const unsigned char* raw, bool valid, int h, unsigned char* tile,
-                                                       int r) {
-  uint32_t outw[16];
-  if (valid) {
-    const uint4 v0 = *reinterpret_cast<const uint4*>(raw);
-    const uint4 v1 = *reinterpret_cast<const uint4*>(raw + 16);
-    const uint32_t hdr = v0.x;
-    const uint32_t ca[9] = {v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w, 0u, 0u};
-    uint32_t c[6];  // code-stream bits [112 h, 112 h + 160): compile-time positions for both halves
-#pragma unroll
-    for (int i = 0; i < 5; i++) c[i] = h ? __funnelshift_r(ca[3 + i], ca[4 + i], 16) : ca[i];
-    c[5] = 0u;
-    const float lo = half_bits_to_float(hdr & 0xFFFFu), hi = half_bits_to_float(hdr >> 16);
-    const float step = __fdiv_rn(__fsub_rn(hi, lo), 10.0f);
-    const float M23 = 8388608.0f, r11 = 0.0909090936183929443359375f;  // 2^23, roundup(1/11)
-#pragma unroll
-    for (int jr = 0; jr < 16; jr++) {
-      const int p = 7 * jr;
-      const uint32_t t = (p & 31) ? __funnelshift_r(c[p >> 5], c[(p >> 5) + 1], p & 31) : c[p >> 5];
-      const float cf = __uint_as_float((t & 0x7Fu) | 0x4B000000u) - M23;      // c, exact
-      const float qe = __fmaf_rd(cf, r11, M23) - M23;                            // floor(c / 11)
-      const float qo = __fmaf_rn(qe, -11.0f, cf);                                // c mod 11
-      outw[jr] = pack_f16x2(__fmaf_rn(qe, step, lo), __fmaf_rn(qo, step, lo));
-    }
-  } else {
-#pragma unroll
-    for (int i = 0; i < 16; i++) outw[i] = 0u;
-  }
-  unsigned char* rowp = tile + (r >> 3) * 1024 + (r & 7) * 128;
-#pragma unroll
-  for (int qq = 0; qq < 4; qq++) {
-    const int cch = 4 * h + qq;
-    *reinterpret_cast<uint4*>(rowp + ((cch ^ (r & 7)) << 4)) =
-        make_uint4(outw[4 * qq], outw[4 * qq + 1], outw[4 * qq + 2], outw[4 * qq + 3]);
-  }
-}
-
 // ---------------------------------------------------------------------------
 // a4 batched decode, weights on the UMMA M side: D[n, j] = sum_k W'[n, k] X[j, k]
 // with M = 128 weight rows and N = 2 Bp columns (x hi of token t in column t,
@@ -736,8 +658,8 @@ __device__ __forceinline__ void qgemv_fast_deq(const uint8_t* __restrict__ W, in
     cp_async_wait<TC_PD>();
     __syncwarp();  // the partner lane's half of the block is visible
     mbar_wait(&empty[s], ((i >> lst) & 1) ^ 1);
-    dequant_q3h64_half_f32(myrow + (i % TC_PK) * TC_BN * SBPAD, n < N && (int64_t)(ks0 + i) * TC_BK < K, h,
-                           smem + s * stage_bytes, r);
+    dequant_q3h64_half_f32<false>(myrow + (i % TC_PK) * TC_BN * SBPAD, n < N && (int64_t)(ks0 + i) * TC_BK < K, h,
+                                  smem + s * stage_bytes, r);
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> tensor core reads
     mbar_arrive(&b_full[s]);
     __syncwarp();  // both halves read before the ring slot is refilled
@@ -906,11 +828,23 @@ static int tc_sms() {
   return n;
 }
 
-// split K until the grid covers the SMs (partials combined with red.add)
+// split K so the grid fills whole waves of SMs (partials combined with red.add):
+// the split count in 1..8 with the best wave efficiency tiles*splits / (waves * SMs),
+// keeping >= 8 k-steps per split; ties go to fewer splits
 static int tc_splits(int tiles, int ktotal) {
-  int splits = 1;
-  while (tiles * splits < tc_sms() && ktotal / (splits * 2) >= 8) splits *= 2;
-  return splits;
+  const int sms = tc_sms();
+  int best = 1;
+  double beff = 0.0;
+  for (int sp = 1; sp <= 8; sp++) {
+    if (sp > 1 && ktotal / sp < 8) break;
+    const int ctas = tiles * sp, waves = (ctas + sms - 1) / sms;
+    const double eff = (double)ctas / ((double)waves * sms);
+    if (eff > beff + 0.02) {
+      beff = eff;
+      best = sp;
+    }
+  }
+  return best;
 }
 
 template <bool DEC>
