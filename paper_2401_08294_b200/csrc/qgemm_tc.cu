@@ -585,7 +585,8 @@ __global__ void __launch_bounds__(TcVar<QT, BS, DEC>::THREADS, 1)
 // is tiny (N rows), so the pipeline holds up to 8 stages; each epilogue thread
 // owns one weight row and adds its hi and lo columns (no exchange), and the y
 // stores are coalesced along n.
-constexpr int TCD_MAXST = 8;
+constexpr int TCD_MAXST = 4;  // measured: 8 stages are no faster (the stage loop is not depth-bound)
+constexpr int TCD_WR = 16;  // weight-tile ring slots (Q3H_B64 decode), 4 KB each
 constexpr int TCD_XRING = 32 * 1024;
 __host__ __device__ constexpr int tcd_ncols(int B) { return 2 * tc_bpad(B) < 16 ? 16 : 2 * tc_bpad(B); }
 __host__ __device__ constexpr int tcd_stage_bytes(int B) { return TC_B_BYTES + tcd_ncols(B) * 128; }
@@ -630,71 +631,64 @@ __device__ __forceinline__ void qgemv_epilogue(uint32_t tmem, uint64_t* acc_full
 }
 
 // the 8-warp Q3H_B64 dequant loop: warp w in 2..9 owns rows [16 (w - 2), +16), lane
-// pair (2i, 2i + 1) = the two halves of row 16 (w - 2) + i; each half copies its
-// 16 bytes of the block with cp.async, and __syncwarp makes the partner's visible
-template <int QT, int BS>
-__device__ __forceinline__ void qgemv_fast_deq(const uint8_t* __restrict__ W, int64_t N, int64_t K, int64_t nb,
-                                               int64_t n0, int ks0, int nks, int stages, int stage_bytes,
-                                               unsigned char* smem, unsigned char* pring, uint64_t* empty,
-                                               uint64_t* b_full, int warp, int lane) {
-  constexpr int SBPAD = tc_sbpad(QT, BS);
-  const int lst = 31 - __clz(stages);
+// pair (2i, 2i + 1) = the two halves of row 16 (w - 2) + i; the weight tile of stage
+// i ([128 rows x 32 B], TMA) is in ring slot i % TCD_WR
+__device__ __forceinline__ void qgemv_fast_deq(int64_t N, int64_t K, int64_t n0, int ks0, int nks, int stages,
+                                               int stage_bytes, unsigned char* smem, unsigned char* wring,
+                                               uint64_t* wfull, uint64_t* wempty, uint64_t* empty, uint64_t* b_full,
+                                               int warp, int lane) {
   const int r = (warp - 2) * 16 + (lane >> 1), h = lane & 1;
   const int64_t n = n0 + r;
-  unsigned char* myrow = pring + r * SBPAD;
-  auto pre = [&](int i) {
-    const int64_t ks = ks0 + i;
-    if (n < N && ks * TC_BK < K) cp_async16(myrow + (i % TC_PK) * TC_BN * SBPAD + 16 * h, W + (n * nb + ks) * 32 + 16 * h);
-  };
-#pragma unroll
-  for (int i = 0; i < TC_PD; i++) {
-    if (i < nks) pre(i);
-    cp_async_commit();
-  }
-  for (int i = 0; i < nks; i++) {
-    const int s = (i & (stages - 1));
-    if (i + TC_PD < nks) pre(i + TC_PD);
-    cp_async_commit();
-    cp_async_wait<TC_PD>();
-    __syncwarp();  // the partner lane's half of the block is visible
-    mbar_wait(&empty[s], ((i >> lst) & 1) ^ 1);
-    dequant_q3h64_half_f32<false>(myrow + (i % TC_PK) * TC_BN * SBPAD, n < N && (int64_t)(ks0 + i) * TC_BK < K, h,
+  int s = 0;
+  uint32_t sph = 0;  // stage slot and its phase (incremental: stages need not be a power of two)
+  for (int i = 0; i < nks; i++, s = (s + 1 == stages) ? (sph ^= 1, 0) : s + 1) {
+    const int ws = i & (TCD_WR - 1);
+    mbar_wait(&wfull[ws], (i / TCD_WR) & 1);
+    mbar_wait(&empty[s], sph ^ 1);
+#ifndef IFB_TCD_NODEQ
+    dequant_q3h64_half_f32<false>(wring + ws * 4096 + r * 32, n < N && (int64_t)(ks0 + i) * TC_BK < K, h,
                                   smem + s * stage_bytes, r);
+#endif
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> tensor core reads
     mbar_arrive(&b_full[s]);
-    __syncwarp();  // both halves read before the ring slot is refilled
+    __syncwarp();  // both halves of every row of this warp read the ring slot
+    if (lane == 0) mbar_arrive(&wempty[ws]);
   }
-  cp_async_wait<0>();
 }
 
 template <int QT, int BS>
 struct TcdVar {
-  static constexpr bool FAST = QT == 35 && BS == 64;  // 8 dequant warps, two threads per row
-  static constexpr int THREADS = FAST ? 384 : 256;
+  // Q3H_B64: weight tiles [128 rows x 32 B] by 2D TMA (warp 12) into a 16-slot
+  // ring, 8 dequant warps (two threads per row)
+  static constexpr bool FAST = QT == 35 && BS == 64;
+  static constexpr int THREADS = FAST ? 416 : 256;
   static constexpr int NDEQ = FAST ? 256 : 128;
-  static constexpr int CONV1 = FAST ? 10 : 6;  // first converter warp after warp 0
+  static constexpr int CONV1 = FAST ? 10 : 6;  // first converter warp after warp 0 (FAST: 10, 11)
 };
 
 template <int QT, int BS>
 __global__ void __launch_bounds__(TcdVar<QT, BS>::THREADS, 1)
-    qgemv_tc_kernel(const __grid_constant__ CUtensorMap xmap, const uint8_t* __restrict__ W, int64_t N, int64_t K,
-                    int B, float* __restrict__ Y, int ksteps_per_split, int atomic_out, int stages) {
+    qgemv_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap wmap,
+                    const uint8_t* __restrict__ W, int64_t N, int64_t K, int B, float* __restrict__ Y,
+                    int ksteps_per_split, int atomic_out, int stages) {
   constexpr int SBPAD = tc_sbpad(QT, BS);
   using V = TcdVar<QT, BS>;
   const int bp = tc_bpad(B), ncols = tcd_ncols(B), stage_bytes = tcd_stage_bytes(B);
   const int nxr = tcd_nxr(B), xslot = bp * TC_BK;
-  const int lst = 31 - __clz(stages), lxr = 31 - __clz(nxr);  // both powers of two
+  const int lxr = 31 - __clz(nxr);  // nxr is a power of two
   extern __shared__ unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   // stage s: W' tile (A, 128 rows) at smem + s * stage_bytes, x tile (B, ncols rows) right after
-  unsigned char* pring = smem + stages * stage_bytes;                       // [TC_PK][128][SBPAD]
-  float* xraw = reinterpret_cast<float*>(pring + TC_PK * TC_BN * SBPAD);   // [nxr][bp][64]
+  unsigned char* pring = smem + stages * stage_bytes;  // [TC_PK][128][SBPAD] (cp.async) or [TCD_WR][128][32] (FAST, TMA)
+  float* xraw = reinterpret_cast<float*>(pring + (V::FAST ? TCD_WR * 4096 : TC_PK * TC_BN * SBPAD));  // [nxr][bp][64]
   uint64_t* a_full = reinterpret_cast<uint64_t*>(reinterpret_cast<unsigned char*>(xraw) + TCD_XRING);  // x ready
   uint64_t* b_full = a_full + TCD_MAXST;  // W' ready
   uint64_t* empty = b_full + TCD_MAXST;
   uint64_t* acc_full = empty + TCD_MAXST;
   uint64_t* xr_full = acc_full + 1;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(xr_full + TC_XRMAX);
+  uint64_t* wfull = xr_full + TC_XRMAX;  // [TCD_WR] (FAST)
+  uint64_t* wempty = wfull + TCD_WR;     // [TCD_WR]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(wempty + TCD_WR);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t n0 = (int64_t)blockIdx.x * TC_BN;
@@ -711,6 +705,10 @@ __global__ void __launch_bounds__(TcdVar<QT, BS>::THREADS, 1)
     }
     mbar_init(acc_full, 1);
     for (int i = 0; i < TC_XRMAX; i++) mbar_init(&xr_full[i], 1);
+    for (int i = 0; i < TCD_WR; i++) {
+      mbar_init(&wfull[i], 1);
+      mbar_init(&wempty[i], 8);  // the 8 dequant warps
+    }
     fence_mbar_init();
   }
   // x tiles: rows of tokens >= B (hi and lo) are never written -> zero them once
@@ -728,17 +726,30 @@ __global__ void __launch_bounds__(TcdVar<QT, BS>::THREADS, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  if (warp == 0 || warp >= V::CONV1) {
+  if (V::FAST && warp == 12) {
+    // ---------------- weight tiles: one 2D TMA per stage, 16 slots ahead ----------------
+    if (lane == 0) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"(&wmap) : "memory");
+      for (int i = 0; i < nks; i++) {
+        const int ws = i & (TCD_WR - 1);
+        mbar_wait(&wempty[ws], ((i / TCD_WR) & 1) ^ 1);
+        mbar_arrive_expect_tx(&wfull[ws], 4096u);
+        tma_load_2d(pring + ws * 4096, &wmap, (ks0 + i) * 32, (int)n0, &wfull[ws]);
+      }
+    }
+  } else if (warp == 0 || (warp >= V::CONV1 && warp < V::CONV1 + 2)) {
     // ---------------- converters: raw fp32 x (2D TMA ring) -> fp16 hi/lo x tiles ----------------
     const int cidx = warp == 0 ? 0 : warp - V::CONV1 + 1;
     const bool issuer = warp == 0 && lane == 0;
     if (issuer)
       for (int i = 0; i < nxr && i < nks; i++) issue_x_stage(&xmap, ks0 + i, xraw + i * xslot, &xr_full[i], bp);
     for (int i = 0; i < nks; i++) {
-      const int s = (i & (stages - 1)), xs = (i & (nxr - 1));
-      mbar_wait(&empty[s], ((i >> lst) & 1) ^ 1);
+      const int s = i % stages, xs = (i & (nxr - 1));
+      mbar_wait(&empty[s], ((i / stages) & 1) ^ 1);
       mbar_wait(&xr_full[xs], (i >> lxr) & 1);
+#ifndef IFB_TCD_NOCONV
       convert_x_tile<false>(xraw + xs * xslot, B, smem + s * stage_bytes + TC_B_BYTES, cidx, bp);
+#endif
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> tensor core reads
       __syncwarp();
       if (lane == 0) mbar_arrive(&a_full[s]);
@@ -750,8 +761,8 @@ __global__ void __launch_bounds__(TcdVar<QT, BS>::THREADS, 1)
     if (lane == 0) {
       const uint32_t idesc = umma_idesc_f16(TC_BN, ncols);
       for (int i = 0; i < nks; i++) {
-        const int s = (i & (stages - 1));
-        const uint32_t par = (i >> lst) & 1;
+        const int s = i % stages;
+        const uint32_t par = (i / stages) & 1;
         mbar_wait(&a_full[s], par);
         mbar_wait(&b_full[s], par);
         tc_fence_after();
@@ -759,7 +770,9 @@ __global__ void __launch_bounds__(TcdVar<QT, BS>::THREADS, 1)
         const uint64_t adesc0 = umma_desc_sw128(st), bdesc0 = umma_desc_sw128(st + TC_B_BYTES);
 #pragma unroll
         for (int kk = 0; kk < TC_BK / 16; kk++)
+#ifndef IFB_TCD_NOMMA
           umma_bf16(tmem, adesc0 + (uint64_t)(kk * 2), bdesc0 + (uint64_t)(kk * 2), idesc, (i > 0) || (kk > 0));
+#endif
         umma_commit(&empty[s]);
       }
       umma_commit(acc_full);
@@ -768,9 +781,9 @@ __global__ void __launch_bounds__(TcdVar<QT, BS>::THREADS, 1)
     // ---------------- Q3H_B64 dequantizers, second half of the 8 warps ----------------
     // (warps 2-9: 16 rows each, lane pairs = the two halves of a row; warps 2-5
     //  run the epilogue below after the same loop)
-    qgemv_fast_deq<QT, BS>(W, N, K, nb, n0, ks0, nks, stages, stage_bytes, smem, pring, empty, b_full, warp, lane);
+    qgemv_fast_deq(N, K, n0, ks0, nks, stages, stage_bytes, smem, pring, wfull, wempty, empty, b_full, warp, lane);
   } else if (V::FAST) {
-    qgemv_fast_deq<QT, BS>(W, N, K, nb, n0, ks0, nks, stages, stage_bytes, smem, pring, empty, b_full, warp, lane);
+    qgemv_fast_deq(N, K, n0, ks0, nks, stages, stage_bytes, smem, pring, wfull, wempty, empty, b_full, warp, lane);
     qgemv_epilogue(tmem, acc_full, Y, N, B, bp, n0, nks, atomic_out, warp, lane);
   } else {
     // ---------------- dequantizers: one weight row per thread (Eq. 2 in fp32, -> fp16) ----------------
@@ -783,11 +796,11 @@ __global__ void __launch_bounds__(TcdVar<QT, BS>::THREADS, 1)
       cp_async_commit();
     }
     for (int i = 0; i < nks; i++) {
-      const int s = (i & (stages - 1));
+      const int s = i % stages;
       if (i + TC_PD < nks) prefetch_row<QT, BS>(W, nb, n, N, ks0 + i + TC_PD, K, myring + ((i + TC_PD) % TC_PK) * TC_BN * SBPAD);
       cp_async_commit();
       cp_async_wait<TC_PD>();
-      mbar_wait(&empty[s], ((i >> lst) & 1) ^ 1);
+      mbar_wait(&empty[s], ((i / stages) & 1) ^ 1);
       dequant_row<QT, BS, true>(myring + (i % TC_PK) * TC_BN * SBPAD, n, N, (int64_t)(ks0 + i) * TC_BK, K,
                                 smem + s * stage_bytes, r);
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> tensor core reads
@@ -921,12 +934,23 @@ if_status qgemv_tc_launch(if_scheme s, const uint8_t* W, int64_t N, int64_t K, c
   if (splits > 1 && !accumulate) {
     if (cudaMemsetAsync(Y, 0, sizeof(float) * B * N, st) != cudaSuccess) return check_launch("qgemv_tc memset");
   }
+  CUtensorMap wmap;  // Q3H_B64 packed weights as bytes [N rows x row_bytes], tiles of 128 rows x 32 B
+  memset(&wmap, 0, sizeof(wmap));
+  if (s.type == IF_Q3H && s.block == 64) {
+    if ((row_bytes & 15) || (reinterpret_cast<uintptr_t>(W) & 15u)) return IF_ERR_UNSUPPORTED;
+    cuuint64_t wd[2] = {(cuuint64_t)row_bytes, (cuuint64_t)N};
+    cuuint64_t ws[1] = {(cuuint64_t)row_bytes};
+    cuuint32_t wb[2] = {32u, (cuuint32_t)TC_BN};
+    cr = g_encode(&wmap, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<uint8_t*>(W), wd, ws, wb, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (cr != CUDA_SUCCESS) return set_error(IF_ERR_CUDA, "qgemv_tc: weight tensor map failed (%d)", (int)cr);
+  }
   return dispatch_scheme(s, [&]<int QT, int BS>() -> if_status {
     auto kern = qgemv_tc_kernel<QT, BS>;
-    constexpr int fixed = TC_PK * TC_BN * tc_sbpad(QT, BS) + TCD_XRING + 1024 + 512;
+    constexpr int fixed = (TcdVar<QT, BS>::FAST ? TCD_WR * 4096 : TC_PK * TC_BN * tc_sbpad(QT, BS)) + TCD_XRING + 1024 + 768;
     const int sb = tcd_stage_bytes((int)B);
     int stages = std::min(TCD_MAXST, (227 * 1024 - fixed) / sb);
-    stages = stages >= 8 ? 8 : stages >= 4 ? 4 : stages >= 2 ? 2 : 0;  // a power of two (shift/mask indexing)
     if (stages < 2) return IF_ERR_UNSUPPORTED;
     const int smem = stages * sb + fixed;
     static bool configured = false;
@@ -935,7 +959,7 @@ if_status qgemv_tc_launch(if_scheme s, const uint8_t* W, int64_t N, int64_t K, c
       configured = true;
     }
     dim3 grid(ntile, 1, splits);
-    kern<<<grid, TcdVar<QT, BS>::THREADS, smem, st>>>(map, W, N, K, (int)B, Y, kper, atomic_out, stages);
+    kern<<<grid, TcdVar<QT, BS>::THREADS, smem, st>>>(map, wmap, W, N, K, (int)B, Y, kper, atomic_out, stages);
     count_launch();
     return check_launch("qgemv_tc");
   });
