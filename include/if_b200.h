@@ -112,7 +112,14 @@ if_status if_dequantize(if_scheme s, const uint8_t* packed, int64_t N, int64_t K
  * 1 <= B <= 64.  x and y 16-byte aligned, W 16-byte aligned (cudaMalloc /
  * torch allocations are).  Codes are not validated (invalid Q3H codes give
  * unspecified values, memory-safe).  Result within 1e-3 normwise of the fp64
- * definition (BASELINE.json north_star); deterministic (same bits every call).
+ * definition (BASELINE.json north_star).
+ * B = 1: fp32 CUDA-core path (Q3H_B64: the persistent engine of decode_mk.cu),
+ *   deterministic (same bits every call).
+ * B >= 2: tcgen05 tensor cores (qgemm_tc.cu): W' formed exactly (Eq. 2, fp32)
+ *   then rounded to fp16, x split into fp16 hi + lo, fp32 accumulation
+ *   (Q23); split-K partials are combined with atomic adds, so the
+ *   low bits may differ between calls.  Shapes the TMA path cannot take
+ *   (unaligned rows) fall back to the CUDA-core kernels.
  * ------------------------------------------------------------------------- */
 if_status if_qgemv(if_scheme s, const uint8_t* W, int64_t N, int64_t K, const float* x, int64_t B,
                    float* y, if_stream_t stream);
@@ -212,8 +219,10 @@ if_status if_comm_recv_prev(if_comm c, float* buf, int64_t n, if_stream_t stream
  * h_in  device fp32 [T, d] (ignored on stages > 0, which receive from stage-1),
  * h_out device fp32 [T, d] (valid on the last stage), last_qkv device fp32
  * [T, (lh + 2 lkv) head_dim] of the stage's last layer (nullable).
- * mode IF_DECODE (1 <= T <= 64, qGEMV, fp32 activations) or IF_PREFILL
- * (T <= 4096, qGEMM on tcgen05 with bf16 activations).
+ * mode IF_DECODE (1 <= T <= 64, fp32 activations: Q3H_B64 on one rank with
+ * T <= 6 runs the persistent engine -- one launch per token for the whole
+ * stage; otherwise per-layer qGEMVs as in if_qgemv) or IF_PREFILL (T <= 4096,
+ * qGEMM on tcgen05 with bf16 activations).
  * workspace: device, if_stack_workspace_bytes(); ZERO-FILL IT ONCE before the
  * first call (cudaMemset) and keep it with this (shape, plan, rank): it carries
  * the decode engine's step epoch across calls.  comm may be NULL when
