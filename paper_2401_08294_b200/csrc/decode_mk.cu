@@ -492,19 +492,25 @@ __global__ void __launch_bounds__(MK_THREADS, 1) decode_mk_kernel(const __grid_c
         }
         if (dbg) { dbg[1] = gtimer(); dbg[9] = clock64(); }
         const uint32_t row_bytes = (uint32_t)g.nbp * 16u;
-        mbar_arrive_expect_tx(xbar, 16u * row_bytes);
+        const uint32_t ssq_bytes = rms ? (uint32_t)((G + 3) & ~3) * 4u : 0u;  // the Sigma h^2 partials ride along
+        mbar_arrive_expect_tx(xbar, 16u * row_bytes + ssq_bytes);
         for (int jj = 0; jj < 16; jj++) bulk_g2s(xs + jj * xstride, img + jj * xstride, row_bytes, xbar, 0ull, false);
+        if (rms) bulk_g2s(ssq_s, P.ssq, ssq_bytes, xbar, 0ull, false);
       }
-      // 2. the sum-h^2 partials (fixed order: deterministic)
+      mbar_wait(xbar, xuse & 1);
+      xuse++;
+      // 2. the sum-h^2 partials (parity-checked like the image; fixed order: deterministic)
       if (rms && cw == MK_NC - 1) {
-        SpinGuard sg;
         float t = 0.f;
         for (int c = lane; c < G; c += 32) {
-          uint32_t v = ld_relaxed_u32(reinterpret_cast<const uint32_t*>(P.ssq) + c);
-          while ((v ^ par) & 1u) {
-            __nanosleep(20);
-            sg.tick();
-            v = ld_relaxed_u32(reinterpret_cast<const uint32_t*>(P.ssq) + c);
+          uint32_t v = __float_as_uint(ssq_s[c]);
+          if ((v ^ par) & 1u) {
+            SpinGuard sg;
+            do {
+              __nanosleep(20);
+              sg.tick();
+              v = ld_relaxed_u32(reinterpret_cast<const uint32_t*>(P.ssq) + c);
+            } while ((v ^ par) & 1u);
           }
           t += __uint_as_float(v & ~1u);
         }
@@ -512,42 +518,50 @@ __global__ void __launch_bounds__(MK_THREADS, 1) decode_mk_kernel(const __grid_c
         for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
         if (lane == 0) red[16] = t;
       }
-      mbar_wait(xbar, xuse & 1);
-      xuse++;
       if (dbg && ct == 0) { dbg[6] = gtimer(); dbg[14] = clock64(); }
       // 3. four threads per block b, four quads each: check every word's parity
       //    (re-read the rare late one from L2), strip it, and form the block sum
       //    of x (x_e + x_o = xe' + 12 x_o in transformed terms)
-      for (int t0 = cw * 32; t0 < 4 * g.nbp; t0 += MK_CT) {
-        const int t = t0 + lane, b = t >> 2, j4 = t & 3;
-        float sx = 0.f;
-        if (b < g.nb) {
-          float4 v[4];
+      for (int t0 = cw * 32; t0 < 4 * g.nbp; t0 += 2 * MK_CT) {
+        // two items per pass (K > 8192: 2 items per thread), all loads first
+        float4 v[2][4];
 #pragma unroll
-          for (int i = 0; i < 4; i++) v[i] = xs[(4 * j4 + i) * xstride + b];
+        for (int u = 0; u < 2; u++) {
+          const int t = t0 + u * MK_CT + lane, b = t >> 2, j4 = t & 3;
 #pragma unroll
-          for (int i = 0; i < 4; i++) {
-            const int jj = 4 * j4 + i;
-            float4 q = v[i];
-            if (!par4_ok(q, par)) {
-              SpinGuard sg;
-              do {
-                if (dbg) atomicAdd(reinterpret_cast<unsigned long long*>(dbg + 7), 1ull);
-                sg.tick();
-                q = ld_relaxed_f4(img + jj * xstride + b);
-              } while (!par4_ok(q, par));
-            }
-            const float4 w = make_float4(__uint_as_float(__float_as_uint(q.x) & ~1u), __uint_as_float(__float_as_uint(q.y) & ~1u),
-                                         __uint_as_float(__float_as_uint(q.z) & ~1u), __uint_as_float(__float_as_uint(q.w) & ~1u));
-            xs[jj * xstride + b] = w;
-            const float c0 = __uint_as_float((uint32_t)(127 - 85 + pos[2 * jj]) << 23);  // 2^(s - 85)
-            const float c1 = __uint_as_float((uint32_t)(127 - 85 + pos[2 * jj + 1]) << 23);
-            sx += (w.z + w.w) * 2.5849394142282115e-26f + 12.0f * (w.x * c0 + w.y * c1);
-          }
+          for (int i = 0; i < 4; i++)
+            v[u][i] = b < g.nb ? xs[(4 * j4 + i) * xstride + b] : make_float4(0.f, 0.f, 0.f, 0.f);
         }
-        sx += __shfl_xor_sync(0xffffffffu, sx, 1);
-        sx += __shfl_xor_sync(0xffffffffu, sx, 2);
-        if (j4 == 0 && b < g.nbp) bs[b] = make_float2(sx, 0.f);
+#pragma unroll
+        for (int u = 0; u < 2; u++) {
+          if (t0 + u * MK_CT >= 4 * g.nbp) break;  // warp-uniform
+          const int t = t0 + u * MK_CT + lane, b = t >> 2, j4 = t & 3;
+          float sx = 0.f;
+          if (b < g.nb) {
+#pragma unroll
+            for (int i = 0; i < 4; i++) {
+              const int jj = 4 * j4 + i;
+              float4 q = v[u][i];
+              if (!par4_ok(q, par)) {
+                SpinGuard sg;
+                do {
+                  if (dbg) atomicAdd(reinterpret_cast<unsigned long long*>(dbg + 7), 1ull);
+                  sg.tick();
+                  q = ld_relaxed_f4(img + jj * xstride + b);
+                } while (!par4_ok(q, par));
+              }
+              const float4 w = make_float4(__uint_as_float(__float_as_uint(q.x) & ~1u), __uint_as_float(__float_as_uint(q.y) & ~1u),
+                                           __uint_as_float(__float_as_uint(q.z) & ~1u), __uint_as_float(__float_as_uint(q.w) & ~1u));
+              xs[jj * xstride + b] = w;
+              const float c0 = __uint_as_float((uint32_t)(127 - 85 + pos[2 * jj]) << 23);  // 2^(s - 85)
+              const float c1 = __uint_as_float((uint32_t)(127 - 85 + pos[2 * jj + 1]) << 23);
+              sx += (w.z + w.w) * 2.5849394142282115e-26f + 12.0f * (w.x * c0 + w.y * c1);
+            }
+          }
+          sx += __shfl_xor_sync(0xffffffffu, sx, 1);
+          sx += __shfl_xor_sync(0xffffffffu, sx, 2);
+          if (j4 == 0 && b < g.nbp) bs[b] = make_float2(sx, 0.f);
+        }
       }
       if (dbg && ct == 0) { dbg[2] = gtimer(); dbg[10] = clock64(); }
       named_bar_sync(1, MK_CT);
