@@ -707,12 +707,14 @@ __global__ void __launch_bounds__(MK_THREADS, 1) decode_mk_kernel(const __grid_c
           }
           gg *= out_scale;
           u *= out_scale;
-          a[h] = gg / (1.0f + expf(-gg)) * u;
+          // silu(g) u with the fast exp / division: a few ulp, far inside the 1e-3 gate
+          a[h] = __fdividef(gg, 1.0f + __expf(-gg)) * u;
         }
         put_pair(P.xs_act, xstride, pos, (g.r0 + rr) / 2, a[0], a[1], (ep * (uint32_t)P.layers + l + 1u) & 1u);
       }
     } else if (kind == 0) {
       const int v_off = (P.lh + P.lkv) * P.hd;
+      const int hd_log2 = (P.hd & (P.hd - 1)) == 0 ? __ffs(P.hd) - 1 : -1;
       const bool last_layer = p == nphase - 4;
       const uint32_t vctx = ep * (uint32_t)P.layers + l + 1u;
       for (int rr = 2 * ct; rr < nr; rr += 2 * MK_CT) {
@@ -727,7 +729,8 @@ __global__ void __launch_bounds__(MK_THREADS, 1) decode_mk_kernel(const __grid_c
         const int n = g.r0 + rr;
         if (n >= v_off) {
           // ctx heads i whose kv group is this v head: scatter the pair
-          const int ev = n - v_off, jv = ev / P.hd, e = ev - jv * P.hd;
+          const int ev = n - v_off;
+          const int jv = hd_log2 >= 0 ? ev >> hd_log2 : ev / P.hd, e = ev - jv * P.hd;
           const int i0 = (jv + P.k0) * P.per - P.h0;
           for (int i = max(i0, 0); i < min(i0 + P.per, P.lh); i++)
             put_pair(P.xs_ctx, xstride, pos, i * P.hd + e, v2[0], v2[1], vctx & 1u);

@@ -61,11 +61,11 @@ for k in range(4):
     first = np.median([np.median(d[:, p, 6] - d[:, p, 1]) for p in ps])
     repoll = dbg.view(G, nph, 16)[:, ps, 7].float().mean().item()
     print(f"{kinds[k]:5s} first-batch-return {first:6.2f} us after dep_ok; ct0 re-polls/phase {repoll:.2f}")
-print("clock64-based intra-CTA durations (us @1965 MHz): start->dep, dep->copied, copied->staged, staged->units, units->signalled")
+print("clock64-based intra-CTA durations (us @1965 MHz): start->dep, dep->copied, copied->staged, staged->units, units, epi-loop, bump")
 for k in range(4):
     ps = [p for p in range(1, nph) if p % 4 == k]
     cols = []
-    for a, b in [(0, 1), (1, 6), (6, 2), (2, 3), (3, 4), (4, 5)]:
+    for a, b in [(0, 1), (1, 6), (6, 2), (2, 3), (3, 4), (4, 7), (7, 5)]:
         cols.append(np.median([np.median(ck[:, p, b] - ck[:, p, a]) for p in ps]))
     print(f"{kinds[k]:5s}" + "".join(f"{v:7.2f}" for v in cols))
 print("kind   wait   sync   copy  stage stream    epi   skew  phase")
