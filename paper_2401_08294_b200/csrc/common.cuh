@@ -82,6 +82,13 @@ __device__ __forceinline__ uint32_t get_code(const uint32_t (&w)[NW + 1], int j)
   return __funnelshift_r(w[wi], w[wi + 1], sh) & ((1u << C) - 1u);
 }
 
+// Programmatic dependent launch (batched-decode chain): a kernel launched with
+// the PDL attribute may start while its predecessor drains; pdl_wait() blocks
+// until the predecessor grid completed and its writes are visible, and
+// pdl_trigger() lets the successor start launching.  No-ops without PDL.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 __device__ __forceinline__ float half_bits_to_float(uint32_t h16) {
   return __half2float(__ushort_as_half((unsigned short)h16));
 }

@@ -673,6 +673,7 @@ __global__ void __launch_bounds__(TcdVar<QT, BS>::THREADS, 1)
                     int ksteps_per_split, int atomic_out, int stages) {
   constexpr int SBPAD = tc_sbpad(QT, BS);
   using V = TcdVar<QT, BS>;
+  pdl_trigger();
   const int bp = tc_bpad(B), ncols = tcd_ncols(B), stage_bytes = tcd_stage_bytes(B);
   const int nxr = tcd_nxr(B), xslot = bp * TC_BK;
   const int lxr = 31 - __clz(nxr);  // nxr is a power of two
@@ -725,6 +726,8 @@ __global__ void __launch_bounds__(TcdVar<QT, BS>::THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  // the predecessor (PDL) wrote x / y: every role but the weight stream waits for it
+  if (!(V::FAST && warp == 12)) pdl_wait();
 
   if (V::FAST && warp == 12) {
     // ---------------- weight tiles: one 2D TMA per stage, 16 slots ahead ----------------
@@ -958,8 +961,17 @@ if_status qgemv_tc_launch(if_scheme s, const uint8_t* W, int64_t N, int64_t K, c
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
       configured = true;
     }
-    dim3 grid(ntile, 1, splits);
-    kern<<<grid, TcdVar<QT, BS>::THREADS, smem, st>>>(map, wmap, W, N, K, (int)B, Y, kper, atomic_out, stages);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(ntile, 1, splits);
+    cfg.blockDim = dim3(TcdVar<QT, BS>::THREADS);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // prologue + weight prefetch overlap the predecessor
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = splits > 1 && !accumulate ? 0 : 1;  // (after the split-K memset: plain stream order)
+    cudaLaunchKernelEx(&cfg, kern, map, wmap, W, N, K, (int)B, Y, kper, atomic_out, stages);
     count_launch();
     return check_launch("qgemv_tc");
   });

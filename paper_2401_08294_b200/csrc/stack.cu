@@ -30,6 +30,8 @@ __device__ __forceinline__ __nv_bfloat16 to_out<__nv_bfloat16>(float v) {
 // a[t] = h[t] / sqrt(mean(h[t]^2) + 1e-5)
 template <typename OutT>
 __global__ void __launch_bounds__(256) rmsnorm_kernel(const float* __restrict__ h, OutT* __restrict__ a, int d) {
+  pdl_trigger();
+  pdl_wait();
   __shared__ float red[8];
   const float* hr = h + (int64_t)blockIdx.x * d;
   float ss = 0.f;
@@ -49,6 +51,8 @@ __global__ void __launch_bounds__(256) rmsnorm_kernel(const float* __restrict__ 
 template <typename OutT>
 __global__ void vbcast_kernel(const float* __restrict__ qkv, OutT* __restrict__ ctx, int T, int lh, int lkv, int hd,
                               int h0, int k0, int per) {
+  pdl_trigger();
+  pdl_wait();
   const int64_t nq = (int64_t)lh * hd, nqkv = (int64_t)(lh + 2 * lkv) * hd;
   const int64_t total = (int64_t)T * nq;
   for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total; idx += (int64_t)gridDim.x * blockDim.x) {
@@ -62,12 +66,29 @@ __global__ void vbcast_kernel(const float* __restrict__ qkv, OutT* __restrict__ 
 // act[t, f] = silu(g) * u with gate/up rows interleaved: g = gu[t, 2f], u = gu[t, 2f+1]
 template <typename OutT>
 __global__ void silu_mul_kernel(const float* __restrict__ gu, OutT* __restrict__ act, int T, int lf) {
+  pdl_trigger();
+  pdl_wait();
   const int64_t total = (int64_t)T * lf;
   for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total; idx += (int64_t)gridDim.x * blockDim.x) {
     const int64_t t = idx / lf, f = idx - t * lf;
     const float g = gu[t * 2 * lf + 2 * f], u = gu[t * 2 * lf + 2 * f + 1];
     act[idx] = to_out<OutT>(g / (1.0f + expf(-g)) * u);
   }
+}
+
+// launch with the programmatic-dependent-launch attribute (decode chain)
+template <typename... KArgs, typename... Args>
+static void launch_pdl(void (*kern)(KArgs...), unsigned grid, unsigned block, cudaStream_t st, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, kern, (KArgs)args...);
 }
 
 static int ew_grid(int64_t n) {
@@ -245,11 +266,11 @@ extern "C" if_status if_run_stack(const if_stack_shape* shape, const if_plan* pl
     if (!Wl.wqkv || !Wl.wo || !Wl.wgu || !Wl.wdown) return set_error(IF_ERR_ARG, "if_run_stack: null weights, layer %d", l);
     if (mode == IF_DECODE) {
       // ---- attention sub-layer ----
-      rmsnorm_kernel<float><<<(unsigned)T, 256, 0, cs>>>(h_out, w.a, L.d);
+      launch_pdl(rmsnorm_kernel<float>, (unsigned)T, 256, cs, (const float*)h_out, w.a, (int)L.d);
       count_launch();
       if ((st = if_qgemv(sc, Wl.wqkv, L.nqkv, L.d, w.a, T, w.qkv, stream))) return st;
-      vbcast_kernel<float><<<ew_grid(T * L.nq), 256, 0, cs>>>(w.qkv, w.ctx, (int)T, L.lh, L.lkv, L.hd, asg.head_begin,
-                                                             asg.kv_begin, per);
+      launch_pdl(vbcast_kernel<float>, (unsigned)ew_grid(T * L.nq), 256, cs, (const float*)w.qkv, w.ctx, (int)T,
+                 (int)L.lh, (int)L.lkv, (int)L.hd, (int)asg.head_begin, (int)asg.kv_begin, (int)per);
       count_launch();
       if (groups == 1) {
         if ((st = if_qgemv_acc(sc, Wl.wo, L.d, L.nq, w.ctx, T, h_out, stream))) return st;
@@ -258,10 +279,11 @@ extern "C" if_status if_run_stack(const if_stack_shape* shape, const if_plan* pl
         if ((st = comm_allreduce_into(comm, w.part, h_out, nh, 1, cs))) return st;  // merge #1
       }
       // ---- feed-forward sub-layer ----
-      rmsnorm_kernel<float><<<(unsigned)T, 256, 0, cs>>>(h_out, w.a, L.d);
+      launch_pdl(rmsnorm_kernel<float>, (unsigned)T, 256, cs, (const float*)h_out, w.a, (int)L.d);
       count_launch();
       if ((st = if_qgemv(sc, Wl.wgu, 2 * L.lf, L.d, w.a, T, w.gu, stream))) return st;
-      silu_mul_kernel<float><<<ew_grid(T * L.lf), 256, 0, cs>>>(w.gu, w.act, (int)T, L.lf);
+      launch_pdl(silu_mul_kernel<float>, (unsigned)ew_grid(T * L.lf), 256, cs, (const float*)w.gu, w.act, (int)T,
+                 (int)L.lf);
       count_launch();
       if (groups == 1) {
         if ((st = if_qgemv_acc(sc, Wl.wdown, L.d, L.lf, w.act, T, h_out, stream))) return st;
