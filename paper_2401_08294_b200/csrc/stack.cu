@@ -28,10 +28,15 @@ __device__ __forceinline__ __nv_bfloat16 to_out<__nv_bfloat16>(float v) {
 }
 
 // a[t] = h[t] / sqrt(mean(h[t]^2) + 1e-5)
+// (zbuf, zn: optionally zero the next qGEMV's output, which then accumulates --
+//  no memset node, so the chain stays programmatic)
 template <typename OutT>
-__global__ void __launch_bounds__(256) rmsnorm_kernel(const float* __restrict__ h, OutT* __restrict__ a, int d) {
+__global__ void __launch_bounds__(256) rmsnorm_kernel(const float* __restrict__ h, OutT* __restrict__ a, int d,
+                                                      float* __restrict__ zbuf = nullptr, int64_t zn = 0) {
   pdl_trigger();
   pdl_wait();
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < zn; i += (int64_t)gridDim.x * blockDim.x)
+    zbuf[i] = 0.f;
   __shared__ float red[8];
   const float* hr = h + (int64_t)blockIdx.x * d;
   float ss = 0.f;
@@ -266,9 +271,10 @@ extern "C" if_status if_run_stack(const if_stack_shape* shape, const if_plan* pl
     if (!Wl.wqkv || !Wl.wo || !Wl.wgu || !Wl.wdown) return set_error(IF_ERR_ARG, "if_run_stack: null weights, layer %d", l);
     if (mode == IF_DECODE) {
       // ---- attention sub-layer ----
-      launch_pdl(rmsnorm_kernel<float>, (unsigned)T, 256, cs, (const float*)h_out, w.a, (int)L.d);
+      launch_pdl(rmsnorm_kernel<float>, (unsigned)T, 256, cs, (const float*)h_out, w.a, (int)L.d, w.qkv,
+                 (int64_t)T * L.nqkv);
       count_launch();
-      if ((st = if_qgemv(sc, Wl.wqkv, L.nqkv, L.d, w.a, T, w.qkv, stream))) return st;
+      if ((st = if_qgemv_acc(sc, Wl.wqkv, L.nqkv, L.d, w.a, T, w.qkv, stream))) return st;
       launch_pdl(vbcast_kernel<float>, (unsigned)ew_grid(T * L.nq), 256, cs, (const float*)w.qkv, w.ctx, (int)T,
                  (int)L.lh, (int)L.lkv, (int)L.hd, (int)asg.head_begin, (int)asg.kv_begin, (int)per);
       count_launch();
@@ -279,9 +285,10 @@ extern "C" if_status if_run_stack(const if_stack_shape* shape, const if_plan* pl
         if ((st = comm_allreduce_into(comm, w.part, h_out, nh, 1, cs))) return st;  // merge #1
       }
       // ---- feed-forward sub-layer ----
-      launch_pdl(rmsnorm_kernel<float>, (unsigned)T, 256, cs, (const float*)h_out, w.a, (int)L.d);
+      launch_pdl(rmsnorm_kernel<float>, (unsigned)T, 256, cs, (const float*)h_out, w.a, (int)L.d, w.gu,
+                 (int64_t)T * 2 * L.lf);
       count_launch();
-      if ((st = if_qgemv(sc, Wl.wgu, 2 * L.lf, L.d, w.a, T, w.gu, stream))) return st;
+      if ((st = if_qgemv_acc(sc, Wl.wgu, 2 * L.lf, L.d, w.a, T, w.gu, stream))) return st;
       launch_pdl(silu_mul_kernel<float>, (unsigned)ew_grid(T * L.lf), 256, cs, (const float*)w.gu, w.act, (int)T,
                  (int)L.lf);
       count_launch();
