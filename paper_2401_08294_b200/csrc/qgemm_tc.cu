@@ -353,8 +353,10 @@ __global__ void __launch_bounds__(TcVar<QT, BS, DEC>::THREADS, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(xr_full + TC_XRMAX);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t n0 = (int64_t)blockIdx.x * TC_BN;
-  const int64_t m0 = (int64_t)blockIdx.y * (TC_BM * MT);
+  // grid (m tiles, n tiles, splits): the CTAs sharing a weight tile are adjacent in
+  // launch order, so the second read of the tile hits L2 instead of HBM
+  const int64_t n0 = (int64_t)blockIdx.y * TC_BN;
+  const int64_t m0 = (int64_t)blockIdx.x * (TC_BM * MT);
   const int64_t nb = K / BS;
   const int ktotal = (int)((K + TC_BK - 1) / TC_BK);
   const int ks0 = blockIdx.z * ksteps_per_split;
@@ -888,7 +890,7 @@ static if_status tc_run(if_scheme s, const CUtensorMap& map, const float* xdec, 
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
       configured = true;
     }
-    dim3 grid(ntile, mtile, splits);
+    dim3 grid(mtile, ntile, splits);
     kern<<<grid, TcVar<QT, BS, DEC>::THREADS, smem, st>>>(map, xdec, W, N, K, M, Y, kper, atomic_out);
     count_launch();
     return check_launch(DEC ? "qgemv_tc" : "qgemm_tc");
