@@ -846,19 +846,20 @@ static int tc_sms() {
   return n;
 }
 
-// split K so the grid fills whole waves of SMs (partials combined with red.add):
-// the split count in 1..8 with the best wave efficiency tiles*splits / (waves * SMs),
-// keeping >= 8 k-steps per split; ties go to fewer splits
+// split K to minimise  waves * (F + k-steps per split): whole waves of SMs against
+// the fixed per-CTA cost (prologue, pipeline fill, atomic epilogue ~ F k-steps,
+// measured); partials combined with red.add
 static int tc_splits(int tiles, int ktotal) {
   const int sms = tc_sms();
+  constexpr int F = 12;
   int best = 1;
-  double beff = 0.0;
+  long bcost = -1;
   for (int sp = 1; sp <= 8; sp++) {
-    if (sp > 1 && ktotal / sp < 8) break;
-    const int ctas = tiles * sp, waves = (ctas + sms - 1) / sms;
-    const double eff = (double)ctas / ((double)waves * sms);
-    if (eff > beff + 0.02) {
-      beff = eff;
+    if (sp > 1 && ktotal / sp < 4) break;
+    const long waves = (tiles * sp + sms - 1) / sms;
+    const long cost = waves * (F + (ktotal + sp - 1) / sp);
+    if (bcost < 0 || cost < bcost) {
+      bcost = cost;
       best = sp;
     }
   }
