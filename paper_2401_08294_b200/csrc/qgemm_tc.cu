@@ -1,27 +1,21 @@
-// qgemm_tc.cu — fused-dequant GEMM on the 5th-gen tensor cores (tcgen05 +
+// qgemm_tc.cu — fused-dequant GEMM/GEMV on the 5th-gen tensor cores (tcgen05 +
 // TMEM + TMA), P:93-94:
 //     Y[m, n] (+)= sum_k W'[n, k] X[m, k]        fp32 accumulate
-// Two uses of one kernel template:
-//  * a5 prefill (DEC = false): X bf16 [M, K] by TMA (SWIZZLE_128B tensor map),
-//    W' -> bf16, two 128-row UMMA M tiles per CTA (256 TMEM columns).
-//  * a4 batched decode (DEC = true, 2 <= B <= 64): x fp32 [B, K] is split
-//    into fp16 hi + lo (x = hi + lo to ~22 bits) by a converter warp straight
-//    into the UMMA A tile (rows 0..63 hi, 64..127 lo), W' -> fp16, one M tile;
-//    the epilogue adds the lo rows to the hi rows.  Error: fp16 rounding of W'
-//    only (Q17), well inside the 1e-3 decode gate.
-// CTA tile: 128 weight rows (UMMA N) x K in steps of 64 (one Q3H_B64 block per
-// row), optional split-K over gridDim.z (partials combined with red.add).
-// Warp roles (8 warps):
-//   warp 0  X producer (TMA, or the fp32 -> fp16 hi/lo converter)
-//   warp 1  TMEM allocator + single-thread tcgen05.mma issuer (kind::f16)
-//   warps 2-5  dequantizers, one weight row per thread: the row's packed bytes
-//           for stage i + PD are prefetched with cp.async (a shared-memory
-//           ring, rows padded to an odd number of 16-byte chunks: conflict-
-//           free), Eq. 2 -> 16-bit, written straight into the UMMA
-//           canonical K-major SW128 layout, fence.proxy.async, mbarrier arrive
-//   warps 2-5  epilogue: tcgen05.ld 32x32b (TMEM lane quarter = warp % 4)
-// Pipeline: full barriers (A: TMA tx bytes or converter arrival; B: 128
-// dequant arrivals), empty barriers armed by tcgen05.commit.
+// Two kernels:
+//  * qgemm_tc_kernel -- a5 prefill: X bf16 [M, K] by TMA (SWIZZLE_128B tensor
+//    map), W' -> bf16, two 128-row UMMA M tiles per CTA (256 TMEM columns),
+//    128 weight rows (UMMA N) per CTA, K in steps of 64 (one Q3H_B64 block per
+//    row).  Warps: 0 TMA producer, 1 TMEM allocator + single-thread
+//    tcgen05.mma issuer (kind::f16), 2-5 (Q3H_B64: 2-9, two threads per row)
+//    dequantizers -- each row's packed bytes prefetched 6 stages ahead with
+//    cp.async into a padded ring (odd 16-byte chunk stride: conflict-free),
+//    Eq. 2 -> bf16 straight into the UMMA canonical K-major SW128
+//    layout, fence.proxy.async, mbarrier arrive -- then 2-5 run the TMEM
+//    epilogue (tcgen05.ld 32x32b).
+//  * qgemv_tc_kernel -- a4 batched decode (2 <= B <= 64): weights on the UMMA M
+//    side (128 rows), x on N = 2 Bpad columns (fp16 hi + lo, Q23);
+//    see the comment above the kernel.
+// Split-K over gridDim.z by a small cost model (partials combined with red.add).
 #include <cuda.h>
 
 #include <algorithm>
@@ -44,7 +38,7 @@ constexpr int TC_THREADS = 256;
 template <int QT, int BS, bool DEC>
 struct TcVar {
   // prefill Q3H_B64: 8 dequant warps (two threads per weight row, exact fp32 Eq. 2)
-  static constexpr bool FAST = !DEC && QT == 35 && BS == 64;
+  static constexpr bool FAST = QT == 35 && BS == 64;
   static constexpr int THREADS = FAST ? 320 : 256;
   static constexpr int NDEQ = FAST ? 256 : 128;  // dequant threads (b_full arrivals)
 };
@@ -62,7 +56,7 @@ __host__ __device__ constexpr int tc_sbpad(int qt, int bs) {
 template <bool DEC, int SBPAD = 48>
 struct TcCfg {
   static constexpr int MT = DEC ? 1 : 2;          // UMMA M tiles per CTA
-  static constexpr int STAGES = (DEC && SBPAD <= 48) ? 4 : 3;
+  static constexpr int STAGES = (DEC && SBPAD <= 48) ? 4 : 3;  // (DEC: historical decode mode, unused)
   static constexpr int STAGE_BYTES = MT * TC_A_BYTES + TC_B_BYTES;
   static constexpr int TMEM_COLS = MT * TC_BN;
 };
@@ -344,13 +338,11 @@ __global__ void __launch_bounds__(TcVar<QT, BS, DEC>::THREADS, 1)
   extern __shared__ unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   unsigned char* pring = smem + STAGES * STAGE_BYTES;  // [TC_PK][TC_BN][SBPAD] raw weight bytes
-  float* xraw = reinterpret_cast<float*>(pring + TC_PK * TC_BN * SBPAD);  // decode: [nxr][Bpad][64] raw x
-  uint64_t* a_full = reinterpret_cast<uint64_t*>(reinterpret_cast<unsigned char*>(xraw) + (DEC ? TC_XRING : 0));
+  uint64_t* a_full = reinterpret_cast<uint64_t*>(pring + TC_PK * TC_BN * SBPAD);
   uint64_t* b_full = a_full + STAGES;
   uint64_t* empty = b_full + STAGES;
   uint64_t* acc_full = empty + STAGES;
-  uint64_t* xr_full = acc_full + 1;  // [TC_XRMAX]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(xr_full + TC_XRMAX);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_full + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // grid (m tiles, n tiles, splits): the CTAs sharing a weight tile are adjacent in
@@ -365,21 +357,12 @@ __global__ void __launch_bounds__(TcVar<QT, BS, DEC>::THREADS, 1)
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; s++) {
-      mbar_init(&a_full[s], DEC ? TC_CONV : 1);
+      mbar_init(&a_full[s], 1);
       mbar_init(&b_full[s], Var::NDEQ);
       mbar_init(&empty[s], 1);
     }
     mbar_init(acc_full, 1);
-    for (int i = 0; i < TC_XRMAX; i++) mbar_init(&xr_full[i], 1);
     fence_mbar_init();
-  }
-  if constexpr (DEC) {
-    // A tiles: rows of tokens >= B are never written by the converter -> zero them
-    for (int i = threadIdx.x; i < STAGES * TC_A_BYTES / 16; i += blockDim.x) {
-      const int s = i / (TC_A_BYTES / 16), o = i % (TC_A_BYTES / 16);
-      reinterpret_cast<uint4*>(smem + s * STAGE_BYTES)[o] = make_uint4(0u, 0u, 0u, 0u);
-    }
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
@@ -392,27 +375,8 @@ __global__ void __launch_bounds__(TcVar<QT, BS, DEC>::THREADS, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  const int conv_first = 6;  // decode-mode converter warps: 0 and 6, 7
-  if (warp == 0 || (DEC && warp >= conv_first)) {
-    if constexpr (DEC) {
-      // ---------------- converters: x fp32 -> fp16 hi/lo A tiles ----------------
-      const int cidx = warp == 0 ? 0 : warp - conv_first + 1;
-      const bool issuer = warp == 0 && lane == 0;
-      const int bpad = tc_bpad((int)M), nxr = tc_nxr((int)M), xslot = bpad * TC_BK;
-      if (issuer)
-        for (int i = 0; i < nxr && i < nks; i++) issue_x_stage(&xmap, ks0 + i, xraw + i * xslot, &xr_full[i], bpad);
-      for (int i = 0; i < nks; i++) {
-        const int s = i % STAGES, xs = i % nxr;
-        mbar_wait(&empty[s], ((i / STAGES) & 1) ^ 1);
-        mbar_wait(&xr_full[xs], (i / nxr) & 1);
-        convert_x_tile<false>(xraw + xs * xslot, (int)M, smem + s * STAGE_BYTES, cidx);
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> tensor core reads
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&a_full[s]);
-        named_bar_sync(3, TC_CONV * 32);  // every converter is done with this raw-x slot
-        if (issuer && i + nxr < nks) issue_x_stage(&xmap, ks0 + i + nxr, xraw + xs * xslot, &xr_full[xs], bpad);
-      }
-    } else if (lane == 0) {
+  if (warp == 0) {
+    if (lane == 0) {
       // ---------------- TMA producer: X tiles ----------------
       asm volatile("prefetch.tensormap [%0];" ::"l"(&xmap) : "memory");
       for (int i = 0; i < nks; i++) {
@@ -427,7 +391,7 @@ __global__ void __launch_bounds__(TcVar<QT, BS, DEC>::THREADS, 1)
   } else if (warp == 1) {
     // ---------------- MMA issuer (one thread) ----------------
     if (lane == 0) {
-      constexpr uint32_t idesc = DEC ? umma_idesc_f16(TC_BM, TC_BN) : umma_idesc_bf16(TC_BM, TC_BN);
+      constexpr uint32_t idesc = umma_idesc_bf16(TC_BM, TC_BN);
       for (int i = 0; i < nks; i++) {
         const int s = i % STAGES;
         const uint32_t par = (i / STAGES) & 1;
@@ -507,66 +471,36 @@ __global__ void __launch_bounds__(TcVar<QT, BS, DEC>::THREADS, 1)
     mbar_wait(acc_full, 0);
     tc_fence_after();
     const int q = warp & 3;  // TMEM lane quarter this warp may access
-    if constexpr (DEC) {
-      // lanes 64..127 hold the lo rows: quarters 2, 3 hand them to quarters 0, 1
-      float* xch = reinterpret_cast<float*>(smem);  // [64 tokens][32 cols], stage 0 (idle now)
+#pragma unroll
+    for (int mt = 0; mt < MT; mt++) {
+      const int64_t m = m0 + mt * TC_BM + q * 32 + lane;
 #pragma unroll
       for (int cc = 0; cc < TC_BN / 32; cc++) {
         uint32_t rr[32];
-        tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + cc * 32, rr);
-        if (q >= 2) {
+        tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + mt * TC_BN + cc * 32, rr);
+        const int64_t nbase = n0 + cc * 32;
+        if (m < M && nks > 0) {
+          float* yrow = Y + m * N + nbase;
+          if (nbase + 32 <= N && (N % 4) == 0) {
 #pragma unroll
-          for (int j = 0; j < 32; j++) xch[((q - 2) * 32 + lane) * 33 + j] = __uint_as_float(rr[j]);
-        }
-        named_bar_sync(2, 128);
-        if (q < 2) {
-          const int64_t m = q * 32 + lane;
-          const int64_t nbase = n0 + cc * 32;
-          if (m < M && nks > 0) {
-            float* yrow = Y + m * N + nbase;
-            for (int j = 0; j < 32; j++) {
-              const float v = __uint_as_float(rr[j]) + xch[(q * 32 + lane) * 33 + j];
+            for (int j = 0; j < 32; j += 4) {
+              if (atomic_out) {
+                asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(yrow + j), "f"(__uint_as_float(rr[j])),
+                             "f"(__uint_as_float(rr[j + 1])), "f"(__uint_as_float(rr[j + 2])), "f"(__uint_as_float(rr[j + 3]))
+                             : "memory");
+              } else {
+                *reinterpret_cast<float4*>(yrow + j) = make_float4(__uint_as_float(rr[j]), __uint_as_float(rr[j + 1]),
+                                                                   __uint_as_float(rr[j + 2]), __uint_as_float(rr[j + 3]));
+              }
+            }
+          } else {
+            for (int j = 0; j < 32; j++)
               if (nbase + j < N) {
-                if (atomic_out) atomicAdd(yrow + j, v);
-                else yrow[j] = v;
+                if (atomic_out)
+                  atomicAdd(yrow + j, __uint_as_float(rr[j]));
+                else
+                  yrow[j] = __uint_as_float(rr[j]);
               }
-            }
-          }
-        }
-        named_bar_sync(2, 128);
-      }
-    } else {
-#pragma unroll
-      for (int mt = 0; mt < MT; mt++) {
-        const int64_t m = m0 + mt * TC_BM + q * 32 + lane;
-#pragma unroll
-        for (int cc = 0; cc < TC_BN / 32; cc++) {
-          uint32_t rr[32];
-          tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + mt * TC_BN + cc * 32, rr);
-          const int64_t nbase = n0 + cc * 32;
-          if (m < M && nks > 0) {
-            float* yrow = Y + m * N + nbase;
-            if (nbase + 32 <= N && (N % 4) == 0) {
-#pragma unroll
-              for (int j = 0; j < 32; j += 4) {
-                if (atomic_out) {
-                  asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(yrow + j), "f"(__uint_as_float(rr[j])),
-                               "f"(__uint_as_float(rr[j + 1])), "f"(__uint_as_float(rr[j + 2])), "f"(__uint_as_float(rr[j + 3]))
-                               : "memory");
-                } else {
-                  *reinterpret_cast<float4*>(yrow + j) = make_float4(__uint_as_float(rr[j]), __uint_as_float(rr[j + 1]),
-                                                                     __uint_as_float(rr[j + 2]), __uint_as_float(rr[j + 3]));
-                }
-              }
-            } else {
-              for (int j = 0; j < 32; j++)
-                if (nbase + j < N) {
-                  if (atomic_out)
-                    atomicAdd(yrow + j, __uint_as_float(rr[j]));
-                  else
-                    yrow[j] = __uint_as_float(rr[j]);
-                }
-            }
           }
         }
       }
