@@ -143,7 +143,9 @@ def run_reference(args):
         "impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": ws,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_layer * L * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"llama2-{args.model}-stack q3h_b64 decode b={args.batch}", "batch": args.batch},
+        "config": {"workload": f"llama2-{args.model}-stack q3h_b64 decode b={args.batch}",
+                   "model": f"llama2-{args.model}-shaped", "global_batch": args.batch, "seq_len": 1,
+                   "parallelism": "single", "scheme": "Q3H_B64 (4.0 bits/weight)"},
         "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": 1, "kind": "oracle", "sample": sample},
         "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
