@@ -514,6 +514,24 @@ __global__ void __launch_bounds__(TcVar<QT, BS, DEC>::THREADS, 1)
   }
 }
 
+// x fp32 [B, K] -> X2 fp16 [2 bp, K]: rows [0, bp) = hi(x), rows [bp, 2 bp) = lo(x) =
+// x - hi (zero rows for tokens >= B).  Run once per qGEMV when the caller provides
+// scratch; the decode kernel then loads its x tiles with one SWIZZLE_128B TMA per stage
+// instead of converting per CTA (every CTA would otherwise redo it).
+__global__ void __launch_bounds__(256) x_split_kernel(const float* __restrict__ x, int B, int64_t K, int bp,
+                                                      __half* __restrict__ x2) {
+  pdl_trigger();
+  pdl_wait();
+  const int64_t total = (int64_t)bp * K;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t t = i / K, k = i - t * K;
+    const float v = t < B ? x[t * K + k] : 0.f;
+    const __half h = __float2half_rn(v);
+    x2[i] = h;
+    x2[(int64_t)bp * K + i] = __float2half_rn(v - __half2float(h));
+  }
+}
+
 // ---------------------------------------------------------------------------
 // a4 batched decode, weights on the UMMA M side: D[n, j] = sum_k W'[n, k] X[j, k]
 // with M = 128 weight rows and N = 2 Bp columns (x hi of token t in column t,
@@ -606,7 +624,7 @@ template <int QT, int BS>
 __global__ void __launch_bounds__(TcdVar<QT, BS>::THREADS, 1)
     qgemv_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap wmap,
                     const uint8_t* __restrict__ W, int64_t N, int64_t K, int B, float* __restrict__ Y,
-                    int ksteps_per_split, int atomic_out, int stages) {
+                    int ksteps_per_split, int atomic_out, int stages, int xpre) {
   constexpr int SBPAD = tc_sbpad(QT, BS);
   using V = TcdVar<QT, BS>;
   pdl_trigger();
@@ -636,7 +654,7 @@ __global__ void __launch_bounds__(TcdVar<QT, BS>::THREADS, 1)
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < stages; s++) {
-      mbar_init(&a_full[s], TC_CONV);
+      mbar_init(&a_full[s], xpre ? 1 : TC_CONV);
       mbar_init(&b_full[s], V::NDEQ);
       mbar_init(&empty[s], 1);
     }
@@ -676,7 +694,18 @@ __global__ void __launch_bounds__(TcdVar<QT, BS>::THREADS, 1)
         tma_load_2d(pring + ws * 4096, &wmap, (ks0 + i) * 32, (int)n0, &wfull[ws]);
       }
     }
-  } else if (warp == 0 || (warp >= V::CONV1 && warp < V::CONV1 + 2)) {
+  } else if (xpre && warp == 0) {
+    // ---------------- x tiles pre-split by x_split_kernel: one SWIZZLE_128B TMA per stage ----------------
+    if (lane == 0) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"(&xmap) : "memory");
+      for (int i = 0; i < nks; i++) {
+        const int s = i % stages;
+        mbar_wait(&empty[s], ((i / stages) & 1) ^ 1);
+        mbar_arrive_expect_tx(&a_full[s], (uint32_t)(ncols * 128));
+        tma_load_2d(smem + s * stage_bytes + TC_B_BYTES, &xmap, (ks0 + i) * TC_BK, 0, &a_full[s]);
+      }
+    }
+  } else if (!xpre && (warp == 0 || (warp >= V::CONV1 && warp < V::CONV1 + 2))) {
     // ---------------- converters: raw fp32 x (2D TMA ring) -> fp16 hi/lo x tiles ----------------
     const int cidx = warp == 0 ? 0 : warp - V::CONV1 + 1;
     const bool issuer = warp == 0 && lane == 0;
@@ -716,15 +745,15 @@ __global__ void __launch_bounds__(TcdVar<QT, BS>::THREADS, 1)
       }
       umma_commit(acc_full);
     }
-  } else if (V::FAST && warp >= 6) {
+  } else if (V::FAST && warp >= 6 && warp < 10) {
     // ---------------- Q3H_B64 dequantizers, second half of the 8 warps ----------------
     // (warps 2-9: 16 rows each, lane pairs = the two halves of a row; warps 2-5
     //  run the epilogue below after the same loop)
     qgemv_fast_deq(N, K, n0, ks0, nks, stages, stage_bytes, smem, pring, wfull, wempty, empty, b_full, warp, lane);
-  } else if (V::FAST) {
+  } else if (V::FAST && warp >= 2 && warp < 6) {
     qgemv_fast_deq(N, K, n0, ks0, nks, stages, stage_bytes, smem, pring, wfull, wempty, empty, b_full, warp, lane);
     qgemv_epilogue(tmem, acc_full, Y, N, B, bp, n0, nks, atomic_out, warp, lane);
-  } else {
+  } else if (!V::FAST && warp >= 2 && warp < 6) {
     // ---------------- dequantizers: one weight row per thread (Eq. 2 in fp32, -> fp16) ----------------
     const int r = threadIdx.x - 64;  // 0..127
     const int64_t n = n0 + r;
@@ -851,7 +880,7 @@ if_status qgemm_tc_launch(if_scheme s, const uint8_t* W, int64_t N, int64_t K, c
 }
 
 if_status qgemv_tc_launch(if_scheme s, const uint8_t* W, int64_t N, int64_t K, const float* x, int64_t B, float* Y,
-                          int accumulate, cudaStream_t st) {
+                          int accumulate, cudaStream_t st, void* x2_scratch, size_t x2_bytes) {
   if (B < 1 || B > 64 || K % 8 != 0 || (reinterpret_cast<uintptr_t>(x) & 15u) || N > (int64_t)1 << 30)
     return IF_ERR_UNSUPPORTED;
   const int64_t row_bytes = K / s.block * q_block_bytes(s.type, s.block);
@@ -866,6 +895,34 @@ if_status qgemv_tc_launch(if_scheme s, const uint8_t* W, int64_t N, int64_t K, c
                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (cr != CUDA_SUCCESS) return set_error(IF_ERR_CUDA, "qgemv_tc: cuTensorMapEncodeTiled failed (%d)", (int)cr);
+  // caller scratch for fp16 hi/lo x: split once, TMA-load the tiles (no per-CTA conversion)
+  const int bp = tc_bpad((int)B), ncols = tcd_ncols((int)B);
+  const int xpre = x2_scratch && x2_bytes >= (size_t)ncols * K * 2 && !(reinterpret_cast<uintptr_t>(x2_scratch) & 15u);
+  if (xpre) {
+    __half* x2 = reinterpret_cast<__half*>(x2_scratch);
+    cudaLaunchConfig_t lc = {};
+    lc.gridDim = dim3((unsigned)std::min<int64_t>(((int64_t)bp * K + 255) / 256, 148 * 8));
+    lc.blockDim = dim3(256);
+    lc.stream = st;
+    cudaLaunchAttribute la[1];
+    la[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    la[0].val.programmaticStreamSerializationAllowed = 1;
+    lc.attrs = la;
+    lc.numAttrs = 1;
+    const float* xa = x;
+    int Bi = (int)B, bpi = bp;
+    int64_t Ki = K;
+    __half* x2a = x2;
+    void* args[] = {(void*)&xa, (void*)&Bi, (void*)&Ki, (void*)&bpi, (void*)&x2a};
+    cudaLaunchKernelExC(&lc, (const void*)x_split_kernel, args);
+    count_launch();
+    cuuint64_t xd[2] = {(cuuint64_t)K, (cuuint64_t)ncols};
+    cuuint64_t xs[1] = {(cuuint64_t)K * 2};
+    cuuint32_t xb[2] = {(cuuint32_t)TC_BK, (cuuint32_t)ncols};
+    cr = g_encode(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, x2, xd, xs, xb, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (cr != CUDA_SUCCESS) return set_error(IF_ERR_CUDA, "qgemv_tc: x2 tensor map failed (%d)", (int)cr);
+  }
   const int ntile = (int)((N + TC_BN - 1) / TC_BN);
   const int ktotal = (int)((K + TC_BK - 1) / TC_BK);
   const int splits = tc_splits(ntile, ktotal);
@@ -908,7 +965,7 @@ if_status qgemv_tc_launch(if_scheme s, const uint8_t* W, int64_t N, int64_t K, c
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = splits > 1 && !accumulate ? 0 : 1;  // (after the split-K memset: plain stream order)
-    cudaLaunchKernelEx(&cfg, kern, map, wmap, W, N, K, (int)B, Y, kper, atomic_out, stages);
+    cudaLaunchKernelEx(&cfg, kern, map, wmap, W, N, K, (int)B, Y, kper, atomic_out, stages, xpre);
     count_launch();
     return check_launch("qgemv_tc");
   });

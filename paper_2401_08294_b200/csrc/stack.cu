@@ -140,6 +140,8 @@ struct WS {
   float* part;
   int* done;  // decode engine: phase counters [4 * MK_MAXL] + epoch
   float* xsimg;  // 3 transformed-input images + sum-h^2 partials (decode engine)
+  void* x2;      // batched decode: fp16 hi/lo split of a qGEMV input (2 x 64 x maxK halves)
+  size_t x2_bytes;
   size_t bytes;
 };
 
@@ -162,6 +164,9 @@ static WS carve(void* base, const Local& L, int64_t T) {
   // 3 images of 16 x xstride float4 (xstride <= nbp_max + 9) + 256 floats
   const size_t nbp_max = (size_t)((std::max(std::max(L.d, L.nq), L.lf) / 64 + 31) / 32) * 32;
   w.xsimg = take(3 * 16 * (nbp_max + 16) * 4 + 256);
+  const size_t maxK = (size_t)std::max(std::max(L.d, L.nq), L.lf);
+  w.x2 = take(64 * maxK);  // 2 x 64 x maxK fp16
+  w.x2_bytes = 64 * maxK * 4;
   w.bytes = off;
   return w;
 }
@@ -274,28 +279,28 @@ extern "C" if_status if_run_stack(const if_stack_shape* shape, const if_plan* pl
       launch_pdl(rmsnorm_kernel<float>, (unsigned)T, 256, cs, (const float*)h_out, w.a, (int)L.d, w.qkv,
                  (int64_t)T * L.nqkv);
       count_launch();
-      if ((st = if_qgemv_acc(sc, Wl.wqkv, L.nqkv, L.d, w.a, T, w.qkv, stream))) return st;
+      if ((st = qgemv_dispatch("if_run_stack(qkv)", sc, Wl.wqkv, L.nqkv, L.d, w.a, T, w.qkv, 1, cs, w.x2, w.x2_bytes))) return st;
       launch_pdl(vbcast_kernel<float>, (unsigned)ew_grid(T * L.nq), 256, cs, (const float*)w.qkv, w.ctx, (int)T,
                  (int)L.lh, (int)L.lkv, (int)L.hd, (int)asg.head_begin, (int)asg.kv_begin, (int)per);
       count_launch();
       if (groups == 1) {
-        if ((st = if_qgemv_acc(sc, Wl.wo, L.d, L.nq, w.ctx, T, h_out, stream))) return st;
+        if ((st = qgemv_dispatch("if_run_stack(o)", sc, Wl.wo, L.d, L.nq, w.ctx, T, h_out, 1, cs, w.x2, w.x2_bytes))) return st;
       } else {
-        if ((st = if_qgemv(sc, Wl.wo, L.d, L.nq, w.ctx, T, w.part, stream))) return st;
+        if ((st = qgemv_dispatch("if_run_stack(o)", sc, Wl.wo, L.d, L.nq, w.ctx, T, w.part, 0, cs, w.x2, w.x2_bytes))) return st;
         if ((st = comm_allreduce_into(comm, w.part, h_out, nh, 1, cs))) return st;  // merge #1
       }
       // ---- feed-forward sub-layer ----
       launch_pdl(rmsnorm_kernel<float>, (unsigned)T, 256, cs, (const float*)h_out, w.a, (int)L.d, w.gu,
                  (int64_t)T * 2 * L.lf);
       count_launch();
-      if ((st = if_qgemv_acc(sc, Wl.wgu, 2 * L.lf, L.d, w.a, T, w.gu, stream))) return st;
+      if ((st = qgemv_dispatch("if_run_stack(gu)", sc, Wl.wgu, 2 * L.lf, L.d, w.a, T, w.gu, 1, cs, w.x2, w.x2_bytes))) return st;
       launch_pdl(silu_mul_kernel<float>, (unsigned)ew_grid(T * L.lf), 256, cs, (const float*)w.gu, w.act, (int)T,
                  (int)L.lf);
       count_launch();
       if (groups == 1) {
-        if ((st = if_qgemv_acc(sc, Wl.wdown, L.d, L.lf, w.act, T, h_out, stream))) return st;
+        if ((st = qgemv_dispatch("if_run_stack(down)", sc, Wl.wdown, L.d, L.lf, w.act, T, h_out, 1, cs, w.x2, w.x2_bytes))) return st;
       } else {
-        if ((st = if_qgemv(sc, Wl.wdown, L.d, L.lf, w.act, T, w.part, stream))) return st;
+        if ((st = qgemv_dispatch("if_run_stack(down)", sc, Wl.wdown, L.d, L.lf, w.act, T, w.part, 0, cs, w.x2, w.x2_bytes))) return st;
         if ((st = comm_allreduce_into(comm, w.part, h_out, nh, 1, cs))) return st;  // merge #2
       }
     } else {
