@@ -64,7 +64,6 @@ struct TcCfg {
 // up to 8/16/32/64): 24 slots at B <= 8 ... 3 at B = 64 (deep L2 prefetch)
 constexpr int TC_XRING = 48 * 1024;
 constexpr int TC_XRMAX = 16;
-__host__ __device__ constexpr int tc_bpad(int B) { return B <= 8 ? 8 : B <= 16 ? 16 : B <= 32 ? 32 : 64; }
 __host__ __device__ constexpr int tc_nxr(int B) {
   return TC_XRING / (tc_bpad(B) * TC_BK * 4) < TC_XRMAX ? TC_XRING / (tc_bpad(B) * TC_BK * 4) : TC_XRMAX;
 }
@@ -880,7 +879,7 @@ if_status qgemm_tc_launch(if_scheme s, const uint8_t* W, int64_t N, int64_t K, c
 }
 
 if_status qgemv_tc_launch(if_scheme s, const uint8_t* W, int64_t N, int64_t K, const float* x, int64_t B, float* Y,
-                          int accumulate, cudaStream_t st, void* x2_scratch, size_t x2_bytes) {
+                          int accumulate, cudaStream_t st, void* x2_scratch, size_t x2_bytes, int x2_ready) {
   if (B < 1 || B > 64 || K % 8 != 0 || (reinterpret_cast<uintptr_t>(x) & 15u) || N > (int64_t)1 << 30)
     return IF_ERR_UNSUPPORTED;
   const int64_t row_bytes = K / s.block * q_block_bytes(s.type, s.block);
@@ -900,6 +899,7 @@ if_status qgemv_tc_launch(if_scheme s, const uint8_t* W, int64_t N, int64_t K, c
   const int xpre = x2_scratch && x2_bytes >= (size_t)ncols * K * 2 && !(reinterpret_cast<uintptr_t>(x2_scratch) & 15u);
   if (xpre) {
     __half* x2 = reinterpret_cast<__half*>(x2_scratch);
+    if (!x2_ready) {
     cudaLaunchConfig_t lc = {};
     lc.gridDim = dim3((unsigned)std::min<int64_t>(((int64_t)bp * K + 255) / 256, 148 * 8));
     lc.blockDim = dim3(256);
@@ -916,6 +916,7 @@ if_status qgemv_tc_launch(if_scheme s, const uint8_t* W, int64_t N, int64_t K, c
     void* args[] = {(void*)&xa, (void*)&Bi, (void*)&Ki, (void*)&bpi, (void*)&x2a};
     cudaLaunchKernelExC(&lc, (const void*)x_split_kernel, args);
     count_launch();
+    }
     cuuint64_t xd[2] = {(cuuint64_t)K, (cuuint64_t)ncols};
     cuuint64_t xs[1] = {(cuuint64_t)K * 2};
     cuuint32_t xb[2] = {(cuuint32_t)TC_BK, (cuuint32_t)ncols};

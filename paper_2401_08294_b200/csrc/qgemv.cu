@@ -291,7 +291,7 @@ static void launch_generic_t(if_scheme s, const uint8_t* W, int64_t N, int64_t K
 
 static if_status qgemv_impl(const char* fn, if_scheme s, const uint8_t* W, int64_t N, int64_t K,
                             const float* x, int64_t B, float* y, int acc, if_stream_t stream,
-                            void* x2_scratch = nullptr, size_t x2_bytes = 0) {
+                            void* x2_scratch = nullptr, size_t x2_bytes = 0, int x2_ready = 0) {
   if (!scheme_ok(s)) return set_error(IF_ERR_SCHEME, "%s: invalid scheme type=%d block=%d", fn, s.type, s.block);
   if (N < 0 || K < 0 || K % s.block) return set_error(IF_ERR_SHAPE, "%s: N=%lld K=%lld", fn, (long long)N, (long long)K);
   if (B < 1 || B > 64) return set_error(IF_ERR_ARG, "%s: B=%lld outside 1..64", fn, (long long)B);
@@ -308,7 +308,7 @@ static if_status qgemv_impl(const char* fn, if_scheme s, const uint8_t* W, int64
   }
   if (B >= 2) {
     // batched decode: the tensor cores (fp16 W', fp16 hi/lo x), weights streamed once
-    if_status r = qgemv_tc_launch(s, W, N, K, x, B, y, acc, st, x2_scratch, x2_bytes);
+    if_status r = qgemv_tc_launch(s, W, N, K, x, B, y, acc, st, x2_scratch, x2_bytes, x2_ready);
     if (r != IF_ERR_UNSUPPORTED) return r;
   }
   if (s.type == IF_Q3H && s.block == 64 && (reinterpret_cast<uintptr_t>(W) & 31u) == 0 && N < (1ll << 31)) {
@@ -341,8 +341,9 @@ static if_status qgemv_impl(const char* fn, if_scheme s, const uint8_t* W, int64
 }
 
 if_status qgemv_dispatch(const char* fn, if_scheme s, const uint8_t* W, int64_t N, int64_t K, const float* x,
-                         int64_t B, float* y, int acc, cudaStream_t st, void* x2_scratch, size_t x2_bytes) {
-  return qgemv_impl(fn, s, W, N, K, x, B, y, acc, (if_stream_t)st, x2_scratch, x2_bytes);
+                         int64_t B, float* y, int acc, cudaStream_t st, void* x2_scratch, size_t x2_bytes,
+                         int x2_ready) {
+  return qgemv_impl(fn, s, W, N, K, x, B, y, acc, (if_stream_t)st, x2_scratch, x2_bytes, x2_ready);
 }
 
 }  // namespace ifb

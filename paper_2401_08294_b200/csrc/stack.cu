@@ -27,16 +27,29 @@ __device__ __forceinline__ __nv_bfloat16 to_out<__nv_bfloat16>(float v) {
   return __float2bfloat16(v);
 }
 
+// optional fp16 hi/lo split of a glue kernel's output for the tensor-core qGEMV that
+// reads it (x2 [2 bp, K]: row t = hi, row bp + t = lo), so no separate split launch
+__device__ __forceinline__ void put_x2(__half* x2, int bp, int64_t K, int64_t t, int64_t k, float v) {
+  const __half h = __float2half_rn(v);
+  x2[t * K + k] = h;
+  x2[((int64_t)bp + t) * K + k] = __float2half_rn(v - __half2float(h));
+}
+
 // a[t] = h[t] / sqrt(mean(h[t]^2) + 1e-5)
 // (zbuf, zn: optionally zero the next qGEMV's output, which then accumulates --
 //  no memset node, so the chain stays programmatic)
 template <typename OutT>
 __global__ void __launch_bounds__(256) rmsnorm_kernel(const float* __restrict__ h, OutT* __restrict__ a, int d,
-                                                      float* __restrict__ zbuf = nullptr, int64_t zn = 0) {
+                                                      float* __restrict__ zbuf = nullptr, int64_t zn = 0,
+                                                      __half* __restrict__ x2 = nullptr, int T = 0, int bp = 0) {
   pdl_trigger();
   pdl_wait();
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < zn; i += (int64_t)gridDim.x * blockDim.x)
     zbuf[i] = 0.f;
+  if (x2 && (int)blockIdx.x >= T) {  // padding token rows of the split
+    for (int i = threadIdx.x; i < d; i += blockDim.x) put_x2(x2, bp, d, blockIdx.x, i, 0.f);
+    return;
+  }
   __shared__ float red[8];
   const float* hr = h + (int64_t)blockIdx.x * d;
   float ss = 0.f;
@@ -49,35 +62,52 @@ __global__ void __launch_bounds__(256) rmsnorm_kernel(const float* __restrict__ 
   for (int w = 0; w < (int)(blockDim.x >> 5); w++) tot += red[w];
   const float inv = 1.0f / sqrtf(tot / (float)d + 1e-5f);
   OutT* ar = a + (int64_t)blockIdx.x * d;
-  for (int i = threadIdx.x; i < d; i += blockDim.x) ar[i] = to_out<OutT>(hr[i] * inv);
+  for (int i = threadIdx.x; i < d; i += blockDim.x) {
+    const float v = hr[i] * inv;
+    ar[i] = to_out<OutT>(v);
+    if (x2) put_x2(x2, bp, d, blockIdx.x, i, v);
+  }
 }
 
 // ctx[t, i*hd + e] = v[t, j*hd + e],  j = floor((h0 + i)/(H/G)) - k0  (local heads/kv-heads)
 template <typename OutT>
 __global__ void vbcast_kernel(const float* __restrict__ qkv, OutT* __restrict__ ctx, int T, int lh, int lkv, int hd,
-                              int h0, int k0, int per) {
+                              int h0, int k0, int per, __half* __restrict__ x2 = nullptr, int bp = 0) {
   pdl_trigger();
   pdl_wait();
   const int64_t nq = (int64_t)lh * hd, nqkv = (int64_t)(lh + 2 * lkv) * hd;
-  const int64_t total = (int64_t)T * nq;
+  const int64_t total = (int64_t)(x2 ? bp : T) * nq;
   for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total; idx += (int64_t)gridDim.x * blockDim.x) {
     const int64_t t = idx / nq, r = idx - t * nq;
+    if (t >= T) {
+      put_x2(x2, bp, nq, t, r, 0.f);
+      continue;
+    }
     const int i = (int)(r / hd), e = (int)(r - (int64_t)i * hd);
     const int j = (h0 + i) / per - k0;
-    ctx[idx] = to_out<OutT>(qkv[t * nqkv + (int64_t)(lh + lkv) * hd + (int64_t)j * hd + e]);
+    const float v = qkv[t * nqkv + (int64_t)(lh + lkv) * hd + (int64_t)j * hd + e];
+    ctx[idx] = to_out<OutT>(v);
+    if (x2) put_x2(x2, bp, nq, t, r, v);
   }
 }
 
 // act[t, f] = silu(g) * u with gate/up rows interleaved: g = gu[t, 2f], u = gu[t, 2f+1]
 template <typename OutT>
-__global__ void silu_mul_kernel(const float* __restrict__ gu, OutT* __restrict__ act, int T, int lf) {
+__global__ void silu_mul_kernel(const float* __restrict__ gu, OutT* __restrict__ act, int T, int lf,
+                                __half* __restrict__ x2 = nullptr, int bp = 0) {
   pdl_trigger();
   pdl_wait();
-  const int64_t total = (int64_t)T * lf;
+  const int64_t total = (int64_t)(x2 ? bp : T) * lf;
   for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total; idx += (int64_t)gridDim.x * blockDim.x) {
     const int64_t t = idx / lf, f = idx - t * lf;
+    if (t >= T) {
+      put_x2(x2, bp, lf, t, f, 0.f);
+      continue;
+    }
     const float g = gu[t * 2 * lf + 2 * f], u = gu[t * 2 * lf + 2 * f + 1];
-    act[idx] = to_out<OutT>(g / (1.0f + expf(-g)) * u);
+    const float v = g / (1.0f + expf(-g)) * u;
+    act[idx] = to_out<OutT>(v);
+    if (x2) put_x2(x2, bp, lf, t, f, v);
   }
 }
 
@@ -271,36 +301,49 @@ extern "C" if_status if_run_stack(const if_stack_shape* shape, const if_plan* pl
       return check_launch("if_run_stack");
     }
   }
+  // batched decode (2 <= T <= 64): the glue kernels also write the fp16 hi/lo split of
+  // the next qGEMV's input into the workspace (x2r: no separate split launch)
+  const bool use_x2 = mode == IF_DECODE && T >= 2;
+  __half* x2h = use_x2 ? reinterpret_cast<__half*>(w.x2) : nullptr;
+  const int bpx = use_x2 ? tc_bpad((int)T) : 0;
+  const int x2r = use_x2 ? 1 : 0;
   for (int l = 0; l < nlayers; l++) {
     const if_layer_weights& Wl = stage_layers[l];
     if (!Wl.wqkv || !Wl.wo || !Wl.wgu || !Wl.wdown) return set_error(IF_ERR_ARG, "if_run_stack: null weights, layer %d", l);
     if (mode == IF_DECODE) {
       // ---- attention sub-layer ----
-      launch_pdl(rmsnorm_kernel<float>, (unsigned)T, 256, cs, (const float*)h_out, w.a, (int)L.d, w.qkv,
-                 (int64_t)T * L.nqkv);
+      launch_pdl(rmsnorm_kernel<float>, (unsigned)std::max<int64_t>(T, bpx), 256, cs, (const float*)h_out, w.a, (int)L.d,
+                 w.qkv, (int64_t)T * L.nqkv, x2h, (int)T, bpx);
       count_launch();
-      if ((st = qgemv_dispatch("if_run_stack(qkv)", sc, Wl.wqkv, L.nqkv, L.d, w.a, T, w.qkv, 1, cs, w.x2, w.x2_bytes))) return st;
-      launch_pdl(vbcast_kernel<float>, (unsigned)ew_grid(T * L.nq), 256, cs, (const float*)w.qkv, w.ctx, (int)T,
-                 (int)L.lh, (int)L.lkv, (int)L.hd, (int)asg.head_begin, (int)asg.kv_begin, (int)per);
+      if ((st = qgemv_dispatch("if_run_stack(qkv)", sc, Wl.wqkv, L.nqkv, L.d, w.a, T, w.qkv, 1, cs, w.x2, w.x2_bytes, x2r)))
+        return st;
+      launch_pdl(vbcast_kernel<float>, (unsigned)ew_grid(std::max<int64_t>(T, bpx) * L.nq), 256, cs, (const float*)w.qkv,
+                 w.ctx, (int)T, (int)L.lh, (int)L.lkv, (int)L.hd, (int)asg.head_begin, (int)asg.kv_begin, (int)per, x2h,
+                 bpx);
       count_launch();
       if (groups == 1) {
-        if ((st = qgemv_dispatch("if_run_stack(o)", sc, Wl.wo, L.d, L.nq, w.ctx, T, h_out, 1, cs, w.x2, w.x2_bytes))) return st;
+        if ((st = qgemv_dispatch("if_run_stack(o)", sc, Wl.wo, L.d, L.nq, w.ctx, T, h_out, 1, cs, w.x2, w.x2_bytes, x2r)))
+          return st;
       } else {
-        if ((st = qgemv_dispatch("if_run_stack(o)", sc, Wl.wo, L.d, L.nq, w.ctx, T, w.part, 0, cs, w.x2, w.x2_bytes))) return st;
+        if ((st = qgemv_dispatch("if_run_stack(o)", sc, Wl.wo, L.d, L.nq, w.ctx, T, w.part, 0, cs, w.x2, w.x2_bytes, x2r)))
+          return st;
         if ((st = comm_allreduce_into(comm, w.part, h_out, nh, 1, cs))) return st;  // merge #1
       }
       // ---- feed-forward sub-layer ----
-      launch_pdl(rmsnorm_kernel<float>, (unsigned)T, 256, cs, (const float*)h_out, w.a, (int)L.d, w.gu,
-                 (int64_t)T * 2 * L.lf);
+      launch_pdl(rmsnorm_kernel<float>, (unsigned)std::max<int64_t>(T, bpx), 256, cs, (const float*)h_out, w.a, (int)L.d,
+                 w.gu, (int64_t)T * 2 * L.lf, x2h, (int)T, bpx);
       count_launch();
-      if ((st = qgemv_dispatch("if_run_stack(gu)", sc, Wl.wgu, 2 * L.lf, L.d, w.a, T, w.gu, 1, cs, w.x2, w.x2_bytes))) return st;
-      launch_pdl(silu_mul_kernel<float>, (unsigned)ew_grid(T * L.lf), 256, cs, (const float*)w.gu, w.act, (int)T,
-                 (int)L.lf);
+      if ((st = qgemv_dispatch("if_run_stack(gu)", sc, Wl.wgu, 2 * L.lf, L.d, w.a, T, w.gu, 1, cs, w.x2, w.x2_bytes, x2r)))
+        return st;
+      launch_pdl(silu_mul_kernel<float>, (unsigned)ew_grid(std::max<int64_t>(T, bpx) * L.lf), 256, cs, (const float*)w.gu,
+                 w.act, (int)T, (int)L.lf, x2h, bpx);
       count_launch();
       if (groups == 1) {
-        if ((st = qgemv_dispatch("if_run_stack(down)", sc, Wl.wdown, L.d, L.lf, w.act, T, h_out, 1, cs, w.x2, w.x2_bytes))) return st;
+        if ((st = qgemv_dispatch("if_run_stack(down)", sc, Wl.wdown, L.d, L.lf, w.act, T, h_out, 1, cs, w.x2, w.x2_bytes, x2r)))
+          return st;
       } else {
-        if ((st = qgemv_dispatch("if_run_stack(down)", sc, Wl.wdown, L.d, L.lf, w.act, T, w.part, 0, cs, w.x2, w.x2_bytes))) return st;
+        if ((st = qgemv_dispatch("if_run_stack(down)", sc, Wl.wdown, L.d, L.lf, w.act, T, w.part, 0, cs, w.x2, w.x2_bytes, x2r)))
+          return st;
         if ((st = comm_allreduce_into(comm, w.part, h_out, nh, 1, cs))) return st;  // merge #2
       }
     } else {
