@@ -154,6 +154,10 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
+// small unsigned integer (< 2^23) -> float on the full-rate pipes (2^23 magic; I2F
+// runs at a fraction of the FMA rate)
+__device__ __forceinline__ float u2f_exact(uint32_t q) { return __uint_as_float(q | 0x4B000000u) - 8388608.0f; }
+
 // Prefetch the SB raw bytes of weight row n for K-stage ks (64 weights) into its
 // ring row (zeros are produced later by dequant_row for rows/stages out of range).
 template <int QT, int BS>
@@ -221,9 +225,9 @@ __device__ __forceinline__ void dequant_row(const unsigned char* raw, int64_t n,
         if constexpr (QT == 35) {
           const uint32_t q1 = (v * 187u) >> 11;  // floor(v/11) for v < 128
           const uint32_t q2 = v - 11u * q1;      // v mod 11
-          out[sub * (BS / 2) + j] = pack16x2<F16>(__fmaf_rn((float)q1, step, lo), __fmaf_rn((float)q2, step, lo));
+          out[sub * (BS / 2) + j] = pack16x2<F16>(__fmaf_rn(u2f_exact(q1), step, lo), __fmaf_rn(u2f_exact(q2), step, lo));
         } else {
-          const float wp = __fmaf_rn((float)v, step, lo);
+          const float wp = __fmaf_rn(u2f_exact(v), step, lo);
           if (j & 1)
             out[sub * (BS / 2) + j / 2] |= pack16x2<F16>(0.f, wp) & 0xFFFF0000u;
           else
