@@ -67,6 +67,14 @@ constexpr int TC_XRMAX = 16;
 __host__ __device__ constexpr int tc_nxr(int B) {
   return TC_XRING / (tc_bpad(B) * TC_BK * 4) < TC_XRMAX ? TC_XRING / (tc_bpad(B) * TC_BK * 4) : TC_XRMAX;
 }
+// wide prefill tiles (Q3H_B64, M > 256): 512 activations per weight tile, two
+// 128 x 256 TMEM accumulators (all 512 columns), two stages of 80 KB -- each W'
+// tile is dequantized once per 512 tokens instead of once per 256
+constexpr int TC_MTW = 4;
+constexpr int TC_STAGES_W = 2;
+__host__ __device__ constexpr int tc_smem_wide(int qt, int bs) {
+  return TC_STAGES_W * (TC_MTW * TC_A_BYTES + TC_B_BYTES) + TC_PK * TC_BN * tc_sbpad(qt, bs) + 1024 + 512;
+}
 template <bool DEC>
 __host__ __device__ constexpr int tc_smem(int qt, int bs) {
   return (tc_sbpad(qt, bs) <= 48 ? TcCfg<DEC, 48>::STAGES : TcCfg<DEC, 64>::STAGES) * TcCfg<DEC>::STAGE_BYTES +
@@ -330,13 +338,27 @@ __device__ __forceinline__ void dequant_q3h64_half_f32(const unsigned char* raw,
   }
 }
 
-template <int QT, int BS, bool DEC>
+#ifdef IFB_TC_PROF
+// instrumentation build only: per CTA {smid, t_start, t_mainloop_end, t_epilogue_end} (%globaltimer ns)
+__device__ unsigned long long g_tc_tl[8192][4];
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+extern "C" void ifx_tc_tl(void* host) { cudaMemcpyFromSymbol(host, g_tc_tl, sizeof(g_tc_tl)); }
+#endif
+template <int QT, int BS, bool DEC, bool WIDE = false>
 __global__ void __launch_bounds__(TcVar<QT, BS, DEC>::THREADS, 1)
     qgemm_tc_kernel(const __grid_constant__ CUtensorMap xmap, const float* __restrict__ xdec, const uint8_t* __restrict__ W,
                     int64_t N, int64_t K, int64_t M, float* __restrict__ Y, int ksteps_per_split, int atomic_out) {
   using Cfg = TcCfg<DEC, tc_sbpad(QT, BS)>;
   using Var = TcVar<QT, BS, DEC>;
-  constexpr int MT = Cfg::MT, STAGES = Cfg::STAGES, STAGE_BYTES = Cfg::STAGE_BYTES;
+  constexpr int MT = WIDE ? TC_MTW : Cfg::MT;
+  constexpr int STAGES = WIDE ? TC_STAGES_W : Cfg::STAGES;
+  constexpr int STAGE_BYTES = MT * TC_A_BYTES + TC_B_BYTES;
+  constexpr int TMEM_COLS = MT * TC_BM;    // 256 or 512 fp32 columns
+  constexpr int UN = MT * TC_BM > 256 ? 256 : MT * TC_BM;  // UMMA N (activations per MMA)
   constexpr int SBPAD = tc_sbpad(QT, BS);
   extern __shared__ unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -348,6 +370,15 @@ __global__ void __launch_bounds__(TcVar<QT, BS, DEC>::THREADS, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_full + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#ifdef IFB_TC_PROF
+  const int cta_id = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
+  if (threadIdx.x == 0 && cta_id < 8192) {
+    unsigned smid;
+    asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
+    g_tc_tl[cta_id][0] = smid;
+    g_tc_tl[cta_id][1] = gtimer();
+  }
+#endif
   // grid (m tiles, n tiles, splits): the CTAs sharing a weight tile are adjacent in
   // launch order, so the second read of the tile hits L2 instead of HBM
   const int64_t n0 = (int64_t)blockIdx.y * TC_BN;
@@ -369,7 +400,7 @@ __global__ void __launch_bounds__(TcVar<QT, BS, DEC>::THREADS, 1)
   }
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                 "n"(Cfg::TMEM_COLS)
+                 "n"(TMEM_COLS)
                  : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
@@ -394,7 +425,11 @@ __global__ void __launch_bounds__(TcVar<QT, BS, DEC>::THREADS, 1)
   } else if (warp == 1) {
     // ---------------- MMA issuer (one thread) ----------------
     if (lane == 0) {
-      constexpr uint32_t idesc = umma_idesc_bf16(TC_BM, TC_BN);
+      // One UMMA 128 x (MT*128) x 16 per k-step: A = the dequantized weight tile
+      // (128 rows = TMEM lanes), B = the MT activation tiles, contiguous in smem (one
+      // K-major SW128 operand of MT*128 rows) -> D[weight row][activation], half the
+      // MMA instructions of 128 x 128 tiles for the same flops.
+      constexpr uint32_t idesc = umma_idesc_bf16(TC_BN, UN);
       for (int i = 0; i < nks; i++) {
         const int s = i % STAGES;
         const uint32_t par = (i / STAGES) & 1;
@@ -402,16 +437,15 @@ __global__ void __launch_bounds__(TcVar<QT, BS, DEC>::THREADS, 1)
         mbar_wait(&b_full[s], par);
         tc_fence_after();
         const uint32_t st = smem_u32(smem + s * STAGE_BYTES);
-        const uint64_t bdesc0 = umma_desc_sw128(st + MT * TC_A_BYTES);
+        const uint64_t adesc0 = umma_desc_sw128(st + MT * TC_A_BYTES);
+        const uint64_t bdesc0 = umma_desc_sw128(st);
 #pragma unroll
-        for (int mt = 0; mt < MT; mt++) {
-          const uint64_t adesc0 = umma_desc_sw128(st + mt * TC_A_BYTES);
+        for (int kk = 0; kk < TC_BK / 16; kk++) {
+          // advance 16 elements = 32 bytes along K inside the 128-byte swizzle row
 #pragma unroll
-          for (int kk = 0; kk < TC_BK / 16; kk++) {
-            // advance 16 elements = 32 bytes along K inside the 128-byte swizzle row
-            umma_bf16(tmem + mt * TC_BN, adesc0 + (uint64_t)(kk * 2), bdesc0 + (uint64_t)(kk * 2), idesc,
-                      (i > 0) || (kk > 0));
-          }
+          for (int j = 0; j < MT * TC_BM / UN; j++)  // accumulator j: activations [j UN, (j + 1) UN)
+            umma_bf16(tmem + j * UN, adesc0 + (uint64_t)(kk * 2),
+                      bdesc0 + (uint64_t)((j * UN * 128) >> 4) + (uint64_t)(kk * 2), idesc, (i > 0) || (kk > 0));
         }
         umma_commit(&empty[s]);  // frees the stage once these MMAs completed
       }
@@ -438,8 +472,10 @@ __global__ void __launch_bounds__(TcVar<QT, BS, DEC>::THREADS, 1)
       cp_async_wait<TC_PD>();
       __syncwarp();  // the partner lane's half of the block is visible
       mbar_wait(&empty[s], ((i / STAGES) & 1) ^ 1);
+#ifndef IFB_TC_KO_DEQ  // knock-out experiment only: W' tiles left stale
       dequant_q3h64_half_f32<true>(myrow + (i % TC_PK) * TC_BN * SBPAD, n < N && (int64_t)(ks0 + i) * TC_BK < K, h,
                                    smem + s * STAGE_BYTES + MT * TC_A_BYTES, r);
+#endif
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> tensor core reads
       mbar_arrive(&b_full[s]);
       __syncwarp();  // both halves read before the ring slot is refilled
@@ -470,50 +506,75 @@ __global__ void __launch_bounds__(TcVar<QT, BS, DEC>::THREADS, 1)
   }
 
   // ---------------- epilogue: TMEM -> registers -> global ----------------
-  if (warp >= 2 && warp < 6) {
+  // TMEM lane = weight row n, column = activation m: a warp's 32 lanes store 32
+  // consecutive floats of one Y row per column (coalesced).  Warp w may read lane
+  // quarter w % 4; with 8 epilogue warps each quarter's columns are split in two.
+  constexpr int NEPI = Var::FAST ? 8 : 4;
+  if (warp >= 2 && warp < 2 + NEPI) {
     mbar_wait(acc_full, 0);
     tc_fence_after();
-    const int q = warp & 3;  // TMEM lane quarter this warp may access
+#ifdef IFB_TC_PROF
+    if (threadIdx.x == 64 && cta_id < 8192) g_tc_tl[cta_id][2] = gtimer();
+#endif
+    const int q = warp & 3;
+    const int half = (warp - 2) / 4;
+    constexpr int NCH = (TC_BM * MT / 32) / (NEPI / 4);  // 32-column chunks per warp
+    // 32 x 32 transpose through the (now idle) stage buffers, 36-float rows: lane
+    // writes its row's 32 values down a column, then 8 lanes x float4 cover one Y
+    // row segment of 32 weight rows -> 128-bit stores / reductions
+    float* sc = reinterpret_cast<float*>(smem) + (warp - 2) * 32 * 36;
+    const int64_t nq = n0 + q * 32;
+    const bool vec = (N % 4 == 0) && nq + 32 <= N && !(reinterpret_cast<uintptr_t>(Y) & 15u);
+#pragma unroll 1
+    for (int c = 0; c < NCH; c++) {
+      const int cc = half * NCH + c;
+      uint32_t rr[32];
+      tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + cc * 32, rr);
+      const int64_t mbase = m0 + cc * 32;
+      if (nks > 0 && nq < N && mbase < M) {
 #pragma unroll
-    for (int mt = 0; mt < MT; mt++) {
-      const int64_t m = m0 + mt * TC_BM + q * 32 + lane;
+        for (int j = 0; j < 32; j++) sc[j * 36 + lane] = __uint_as_float(rr[j]);
+        __syncwarp();
+        const int nl = (lane & 7) * 4;
 #pragma unroll
-      for (int cc = 0; cc < TC_BN / 32; cc++) {
-        uint32_t rr[32];
-        tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + mt * TC_BN + cc * 32, rr);
-        const int64_t nbase = n0 + cc * 32;
-        if (m < M && nks > 0) {
-          float* yrow = Y + m * N + nbase;
-          if (nbase + 32 <= N && (N % 4) == 0) {
-#pragma unroll
-            for (int j = 0; j < 32; j += 4) {
-              if (atomic_out) {
-                asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(yrow + j), "f"(__uint_as_float(rr[j])),
-                             "f"(__uint_as_float(rr[j + 1])), "f"(__uint_as_float(rr[j + 2])), "f"(__uint_as_float(rr[j + 3]))
+        for (int it = 0; it < 8; it++) {
+          const int ml = it * 4 + (lane >> 3);
+          const int64_t m = mbase + ml;
+          if (m < M) {
+            const float4 v = *reinterpret_cast<const float4*>(sc + ml * 36 + nl);
+            float* yp = Y + m * N + nq + nl;
+            if (vec) {
+              if (atomic_out)
+                asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(yp), "f"(v.x), "f"(v.y), "f"(v.z),
+                             "f"(v.w)
                              : "memory");
-              } else {
-                *reinterpret_cast<float4*>(yrow + j) = make_float4(__uint_as_float(rr[j]), __uint_as_float(rr[j + 1]),
-                                                                   __uint_as_float(rr[j + 2]), __uint_as_float(rr[j + 3]));
-              }
+              else
+                *reinterpret_cast<float4*>(yp) = v;
+            } else {
+              const float vv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+              for (int e = 0; e < 4; e++)
+                if (nq + nl + e < N) {
+                  if (atomic_out)
+                    atomicAdd(yp + e, vv[e]);
+                  else
+                    yp[e] = vv[e];
+                }
             }
-          } else {
-            for (int j = 0; j < 32; j++)
-              if (nbase + j < N) {
-                if (atomic_out)
-                  atomicAdd(yrow + j, __uint_as_float(rr[j]));
-                else
-                  yrow[j] = __uint_as_float(rr[j]);
-              }
           }
         }
+        __syncwarp();
       }
     }
     tc_fence_before();
   }
   __syncthreads();
+#ifdef IFB_TC_PROF
+  if (threadIdx.x == 0 && cta_id < 8192) g_tc_tl[cta_id][3] = gtimer();
+#endif
   if (warp == 1) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(Cfg::TMEM_COLS) : "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(TMEM_COLS) : "memory");
   }
 }
 
@@ -840,26 +901,37 @@ static if_status tc_run(if_scheme s, const CUtensorMap& map, const float* xdec, 
   const int64_t row_bytes = K / s.block * q_block_bytes(s.type, s.block);
   if ((row_bytes & 3) || (reinterpret_cast<uintptr_t>(W) & 3u)) return IF_ERR_UNSUPPORTED;
   const int ntile = (int)((N + TC_BN - 1) / TC_BN);
-  const int mtile = DEC ? 1 : (int)((M + TC_BM * TcCfg<DEC>::MT - 1) / (TC_BM * TcCfg<DEC>::MT));
   const int ktotal = (int)((K + TC_BK - 1) / TC_BK);
-  const int splits = tc_splits(ntile * mtile, ktotal);
-  const int kper = (ktotal + splits - 1) / splits;
-  const int atomic_out = (splits > 1) || accumulate;
-  if (splits > 1 && !accumulate) {
-    if (cudaMemsetAsync(Y, 0, sizeof(float) * M * N, st) != cudaSuccess) return check_launch("qgemm_tc memset");
-  }
   return dispatch_scheme(s, [&]<int QT, int BS>() -> if_status {
-    auto kern = qgemm_tc_kernel<QT, BS, DEC>;
-    constexpr int smem = tc_smem<DEC>(QT, BS);
-    static_assert(smem <= 227 * 1024, "shared memory");
-    static bool configured = false;
-    if (!configured) {
-      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-      configured = true;
+    auto go = [&]<bool WIDE>() -> if_status {
+      constexpr int MT = WIDE ? TC_MTW : TcCfg<DEC>::MT;
+      const int mtile = DEC ? 1 : (int)((M + TC_BM * MT - 1) / (TC_BM * MT));
+      const int splits = tc_splits(ntile * mtile, ktotal);
+      const int kper = (ktotal + splits - 1) / splits;
+      const int atomic_out = (splits > 1) || accumulate;
+      if (splits > 1 && !accumulate) {
+        if (cudaMemsetAsync(Y, 0, sizeof(float) * M * N, st) != cudaSuccess) return check_launch("qgemm_tc memset");
+      }
+      auto kern = qgemm_tc_kernel<QT, BS, DEC, WIDE>;
+      constexpr int smem = WIDE ? tc_smem_wide(QT, BS) : tc_smem<DEC>(QT, BS);
+      static_assert(smem <= 227 * 1024, "shared memory");
+      static bool configured = false;
+      if (!configured) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        configured = true;
+      }
+      dim3 grid(mtile, ntile, splits);
+      kern<<<grid, TcVar<QT, BS, DEC>::THREADS, smem, st>>>(map, xdec, W, N, K, M, Y, kper, atomic_out);
+      count_launch();
+      return IF_OK;
+    };
+    if_status r;
+    if constexpr (!DEC && TcVar<QT, BS, DEC>::FAST) {
+      r = M > TC_BM * TcCfg<DEC>::MT ? go.template operator()<true>() : go.template operator()<false>();
+    } else {
+      r = go.template operator()<false>();
     }
-    dim3 grid(mtile, ntile, splits);
-    kern<<<grid, TcVar<QT, BS, DEC>::THREADS, smem, st>>>(map, xdec, W, N, K, M, Y, kper, atomic_out);
-    count_launch();
+    if (r != IF_OK) return r;
     return check_launch(DEC ? "qgemv_tc" : "qgemm_tc");
   });
 }

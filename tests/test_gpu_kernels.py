@@ -206,8 +206,9 @@ def test_qgemm_all_schemes(qtype, bs):
 
 
 @pytest.mark.parametrize("M,N,K", [(1, 64, 64), (17, 200, 64 * 5), (128, 128, 4096), (512, 384, 64 * 20),
-                                   (300, 1000, 64 * 3)])
+                                   (300, 1000, 64 * 3), (257, 130, 64 * 7), (700, 260, 64 * 11), (1024, 256, 4096)])
 def test_qgemm_q3h_shapes(M, N, K):
+    """M > 256: the wide-tile variant (512 tokens per weight tile, two TMEM accumulators)."""
     d = dev()
     rng = np.random.default_rng(M + N + K)
     W = (rng.standard_normal((N, K)) / np.sqrt(K)).astype(np.float32)
