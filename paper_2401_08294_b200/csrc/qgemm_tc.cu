@@ -72,8 +72,11 @@ __host__ __device__ constexpr int tc_nxr(int B) {
 // tile is dequantized once per 512 tokens instead of once per 256
 constexpr int TC_MTW = 4;
 constexpr int TC_STAGES_W = 2;
+// raw-weight ring of the wide variant: 8 slots when the rows are <= 48 bytes per
+// stage, else 4 (prefetch distance 2) so that two 80 KB stages still fit
+__host__ __device__ constexpr int tc_pk_wide(int qt, int bs) { return tc_sbpad(qt, bs) <= 48 ? TC_PK : 4; }
 __host__ __device__ constexpr int tc_smem_wide(int qt, int bs) {
-  return TC_STAGES_W * (TC_MTW * TC_A_BYTES + TC_B_BYTES) + TC_PK * TC_BN * tc_sbpad(qt, bs) + 1024 + 512;
+  return TC_STAGES_W * (TC_MTW * TC_A_BYTES + TC_B_BYTES) + tc_pk_wide(qt, bs) * TC_BN * tc_sbpad(qt, bs) + 1024 + 512;
 }
 template <bool DEC>
 __host__ __device__ constexpr int tc_smem(int qt, int bs) {
@@ -359,11 +362,13 @@ __global__ void __launch_bounds__(TcVar<QT, BS, DEC>::THREADS, 1)
   constexpr int STAGE_BYTES = MT * TC_A_BYTES + TC_B_BYTES;
   constexpr int TMEM_COLS = MT * TC_BM;    // 256 or 512 fp32 columns
   constexpr int UN = MT * TC_BM > 256 ? 256 : MT * TC_BM;  // UMMA N (activations per MMA)
+  constexpr int PK = WIDE ? tc_pk_wide(QT, BS) : TC_PK;   // raw ring slots
+  constexpr int PD = PK - 2;                              // cp.async prefetch distance
   constexpr int SBPAD = tc_sbpad(QT, BS);
   extern __shared__ unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  unsigned char* pring = smem + STAGES * STAGE_BYTES;  // [TC_PK][TC_BN][SBPAD] raw weight bytes
-  uint64_t* a_full = reinterpret_cast<uint64_t*>(pring + TC_PK * TC_BN * SBPAD);
+  unsigned char* pring = smem + STAGES * STAGE_BYTES;  // [PK][TC_BN][SBPAD] raw weight bytes
+  uint64_t* a_full = reinterpret_cast<uint64_t*>(pring + PK * TC_BN * SBPAD);
   uint64_t* b_full = a_full + STAGES;
   uint64_t* empty = b_full + STAGES;
   uint64_t* acc_full = empty + STAGES;
@@ -458,22 +463,22 @@ __global__ void __launch_bounds__(TcVar<QT, BS, DEC>::THREADS, 1)
     unsigned char* myrow = pring + r * SBPAD;  // half h copies bytes [16h, 16h + 16) of the block
     auto pre = [&](int i) {
       const int64_t ks = ks0 + i;
-      if (n < N && ks * TC_BK < K) cp_async16(myrow + (i % TC_PK) * TC_BN * SBPAD + 16 * h, W + (n * nb + ks) * 32 + 16 * h);
+      if (n < N && ks * TC_BK < K) cp_async16(myrow + (i % PK) * TC_BN * SBPAD + 16 * h, W + (n * nb + ks) * 32 + 16 * h);
     };
 #pragma unroll
-    for (int i = 0; i < TC_PD; i++) {
+    for (int i = 0; i < PD; i++) {
       if (i < nks) pre(i);
       cp_async_commit();
     }
     for (int i = 0; i < nks; i++) {
       const int s = i % STAGES;
-      if (i + TC_PD < nks) pre(i + TC_PD);
+      if (i + PD < nks) pre(i + PD);
       cp_async_commit();
-      cp_async_wait<TC_PD>();
+      cp_async_wait<PD>();
       __syncwarp();  // the partner lane's half of the block is visible
       mbar_wait(&empty[s], ((i / STAGES) & 1) ^ 1);
 #ifndef IFB_TC_KO_DEQ  // knock-out experiment only: W' tiles left stale
-      dequant_q3h64_half_f32<true>(myrow + (i % TC_PK) * TC_BN * SBPAD, n < N && (int64_t)(ks0 + i) * TC_BK < K, h,
+      dequant_q3h64_half_f32<true>(myrow + (i % PK) * TC_BN * SBPAD, n < N && (int64_t)(ks0 + i) * TC_BK < K, h,
                                    smem + s * STAGE_BYTES + MT * TC_A_BYTES, r);
 #endif
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> tensor core reads
@@ -487,18 +492,18 @@ __global__ void __launch_bounds__(TcVar<QT, BS, DEC>::THREADS, 1)
     const int64_t n = n0 + r;
     unsigned char* myring = pring + r * SBPAD;
 #pragma unroll
-    for (int i = 0; i < TC_PD; i++) {
-      if (i < nks) prefetch_row<QT, BS>(W, nb, n, N, ks0 + i, K, myring + (i % TC_PK) * TC_BN * SBPAD);
+    for (int i = 0; i < PD; i++) {
+      if (i < nks) prefetch_row<QT, BS>(W, nb, n, N, ks0 + i, K, myring + (i % PK) * TC_BN * SBPAD);
       cp_async_commit();
     }
     for (int i = 0; i < nks; i++) {
       const int s = i % STAGES;
-      if (i + TC_PD < nks) prefetch_row<QT, BS>(W, nb, n, N, ks0 + i + TC_PD, K, myring + ((i + TC_PD) % TC_PK) * TC_BN * SBPAD);
+      if (i + PD < nks) prefetch_row<QT, BS>(W, nb, n, N, ks0 + i + PD, K, myring + ((i + PD) % PK) * TC_BN * SBPAD);
       cp_async_commit();
-      cp_async_wait<TC_PD>();  // stage i's bytes have landed (own copies only: no barrier needed)
+      cp_async_wait<PD>();  // stage i's bytes have landed (own copies only: no barrier needed)
       mbar_wait(&empty[s], ((i / STAGES) & 1) ^ 1);
       unsigned char* btile = smem + s * STAGE_BYTES + MT * TC_A_BYTES;
-      dequant_row<QT, BS, DEC>(myring + (i % TC_PK) * TC_BN * SBPAD, n, N, (int64_t)(ks0 + i) * TC_BK, K, btile, r);
+      dequant_row<QT, BS, DEC>(myring + (i % PK) * TC_BN * SBPAD, n, N, (int64_t)(ks0 + i) * TC_BK, K, btile, r);
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> tensor core reads
       mbar_arrive(&b_full[s]);
     }
@@ -926,7 +931,7 @@ static if_status tc_run(if_scheme s, const CUtensorMap& map, const float* xdec, 
       return IF_OK;
     };
     if_status r;
-    if constexpr (!DEC && TcVar<QT, BS, DEC>::FAST) {
+    if constexpr (!DEC) {
       r = M > TC_BM * TcCfg<DEC>::MT ? go.template operator()<true>() : go.template operator()<false>();
     } else {
       r = go.template operator()<false>();

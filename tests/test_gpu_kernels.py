@@ -191,10 +191,12 @@ def test_qgemv_one_hot_and_empty():
 
 # ---------------------------------------------------------------- qGEMM
 @pytest.mark.parametrize("qtype,bs", SCHEMES)
-def test_qgemm_all_schemes(qtype, bs):
+@pytest.mark.parametrize("M", [70, 300])
+def test_qgemm_all_schemes(qtype, bs, M):
+    """M = 300 > 256: the wide-tile variant (512 tokens per tile, ragged)."""
     d = dev()
-    rng = np.random.default_rng(qtype + bs)
-    N, K, M = 136, 64 * 9, 70
+    rng = np.random.default_rng(qtype + bs + M)
+    N, K = 136, 64 * 9
     W = (rng.standard_normal((N, K)) / np.sqrt(K)).astype(np.float32)
     p = O.quantize(qtype, bs, W)
     Xb, Xf = to_bf16_exact(rng.standard_normal((M, K)))
