@@ -78,6 +78,32 @@ __host__ __device__ constexpr int tc_pk_wide(int qt, int bs) { return tc_sbpad(q
 __host__ __device__ constexpr int tc_smem_wide(int qt, int bs) {
   return TC_STAGES_W * (TC_MTW * TC_A_BYTES + TC_B_BYTES) + tc_pk_wide(qt, bs) * TC_BN * tc_sbpad(qt, bs) + 1024 + 512;
 }
+// Prefill tile shapes (weight rows x tokens per CTA):
+//   TC_BASE 128 x 256, TC_WIDE 128 x 512 (M > 256), TC_TALL 256 x 256.
+// The in-CTA dequantization is the limiter (a knock-out run without it halves the
+// mainloop), so the more tokens share one dequantized tile the better: WIDE beats
+// BASE by 1.4-1.9x.  TALL halves the X bytes per flop (L2 -> SM traffic) but
+// dequantizes twice as much per flop: measured 10-25% slower than WIDE (DESIGN.md
+// §6), kept compiled-out (not dispatched).
+enum { TC_BASE = 0, TC_WIDE = 1, TC_TALL = 2 };
+template <int QT, int BS, int SHAPE>
+struct TcShape {
+  static constexpr bool FAST = QT == 35 && BS == 64;
+  static constexpr int MT = SHAPE == TC_WIDE ? 4 : 2;     // 128-token X tiles
+  static constexpr int RT = SHAPE == TC_TALL ? 2 : 1;     // 128-row weight tiles
+  static constexpr int ROWS = RT * TC_BN;
+  static constexpr int STAGES = SHAPE == TC_BASE ? TcCfg<false, tc_sbpad(QT, BS)>::STAGES : 2;
+  static constexpr int STAGE_BYTES = MT * TC_A_BYTES + RT * TC_B_BYTES;
+  static constexpr int UN = MT * TC_BM > 256 ? 256 : MT * TC_BM;  // UMMA N
+  static constexpr int NJ = MT * TC_BM / UN;                        // accumulators per row tile
+  static constexpr int TMEM_COLS = RT * MT * TC_BM;
+  static constexpr int PK = SHAPE == TC_BASE ? TC_PK : SHAPE == TC_WIDE ? tc_pk_wide(QT, BS) : 4;
+  static constexpr int PD = PK - 2;
+  static constexpr int NDEQ = FAST ? 2 * ROWS : ROWS;  // dequant threads
+  static constexpr int THREADS = 64 + (NDEQ > 192 ? NDEQ : 192);
+  static constexpr int NEPI = (NDEQ / 32) > 16 ? 16 : (NDEQ / 32);  // epilogue warps (multiple of 4)
+  static constexpr int SMEM = STAGES * STAGE_BYTES + PK * ROWS * tc_sbpad(QT, BS) + 1024 + 512;
+};
 template <bool DEC>
 __host__ __device__ constexpr int tc_smem(int qt, int bs) {
   return (tc_sbpad(qt, bs) <= 48 ? TcCfg<DEC, 48>::STAGES : TcCfg<DEC, 64>::STAGES) * TcCfg<DEC>::STAGE_BYTES +
@@ -351,24 +377,20 @@ __device__ __forceinline__ unsigned long long gtimer() {
 }
 extern "C" void ifx_tc_tl(void* host) { cudaMemcpyFromSymbol(host, g_tc_tl, sizeof(g_tc_tl)); }
 #endif
-template <int QT, int BS, bool DEC, bool WIDE = false>
-__global__ void __launch_bounds__(TcVar<QT, BS, DEC>::THREADS, 1)
+template <int QT, int BS, bool DEC, int SHAPE = TC_BASE>
+__global__ void __launch_bounds__(TcShape<QT, BS, SHAPE>::THREADS, 1)
     qgemm_tc_kernel(const __grid_constant__ CUtensorMap xmap, const float* __restrict__ xdec, const uint8_t* __restrict__ W,
                     int64_t N, int64_t K, int64_t M, float* __restrict__ Y, int ksteps_per_split, int atomic_out) {
-  using Cfg = TcCfg<DEC, tc_sbpad(QT, BS)>;
-  using Var = TcVar<QT, BS, DEC>;
-  constexpr int MT = WIDE ? TC_MTW : Cfg::MT;
-  constexpr int STAGES = WIDE ? TC_STAGES_W : Cfg::STAGES;
-  constexpr int STAGE_BYTES = MT * TC_A_BYTES + TC_B_BYTES;
-  constexpr int TMEM_COLS = MT * TC_BM;    // 256 or 512 fp32 columns
-  constexpr int UN = MT * TC_BM > 256 ? 256 : MT * TC_BM;  // UMMA N (activations per MMA)
-  constexpr int PK = WIDE ? tc_pk_wide(QT, BS) : TC_PK;   // raw ring slots
-  constexpr int PD = PK - 2;                              // cp.async prefetch distance
+  using Var = TcShape<QT, BS, SHAPE>;
+  constexpr int MT = Var::MT, RT = Var::RT, ROWS = Var::ROWS, NJ = Var::NJ, UN = Var::UN;
+  constexpr int STAGES = Var::STAGES, STAGE_BYTES = Var::STAGE_BYTES, TMEM_COLS = Var::TMEM_COLS;
+  constexpr int PK = Var::PK;  // raw ring slots
+  constexpr int PD = Var::PD;  // cp.async prefetch distance
   constexpr int SBPAD = tc_sbpad(QT, BS);
   extern __shared__ unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  unsigned char* pring = smem + STAGES * STAGE_BYTES;  // [PK][TC_BN][SBPAD] raw weight bytes
-  uint64_t* a_full = reinterpret_cast<uint64_t*>(pring + PK * TC_BN * SBPAD);
+  unsigned char* pring = smem + STAGES * STAGE_BYTES;  // [PK][ROWS][SBPAD] raw weight bytes
+  uint64_t* a_full = reinterpret_cast<uint64_t*>(pring + PK * ROWS * SBPAD);
   uint64_t* b_full = a_full + STAGES;
   uint64_t* empty = b_full + STAGES;
   uint64_t* acc_full = empty + STAGES;
@@ -386,7 +408,7 @@ __global__ void __launch_bounds__(TcVar<QT, BS, DEC>::THREADS, 1)
 #endif
   // grid (m tiles, n tiles, splits): the CTAs sharing a weight tile are adjacent in
   // launch order, so the second read of the tile hits L2 instead of HBM
-  const int64_t n0 = (int64_t)blockIdx.y * TC_BN;
+  const int64_t n0 = (int64_t)blockIdx.y * ROWS;
   const int64_t m0 = (int64_t)blockIdx.x * (TC_BM * MT);
   const int64_t nb = K / BS;
   const int ktotal = (int)((K + TC_BK - 1) / TC_BK);
@@ -430,10 +452,9 @@ __global__ void __launch_bounds__(TcVar<QT, BS, DEC>::THREADS, 1)
   } else if (warp == 1) {
     // ---------------- MMA issuer (one thread) ----------------
     if (lane == 0) {
-      // One UMMA 128 x (MT*128) x 16 per k-step: A = the dequantized weight tile
-      // (128 rows = TMEM lanes), B = the MT activation tiles, contiguous in smem (one
-      // K-major SW128 operand of MT*128 rows) -> D[weight row][activation], half the
-      // MMA instructions of 128 x 128 tiles for the same flops.
+      // UMMA 128 x UN x 16: A = a dequantized 128-row weight tile (rows = TMEM lanes),
+      // B = UN tokens of the MT X tiles (contiguous in smem: one K-major SW128 operand)
+      // -> D[weight row][token]; accumulator (rt, j) at TMEM columns (rt NJ + j) UN.
       constexpr uint32_t idesc = umma_idesc_bf16(TC_BN, UN);
       for (int i = 0; i < nks; i++) {
         const int s = i % STAGES;
@@ -448,22 +469,24 @@ __global__ void __launch_bounds__(TcVar<QT, BS, DEC>::THREADS, 1)
         for (int kk = 0; kk < TC_BK / 16; kk++) {
           // advance 16 elements = 32 bytes along K inside the 128-byte swizzle row
 #pragma unroll
-          for (int j = 0; j < MT * TC_BM / UN; j++)  // accumulator j: activations [j UN, (j + 1) UN)
-            umma_bf16(tmem + j * UN, adesc0 + (uint64_t)(kk * 2),
-                      bdesc0 + (uint64_t)((j * UN * 128) >> 4) + (uint64_t)(kk * 2), idesc, (i > 0) || (kk > 0));
+          for (int rt = 0; rt < RT; rt++)
+#pragma unroll
+            for (int j = 0; j < NJ; j++)
+              umma_bf16(tmem + (rt * NJ + j) * UN, adesc0 + (uint64_t)((rt * TC_B_BYTES) >> 4) + (uint64_t)(kk * 2),
+                        bdesc0 + (uint64_t)((j * UN * 128) >> 4) + (uint64_t)(kk * 2), idesc, (i > 0) || (kk > 0));
         }
         umma_commit(&empty[s]);  // frees the stage once these MMAs completed
       }
       umma_commit(acc_full);
     }
-  } else if (Var::FAST && warp < 10) {
-    // ---------------- Q3H_B64 dequantizers: two threads per row (warps 2-9) ----------------
+  } else if (Var::FAST && warp < 2 + Var::NDEQ / 32) {
+    // ---------------- Q3H_B64 dequantizers: two threads per row (warps 2-9 / 2-17) ----------------
     const int r = (warp - 2) * 16 + (lane >> 1), h = lane & 1;
     const int64_t n = n0 + r;
     unsigned char* myrow = pring + r * SBPAD;  // half h copies bytes [16h, 16h + 16) of the block
     auto pre = [&](int i) {
       const int64_t ks = ks0 + i;
-      if (n < N && ks * TC_BK < K) cp_async16(myrow + (i % PK) * TC_BN * SBPAD + 16 * h, W + (n * nb + ks) * 32 + 16 * h);
+      if (n < N && ks * TC_BK < K) cp_async16(myrow + (i % PK) * ROWS * SBPAD + 16 * h, W + (n * nb + ks) * 32 + 16 * h);
     };
 #pragma unroll
     for (int i = 0; i < PD; i++) {
@@ -478,7 +501,7 @@ __global__ void __launch_bounds__(TcVar<QT, BS, DEC>::THREADS, 1)
       __syncwarp();  // the partner lane's half of the block is visible
       mbar_wait(&empty[s], ((i / STAGES) & 1) ^ 1);
 #ifndef IFB_TC_KO_DEQ  // knock-out experiment only: W' tiles left stale
-      dequant_q3h64_half_f32<true>(myrow + (i % PK) * TC_BN * SBPAD, n < N && (int64_t)(ks0 + i) * TC_BK < K, h,
+      dequant_q3h64_half_f32<true>(myrow + (i % PK) * ROWS * SBPAD, n < N && (int64_t)(ks0 + i) * TC_BK < K, h,
                                    smem + s * STAGE_BYTES + MT * TC_A_BYTES, r);
 #endif
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> tensor core reads
@@ -486,24 +509,24 @@ __global__ void __launch_bounds__(TcVar<QT, BS, DEC>::THREADS, 1)
       __syncwarp();  // both halves read before the ring slot is refilled
     }
     cp_async_wait<0>();
-  } else if (!Var::FAST && warp < 6) {
+  } else if (!Var::FAST && warp < 2 + Var::NDEQ / 32) {
     // ---------------- dequantizers: one weight row per thread ----------------
     const int r = threadIdx.x - 64;  // 0..127
     const int64_t n = n0 + r;
     unsigned char* myring = pring + r * SBPAD;
 #pragma unroll
     for (int i = 0; i < PD; i++) {
-      if (i < nks) prefetch_row<QT, BS>(W, nb, n, N, ks0 + i, K, myring + (i % PK) * TC_BN * SBPAD);
+      if (i < nks) prefetch_row<QT, BS>(W, nb, n, N, ks0 + i, K, myring + (i % PK) * ROWS * SBPAD);
       cp_async_commit();
     }
     for (int i = 0; i < nks; i++) {
       const int s = i % STAGES;
-      if (i + PD < nks) prefetch_row<QT, BS>(W, nb, n, N, ks0 + i + PD, K, myring + ((i + PD) % PK) * TC_BN * SBPAD);
+      if (i + PD < nks) prefetch_row<QT, BS>(W, nb, n, N, ks0 + i + PD, K, myring + ((i + PD) % PK) * ROWS * SBPAD);
       cp_async_commit();
       cp_async_wait<PD>();  // stage i's bytes have landed (own copies only: no barrier needed)
       mbar_wait(&empty[s], ((i / STAGES) & 1) ^ 1);
       unsigned char* btile = smem + s * STAGE_BYTES + MT * TC_A_BYTES;
-      dequant_row<QT, BS, DEC>(myring + (i % PK) * TC_BN * SBPAD, n, N, (int64_t)(ks0 + i) * TC_BK, K, btile, r);
+      dequant_row<QT, BS, DEC>(myring + (i % PK) * ROWS * SBPAD, n, N, (int64_t)(ks0 + i) * TC_BK, K, btile, r);
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> tensor core reads
       mbar_arrive(&b_full[s]);
     }
@@ -511,10 +534,9 @@ __global__ void __launch_bounds__(TcVar<QT, BS, DEC>::THREADS, 1)
   }
 
   // ---------------- epilogue: TMEM -> registers -> global ----------------
-  // TMEM lane = weight row n, column = activation m: a warp's 32 lanes store 32
-  // consecutive floats of one Y row per column (coalesced).  Warp w may read lane
-  // quarter w % 4; with 8 epilogue warps each quarter's columns are split in two.
-  constexpr int NEPI = Var::FAST ? 8 : 4;
+  // TMEM lane = weight row, column = token.  Warp w may read lane quarter w % 4;
+  // the NEPI / 4 warps of a quarter split its 32-column chunks.
+  constexpr int NEPI = Var::NEPI;
   if (warp >= 2 && warp < 2 + NEPI) {
     mbar_wait(acc_full, 0);
     tc_fence_after();
@@ -523,19 +545,17 @@ __global__ void __launch_bounds__(TcVar<QT, BS, DEC>::THREADS, 1)
 #endif
     const int q = warp & 3;
     const int half = (warp - 2) / 4;
-    constexpr int NCH = (TC_BM * MT / 32) / (NEPI / 4);  // 32-column chunks per warp
-    // 32 x 32 transpose through the (now idle) stage buffers, 36-float rows: lane
-    // writes its row's 32 values down a column, then 8 lanes x float4 cover one Y
-    // row segment of 32 weight rows -> 128-bit stores / reductions
+    constexpr int NCH = (TMEM_COLS / 32) / (NEPI / 4);  // 32-column chunks per warp
     float* sc = reinterpret_cast<float*>(smem) + (warp - 2) * 32 * 36;
-    const int64_t nq = n0 + q * 32;
-    const bool vec = (N % 4 == 0) && nq + 32 <= N && !(reinterpret_cast<uintptr_t>(Y) & 15u);
 #pragma unroll 1
     for (int c = 0; c < NCH; c++) {
       const int cc = half * NCH + c;
       uint32_t rr[32];
       tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + cc * 32, rr);
-      const int64_t mbase = m0 + cc * 32;
+      const int acc = (cc * 32) / UN, rt = acc / NJ;  // accumulator (rt, j)
+      const int64_t mbase = m0 + (acc % NJ) * UN + (cc * 32) % UN;
+      const int64_t nq = n0 + rt * TC_BN + q * 32;
+      const bool vec = (N % 4 == 0) && nq + 32 <= N && !(reinterpret_cast<uintptr_t>(Y) & 15u);
       if (nks > 0 && nq < N && mbase < M) {
 #pragma unroll
         for (int j = 0; j < 32; j++) sc[j * 36 + lane] = __uint_as_float(rr[j]);
@@ -905,20 +925,20 @@ static if_status tc_run(if_scheme s, const CUtensorMap& map, const float* xdec, 
   // number of blocks per row is 2-byte aligned: SIMT path)
   const int64_t row_bytes = K / s.block * q_block_bytes(s.type, s.block);
   if ((row_bytes & 3) || (reinterpret_cast<uintptr_t>(W) & 3u)) return IF_ERR_UNSUPPORTED;
-  const int ntile = (int)((N + TC_BN - 1) / TC_BN);
   const int ktotal = (int)((K + TC_BK - 1) / TC_BK);
   return dispatch_scheme(s, [&]<int QT, int BS>() -> if_status {
-    auto go = [&]<bool WIDE>() -> if_status {
-      constexpr int MT = WIDE ? TC_MTW : TcCfg<DEC>::MT;
-      const int mtile = DEC ? 1 : (int)((M + TC_BM * MT - 1) / (TC_BM * MT));
+    auto go = [&]<int SHAPE>() -> if_status {
+      using V = TcShape<QT, BS, SHAPE>;
+      const int ntile = (int)((N + V::ROWS - 1) / V::ROWS);
+      const int mtile = (int)((M + TC_BM * V::MT - 1) / (TC_BM * V::MT));
       const int splits = tc_splits(ntile * mtile, ktotal);
       const int kper = (ktotal + splits - 1) / splits;
       const int atomic_out = (splits > 1) || accumulate;
       if (splits > 1 && !accumulate) {
         if (cudaMemsetAsync(Y, 0, sizeof(float) * M * N, st) != cudaSuccess) return check_launch("qgemm_tc memset");
       }
-      auto kern = qgemm_tc_kernel<QT, BS, DEC, WIDE>;
-      constexpr int smem = WIDE ? tc_smem_wide(QT, BS) : tc_smem<DEC>(QT, BS);
+      auto kern = qgemm_tc_kernel<QT, BS, DEC, SHAPE>;
+      constexpr int smem = V::SMEM;
       static_assert(smem <= 227 * 1024, "shared memory");
       static bool configured = false;
       if (!configured) {
@@ -926,16 +946,12 @@ static if_status tc_run(if_scheme s, const CUtensorMap& map, const float* xdec, 
         configured = true;
       }
       dim3 grid(mtile, ntile, splits);
-      kern<<<grid, TcVar<QT, BS, DEC>::THREADS, smem, st>>>(map, xdec, W, N, K, M, Y, kper, atomic_out);
+      kern<<<grid, V::THREADS, smem, st>>>(map, xdec, W, N, K, M, Y, kper, atomic_out);
       count_launch();
       return IF_OK;
     };
-    if_status r;
-    if constexpr (!DEC) {
-      r = M > TC_BM * TcCfg<DEC>::MT ? go.template operator()<true>() : go.template operator()<false>();
-    } else {
-      r = go.template operator()<false>();
-    }
+    // M > 256: 512-token tiles (each weight dequantized once per 512 tokens)
+    if_status r = M > 256 ? go.template operator()<TC_WIDE>() : go.template operator()<TC_BASE>();
     if (r != IF_OK) return r;
     return check_launch(DEC ? "qgemv_tc" : "qgemm_tc");
   });
