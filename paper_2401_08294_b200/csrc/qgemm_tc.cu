@@ -99,7 +99,7 @@ struct TcShape {
   static constexpr int TMEM_COLS = RT * MT * TC_BM;
   static constexpr int PK = SHAPE == TC_BASE ? TC_PK : SHAPE == TC_WIDE ? tc_pk_wide(QT, BS) : 4;
   static constexpr int PD = PK - 2;
-  static constexpr int NDEQ = FAST ? 2 * ROWS : ROWS;  // dequant threads
+  static constexpr int NDEQ = 2 * ROWS;  // dequant threads: two per weight row
   static constexpr int THREADS = 64 + (NDEQ > 192 ? NDEQ : 192);
   static constexpr int NEPI = (NDEQ / 32) > 16 ? 16 : (NDEQ / 32);  // epilogue warps (multiple of 4)
   static constexpr int SMEM = STAGES * STAGE_BYTES + PK * ROWS * tc_sbpad(QT, BS) + 1024 + 512;
@@ -211,11 +211,30 @@ __device__ __forceinline__ void prefetch_row(const uint8_t* __restrict__ W, int6
     for (int i = 0; i < SB / 4; i++) cp_async4(dst + 4 * i, src + 4 * i);
   }
 }
+// the same copy shared by two threads: part g (0/1) issues every other unit
+template <int QT, int BS>
+__device__ __forceinline__ void prefetch_row_part(const uint8_t* __restrict__ W, int64_t nb, int64_t n, int64_t N,
+                                                  int64_t ks, int64_t K, unsigned char* dst, int g) {
+  constexpr int SB = tc_sb(QT, BS);
+  if (n >= N || ks * TC_BK >= K) return;
+  const uint8_t* src = W + (n * nb + ks * (TC_BK / BS)) * q_block_bytes(QT, BS);
+  if (SB % 16 == 0 && (reinterpret_cast<uintptr_t>(src) & 15u) == 0) {
+#pragma unroll
+    for (int i = 0; i < SB / 16; i++)
+      if ((i & 1) == g) cp_async16(dst + 16 * i, src + 16 * i);
+  } else {
+#pragma unroll
+    for (int i = 0; i < SB / 4; i++)
+      if ((i & 1) == g) cp_async4(dst + 4 * i, src + 4 * i);
+  }
+}
 
 // Dequantize weight row n, weights [k0, k0 + 64), from its raw bytes in the ring
 // into 128 bytes of 16-bit values in the SW128 K-major layout at row r of the
 // B tile (zeros beyond N or K).
-template <int QT, int BS, bool F16>
+// HALF = 0 / 1: only weights [32 HALF, 32 HALF + 32) of the stage (chunks 4 HALF ..
+// 4 HALF + 3 of the row); -1: all 64.
+template <int QT, int BS, bool F16, int HALF = -1>
 __device__ __forceinline__ void dequant_row(const unsigned char* raw, int64_t n, int64_t N, int64_t k0, int64_t K,
                                            unsigned char* btile, int r) {
   constexpr int D = q_levels(QT);
@@ -234,8 +253,10 @@ __device__ __forceinline__ void dequant_row(const unsigned char* raw, int64_t n,
       words[4 * i] = v.x, words[4 * i + 1] = v.y, words[4 * i + 2] = v.z, words[4 * i + 3] = v.w;
     }
     words[SBW] = 0u;
+    constexpr int SUB0 = (HALF >= 0 && BS == 32) ? HALF : 0;
+    constexpr int SUB1 = (HALF >= 0 && BS == 32) ? HALF + 1 : TC_BK / BS;
 #pragma unroll
-    for (int sub = 0; sub < TC_BK / BS; sub++) {
+    for (int sub = SUB0; sub < SUB1; sub++) {
       // block sub starts at byte sub * BB (a multiple of 2): word-aligned or a halfword in
       const int boff = sub * BB;
       if (k0 + sub * BS >= K) {
@@ -256,19 +277,18 @@ __device__ __forceinline__ void dequant_row(const unsigned char* raw, int64_t n,
       const float lo = half_bits_to_float(w[0] & 0xFFFFu);
       const float hi = half_bits_to_float(w[0] >> 16);
       const float step = __fdiv_rn(__fsub_rn(hi, lo), (float)D);
+      constexpr int J0 = (HALF >= 0 && BS == 64) ? HALF * NC / 2 : 0;
+      constexpr int J1 = (HALF >= 0 && BS == 64) ? (HALF + 1) * NC / 2 : NC;
 #pragma unroll
-      for (int j = 0; j < NC; j++) {
+      for (int j = J0; j < J1; j++) {
         const uint32_t v = get_code<C, NW>(w, j);
         if constexpr (QT == 35) {
           const uint32_t q1 = (v * 187u) >> 11;  // floor(v/11) for v < 128
           const uint32_t q2 = v - 11u * q1;      // v mod 11
           out[sub * (BS / 2) + j] = pack16x2<F16>(__fmaf_rn(u2f_exact(q1), step, lo), __fmaf_rn(u2f_exact(q2), step, lo));
-        } else {
-          const float wp = __fmaf_rn(u2f_exact(v), step, lo);
-          if (j & 1)
-            out[sub * (BS / 2) + j / 2] |= pack16x2<F16>(0.f, wp) & 0xFFFF0000u;
-          else
-            out[sub * (BS / 2) + j / 2] = pack16x2<F16>(wp, 0.f) & 0x0000FFFFu;
+        } else if (j & 1) {  // pairs of consecutive weights -> one packed word
+          const float w0 = __fmaf_rn(u2f_exact(get_code<C, NW>(w, j - 1)), step, lo);
+          out[sub * (BS / 2) + j / 2] = pack16x2<F16>(w0, __fmaf_rn(u2f_exact(v), step, lo));
         }
       }
     }
@@ -279,7 +299,7 @@ __device__ __forceinline__ void dequant_row(const unsigned char* raw, int64_t n,
   // 8 chunks of 16 B; chunk c of row r lives at chunk (c ^ (r % 8)) of the row (SW128)
   unsigned char* rowp = btile + (r >> 3) * 1024 + (r & 7) * 128;
 #pragma unroll
-  for (int c = 0; c < 8; c++) {
+  for (int c = (HALF >= 0 ? 4 * HALF : 0); c < (HALF >= 0 ? 4 * HALF + 4 : 8); c++) {
     uint4 v = make_uint4(out[4 * c], out[4 * c + 1], out[4 * c + 2], out[4 * c + 3]);
     *reinterpret_cast<uint4*>(rowp + ((c ^ (r & 7)) << 4)) = v;
   }
@@ -510,23 +530,39 @@ __global__ void __launch_bounds__(TcShape<QT, BS, SHAPE>::THREADS, 1)
     }
     cp_async_wait<0>();
   } else if (!Var::FAST && warp < 2 + Var::NDEQ / 32) {
-    // ---------------- dequantizers: one weight row per thread ----------------
-    const int r = threadIdx.x - 64;  // 0..127
+    // ---------------- dequantizers: two threads per weight row ----------------
+    // warps 2..(2 + ROWS/32) take weights [0, 32) of the stage, the next ROWS/32 warps
+    // [32, 64) of the same rows (warp-uniform halves: no divergence).  The pair shares
+    // the row's ring slot, each copying every other unit; a 64-thread named barrier
+    // per stage makes both halves of the copy visible to both warps.
+    constexpr int RW = ROWS / 32;                  // warps per half
+    const int g = (warp - 2) / RW;                 // half
+    const int r = ((warp - 2) % RW) * 32 + lane;  // row
+    const int bar_id = 1 + (warp - 2) % RW;       // named barrier of the warp pair
     const int64_t n = n0 + r;
     unsigned char* myring = pring + r * SBPAD;
 #pragma unroll
     for (int i = 0; i < PD; i++) {
-      if (i < nks) prefetch_row<QT, BS>(W, nb, n, N, ks0 + i, K, myring + (i % PK) * ROWS * SBPAD);
+      if (i < nks) prefetch_row_part<QT, BS>(W, nb, n, N, ks0 + i, K, myring + (i % PK) * ROWS * SBPAD, g);
       cp_async_commit();
     }
     for (int i = 0; i < nks; i++) {
       const int s = i % STAGES;
-      if (i + PD < nks) prefetch_row<QT, BS>(W, nb, n, N, ks0 + i + PD, K, myring + ((i + PD) % PK) * ROWS * SBPAD);
+      // slot (i + PD) % PK was last read at stage i + PD - PK <= i - 2: both warps have
+      // passed stage i - 1's barrier since
+      if (i + PD < nks)
+        prefetch_row_part<QT, BS>(W, nb, n, N, ks0 + i + PD, K, myring + ((i + PD) % PK) * ROWS * SBPAD, g);
       cp_async_commit();
-      cp_async_wait<PD>();  // stage i's bytes have landed (own copies only: no barrier needed)
+      cp_async_wait<PD>();
+      asm volatile("bar.sync %0, 64;" ::"r"(bar_id) : "memory");  // the partner's copies landed too
       mbar_wait(&empty[s], ((i / STAGES) & 1) ^ 1);
       unsigned char* btile = smem + s * STAGE_BYTES + MT * TC_A_BYTES;
-      dequant_row<QT, BS, DEC>(myring + (i % PK) * ROWS * SBPAD, n, N, (int64_t)(ks0 + i) * TC_BK, K, btile, r);
+      const unsigned char* raw = myring + (i % PK) * ROWS * SBPAD;
+      const int64_t k0 = (int64_t)(ks0 + i) * TC_BK;
+      if (g == 0)
+        dequant_row<QT, BS, DEC, 0>(raw, n, N, k0, K, btile, r);
+      else
+        dequant_row<QT, BS, DEC, 1>(raw, n, N, k0, K, btile, r);
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> tensor core reads
       mbar_arrive(&b_full[s]);
     }
