@@ -439,7 +439,7 @@ __global__ void __launch_bounds__(TcShape<QT, BS, SHAPE>::THREADS, 1)
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; s++) {
       mbar_init(&a_full[s], 1);
-      mbar_init(&b_full[s], Var::NDEQ);
+      mbar_init(&b_full[s], Var::NDEQ / 32);  // one arrival per dequant warp
       mbar_init(&empty[s], 1);
     }
     mbar_init(acc_full, 1);
@@ -525,7 +525,8 @@ __global__ void __launch_bounds__(TcShape<QT, BS, SHAPE>::THREADS, 1)
                                    smem + s * STAGE_BYTES + MT * TC_A_BYTES, r);
 #endif
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> tensor core reads
-      mbar_arrive(&b_full[s]);
+      __syncwarp();  // the warp's W' rows (each lane fenced its own stores) ...
+      if (lane == 0) mbar_arrive(&b_full[s]);  // ... one arrival per warp
       __syncwarp();  // both halves read before the ring slot is refilled
     }
     cp_async_wait<0>();
@@ -564,7 +565,8 @@ __global__ void __launch_bounds__(TcShape<QT, BS, SHAPE>::THREADS, 1)
       else
         dequant_row<QT, BS, DEC, 1>(raw, n, N, k0, K, btile, r);
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> tensor core reads
-      mbar_arrive(&b_full[s]);
+      __syncwarp();  // the warp's W' rows (each lane fenced its own stores) ...
+      if (lane == 0) mbar_arrive(&b_full[s]);  // ... one arrival per warp
     }
     cp_async_wait<0>();
   }
@@ -709,6 +711,12 @@ __device__ __forceinline__ void qgemv_epilogue(uint32_t tmem, uint64_t* acc_full
   tc_fence_before();
 }
 
+#ifdef IFB_TCD_PROF
+// instrumentation build only: per CTA clock64 sums {MMA: wait x, wait W', issue, total;
+// dequant warp 2 lane 0: wait weight slot, wait free stage, dequant, total}
+__device__ unsigned long long g_tcd_prof[4096][8];
+extern "C" void ifx_tcd_prof(void* host) { cudaMemcpyFromSymbol(host, g_tcd_prof, sizeof(g_tcd_prof)); }
+#endif
 // the 8-warp Q3H_B64 dequant loop: warp w in 2..9 owns rows [16 (w - 2), +16), lane
 // pair (2i, 2i + 1) = the two halves of row 16 (w - 2) + i; the weight tile of stage
 // i ([128 rows x 32 B], TMA) is in ring slot i % TCD_WR
@@ -720,16 +728,37 @@ __device__ __forceinline__ void qgemv_fast_deq(int64_t N, int64_t K, int64_t n0,
   const int64_t n = n0 + r;
   int s = 0;
   uint32_t sph = 0;  // stage slot and its phase (incremental: stages need not be a power of two)
+#ifdef IFB_TCD_PROF
+  unsigned long long p0 = 0, p1 = 0, p2 = 0, tstart = clock64();
+#endif
   for (int i = 0; i < nks; i++, s = (s + 1 == stages) ? (sph ^= 1, 0) : s + 1) {
     const int ws = i & (TCD_WR - 1);
+#ifdef IFB_TCD_PROF
+    unsigned long long ta = clock64();
+#endif
     mbar_wait(&wfull[ws], (i / TCD_WR) & 1);
+#ifdef IFB_TCD_PROF
+    unsigned long long tb = clock64();
+#endif
     mbar_wait(&empty[s], sph ^ 1);
+#ifdef IFB_TCD_PROF
+    unsigned long long tc = clock64();
+#endif
 #ifndef IFB_TCD_NODEQ
     dequant_q3h64_half_f32<false>(wring + ws * 4096 + r * 32, n < N && (int64_t)(ks0 + i) * TC_BK < K, h,
                                   smem + s * stage_bytes, r);
 #endif
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> tensor core reads
-    mbar_arrive(&b_full[s]);
+    __syncwarp();  // the warp's W' rows (each lane fenced its own stores) ...
+    if (lane == 0) mbar_arrive(&b_full[s]);  // ... one arrival per warp
+#ifdef IFB_TCD_PROF
+    unsigned long long td = clock64();
+    p0 += tb - ta, p1 += tc - tb, p2 += td - tc;
+    if (warp == 2 && lane == 0 && i == nks - 1 && blockIdx.x < 4096) {
+      g_tcd_prof[blockIdx.x][4] = p0, g_tcd_prof[blockIdx.x][5] = p1, g_tcd_prof[blockIdx.x][6] = p2;
+      g_tcd_prof[blockIdx.x][7] = td - tstart;
+    }
+#endif
     __syncwarp();  // both halves of every row of this warp read the ring slot
     if (lane == 0) mbar_arrive(&wempty[ws]);
   }
@@ -780,7 +809,7 @@ __global__ void __launch_bounds__(TcdVar<QT, BS>::THREADS, 1)
   if (threadIdx.x == 0) {
     for (int s = 0; s < stages; s++) {
       mbar_init(&a_full[s], xpre ? 1 : TC_CONV);
-      mbar_init(&b_full[s], V::NDEQ);
+      mbar_init(&b_full[s], V::NDEQ / 32);  // one arrival per dequant warp
       mbar_init(&empty[s], 1);
     }
     mbar_init(acc_full, 1);
@@ -853,11 +882,31 @@ __global__ void __launch_bounds__(TcdVar<QT, BS>::THREADS, 1)
     // ---------------- MMA issuer (one thread): A = W' (M = 128), B = x (N = ncols) ----------------
     if (lane == 0) {
       const uint32_t idesc = umma_idesc_f16(TC_BN, ncols);
+#ifdef IFB_TCD_PROF
+      unsigned long long q0 = 0, q1 = 0, q2 = 0, tstart = clock64(), tprev = 0;
+#endif
       for (int i = 0; i < nks; i++) {
         const int s = i % stages;
         const uint32_t par = (i / stages) & 1;
+#ifdef IFB_TCD_PROF
+        unsigned long long ta = clock64();
+        if (i > 0) q2 += ta - tprev;
+#endif
         mbar_wait(&a_full[s], par);
+#ifdef IFB_TCD_PROF
+        unsigned long long tb = clock64();
+        q0 += tb - ta;
+#endif
         mbar_wait(&b_full[s], par);
+#ifdef IFB_TCD_PROF
+        unsigned long long tc = clock64();
+        q1 += tc - tb;
+        tprev = tc;
+        if (i == nks - 1 && blockIdx.x < 4096) {
+          g_tcd_prof[blockIdx.x][0] = q0, g_tcd_prof[blockIdx.x][1] = q1, g_tcd_prof[blockIdx.x][2] = q2;
+          g_tcd_prof[blockIdx.x][3] = tc - tstart;
+        }
+#endif
         tc_fence_after();
         const uint32_t st = smem_u32(smem + s * stage_bytes);
         const uint64_t adesc0 = umma_desc_sw128(st), bdesc0 = umma_desc_sw128(st + TC_B_BYTES);
@@ -897,7 +946,8 @@ __global__ void __launch_bounds__(TcdVar<QT, BS>::THREADS, 1)
       dequant_row<QT, BS, true>(myring + (i % TC_PK) * TC_BN * SBPAD, n, N, (int64_t)(ks0 + i) * TC_BK, K,
                                 smem + s * stage_bytes, r);
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> tensor core reads
-      mbar_arrive(&b_full[s]);
+      __syncwarp();  // the warp's W' rows (each lane fenced its own stores) ...
+      if (lane == 0) mbar_arrive(&b_full[s]);  // ... one arrival per warp
     }
     cp_async_wait<0>();
     qgemv_epilogue(tmem, acc_full, Y, N, B, bp, n0, nks, atomic_out, warp, lane);
