@@ -98,8 +98,26 @@ def dist_env():
 
 
 # ---------------------------------------------------------------------------
-# reference arm: the CPU oracle, as it stands
+# reference arm / cpu_baseline: the CPU oracle, as it stands
 # ---------------------------------------------------------------------------
+def host_cores() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
 def _oracle_layer(model: str):
     """Layer 0 of the stack, quantized by the oracle from the host generator."""
     import numpy as np
@@ -115,63 +133,133 @@ def _oracle_layer(model: str):
     wo = O.quantize(35, 64, synth.weight(l, "o", d, H * hd, d))
     wgu = O.quantize(35, 64, np.concatenate([synth.weight(l, "gate", Fd, d, d), synth.weight(l, "up", Fd, d, d)]))
     wd = O.quantize(35, 64, synth.weight(l, "down", d, Fd, d))
-    return cfg, ([wqkv], [wo], [wgu], [wd])
+    return cfg, (wqkv, wo, wgu, wd)
+
+
+class OracleStep:
+    """One FULL decode step of the stack (all L layers, Q18) timed on the host's CPU
+    cores.  Bounded set-up: layer 0's packed weights serve every layer (the oracle's
+    time does not depend on the weight values).
+      threads == 1: O.stack_f64 itself -- the oracle as it stands;
+      threads  > 1: the same step with each of the oracle's matmuls (ref_matmul_f64)
+                    split into row ranges run on `threads` C threads (ctypes drops the
+                    GIL), the fp64 glue in numpy.  tests/test_bench_cpu.py checks it
+                    against O.stack_f64."""
+
+    def __init__(self, model: str, batch: int):
+        import synth
+        self.cfg, self.W = _oracle_layer(model)
+        self.h = synth.activations(batch, self.cfg["hidden"])
+        self.batch = batch
+
+    def run(self, threads: int, layers=None):
+        if threads <= 1:
+            return self._single(layers)
+        return stack_rows_threaded(self.cfg, self.W, self.h, threads, layers)
+
+    def _single(self, layers=None):
+        import oracle as O
+        L = self.cfg["layers"] if layers is None else layers
+        shape = dict(self.cfg, qtype=35, block=64)
+        return O.stack_f64(shape, [self.W[0]] * L, [self.W[1]] * L, [self.W[2]] * L, [self.W[3]] * L, self.h)[0]
+
+
+def stack_rows_threaded(cfg, W, h, threads: int, layers=None):
+    """The oracle stack step with row-split matmuls on `threads` threads (see OracleStep)."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    import numpy as np
+
+    import oracle as O
+    d, H, G, hd, Fd = cfg["hidden"], cfg["heads"], cfg["kv_heads"], cfg["head_dim"], cfg["ffn"]
+    L = cfg["layers"] if layers is None else layers
+    nq, nkv = H * hd, G * hd
+    wqkv, wo, wgu, wd = W
+
+    def mm(packed, N, K, X):
+        rb = O.packed_bytes(35, 64, 1, K)
+        cuts = [N * i // threads for i in range(threads + 1)]
+        parts = [(cuts[i], cuts[i + 1]) for i in range(threads) if cuts[i + 1] > cuts[i]]
+        Xf = np.ascontiguousarray(X, np.float32)
+        outs = list(pool.map(lambda rg: O.matmul_f64(35, 64, packed[rg[0] * rb:rg[1] * rb], rg[1] - rg[0], K, Xf),
+                             parts))
+        return np.concatenate(outs, axis=1)
+
+    def rms(x):
+        return x / np.sqrt((x * x).mean(axis=1, keepdims=True) + 1e-5)
+
+    hh = np.asarray(h, np.float64).copy()
+    with ThreadPoolExecutor(threads) as pool:
+        for _ in range(L):
+            qkv = mm(wqkv, nq + 2 * nkv, d, rms(hh))
+            v = qkv[:, nq + nkv:]
+            ctx = np.concatenate([v[:, (i // (H // G)) * hd:(i // (H // G) + 1) * hd] for i in range(H)], axis=1)
+            hh = hh + mm(wo, d, nq, ctx)
+            gu = mm(wgu, 2 * Fd, d, rms(hh))
+            g, u = gu[:, :Fd], gu[:, Fd:]
+            hh = hh + mm(wd, d, Fd, g / (1.0 + np.exp(-g)) * u)
+    return hh
 
 
 def run_reference(args):
     ws, rank, _ = dist_env()
     if rank != 0:
         return
-    import oracle as O
-    import synth
-
-    cfg, W = _oracle_layer(args.model)
-    L = cfg["layers"]
-    h = synth.activations(args.batch, cfg["hidden"])
-    shape1 = dict(cfg, layers=1, qtype=35, block=64)
+    cores = host_cores()
+    if args.model is None:  # the same workload as our arm
+        args.model = "7b" if ws == 1 else "70b"
+    step = OracleStep(args.model, args.batch)
+    L = step.cfg["layers"]
+    # a step is one full decode step (7B/13B); the 70B step (68 G MACs) is bounded to
+    # 8 of its 80 layers and the tokens/s extrapolated (ms_per_step stays measured)
+    nl = L if args.model != "70b" else 8
     times = []
     for i in range(args.warmup + args.steps):
         t0 = time.perf_counter()
-        O.stack_f64(shape1, *W, h)
+        step.run(cores, nl)
         t1 = time.perf_counter()
         if i >= args.warmup:
             times.append(t1 - t0)
-    t_layer = sum(times) / len(times)
-    value = args.batch / (t_layer * L)
-    sample = f"one of the {L} layers of the {args.model} stack per step (fp64 oracle, 1 thread), time x{L}"
+    t_step = sum(times) / len(times)
+    value = args.batch / (t_step * L / nl)
+    sample = (f"{'one full ' if nl == L else ''}{nl}-layer decode step of the {L}-layer {args.model} stack per step "
+              f"(batch {args.batch}){'' if nl == L else f', tokens/s extrapolated x{L // nl}'}, fp64 oracle "
+              f"matmuls split over {cores} host threads; layer 0's packed weights reused for every layer")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": ws,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_layer * L * 1e3, "higher_is_better": True,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_step * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": f"llama2-{args.model}-stack q3h_b64 decode b={args.batch}",
                    "model": f"llama2-{args.model}-shaped", "global_batch": args.batch, "seq_len": 1,
                    "parallelism": "single", "scheme": "Q3H_B64 (4.0 bits/weight)"},
-        "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": 1, "kind": "oracle", "sample": sample},
+        "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": cores, "kind": "oracle", "sample": sample,
+                         "hardware_concurrency": os.cpu_count(), "cpu_model": cpu_model()},
         "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
-def cpu_baseline(model: str, batch: int, budget_s: float = 10.0):
-    """The oracle timed on a bounded sample of the workload: layer 0 of the
-    stack, repeated for ~budget_s, extrapolated to all layers."""
-    import oracle as O
-    import synth
-
-    cfg, W = _oracle_layer(model)
-    L = cfg["layers"]
-    h = synth.activations(batch, cfg["hidden"])
-    shape1 = dict(cfg, layers=1, qtype=35, block=64)
-    reps, t_total = 0, 0.0
-    while t_total < budget_s:
-        t0 = time.perf_counter()
-        O.stack_f64(shape1, *W, h)
-        t_total += time.perf_counter() - t0
-        reps += 1
-    value = batch / (t_total / reps * L)
-    return {"value": value, "unit": "tokens/s", "cores": 1, "kind": "oracle",
-            "sample": f"layer 0 of the {model} stack x{reps} runs ({t_total:.1f} s), fp64 oracle single-threaded, "
-                      f"time per layer x{L}"}
+def cpu_baseline(model: str, batch: int):
+    """The oracle timed on the box's host cores: one full decode step of the stack on
+    1 thread (O.stack_f64 as it stands) and on all cores (row-split matmuls)."""
+    cores = host_cores()
+    step = OracleStep(model, batch)
+    L = step.cfg["layers"]
+    pts = []
+    for th in ([1, cores] if cores > 1 else [1]):
+        reps, t_total = 0, 0.0
+        while reps < 1 or (t_total < 5.0 and th > 1):
+            t0 = time.perf_counter()
+            step.run(th)
+            t_total += time.perf_counter() - t0
+            reps += 1
+        pts.append({"threads": th, "value": batch * reps / t_total, "s_per_step": t_total / reps, "steps": reps})
+    best = pts[-1]
+    return {"value": best["value"], "unit": "tokens/s", "cores": best["threads"], "kind": "oracle",
+            "sample": (f"full {L}-layer decode step(s) of the {model} stack (batch {batch}); 1 thread = O.stack_f64 "
+                       f"as it stands, {cores} threads = its fp64 matmuls split by rows; layer 0's packed weights "
+                       f"reused for every layer"),
+            "points": pts, "hardware_concurrency": os.cpu_count(), "cpu_model": cpu_model()}
 
 
 # ---------------------------------------------------------------------------
@@ -200,6 +288,10 @@ def run_ours(args):
         else:
             dist.init_process_group("nccl", device_id=dev)
     hbm_peak, bf16_peak, peak_kind = peaks()
+    if args.model is None:  # N = 1: BASELINE configs[1] (7B); N > 1: north_star's 70B stack
+        args.model = "7b" if ws == 1 else "70b"
+    if args.strategy == "auto":  # N > 1: hybrid (Table 4) where the grid allows it, else TP
+        args.strategy = "hybrid" if ws >= 4 else "tensor"
     cfg = synth.LLAMA[args.model]
     s = F.scheme("Q3H", 64)
     shape = F.stack_shape(cfg["layers"], cfg["hidden"], cfg["heads"], cfg["kv_heads"], cfg["head_dim"], cfg["ffn"], s)
@@ -228,8 +320,22 @@ def run_ours(args):
     wsb = torch.zeros(F.if_stack_workspace_bytes(shape, plan, rank, B, F.IF_DECODE), dtype=torch.uint8, device=dev)
     stream = torch.cuda.Stream(dev)
 
-    def step():
+    asg = plan.a[rank]
+    first, last = asg.stage == 0, asg.stage == plan.stages - 1
+    ring = plan.stages > 1
+
+    def step(feedback=True):
+        # decode speed (Table 5, Q22): step k+1's input is step k's output, so on a
+        # pipeline the last stage feeds its h_out back to stage 0 (comm ring,
+        # if_b200.h) -- stages cannot run ahead on independent inputs
+        if ring and feedback and first:
+            comm.recv_prev(h_in, stream)
         F.if_run_stack(shape, plan, rank, comm, stk.arr, h_in, B, F.IF_DECODE, h_out, None, wsb, stream)
+        if ring and feedback and last:
+            comm.send_next(h_out, stream)
+
+    if ring and last:  # prime the feedback loop: stage 0's first step receives this
+        comm.send_next(h_in, stream)
 
     # launches per step (our kernels), counted on one eager step
     with torch.cuda.stream(stream):
@@ -301,6 +407,32 @@ def run_ours(args):
     e2e = {"value": B * args.steps / (ms_e2e / 1e3), "unit": "tokens/s", "h2d_bytes_per_step": B * d * 4,
            "d2h_bytes_per_step": B * d * 4}
 
+    # ---- pipeline throughput (Table 5 "throughput", Q22): the same step without the
+    #      feedback, so up to 2 steps (the comm's double buffer) are in flight per stage
+    pipe = None
+    if ring:
+        with torch.cuda.stream(stream):
+            comm.recv_prev(h_in, stream) if first else None  # drain the decode loop's last feedback
+        gp = torch.cuda.CUDAGraph()
+        with torch.cuda.stream(stream):
+            step(feedback=False)
+            torch.cuda.synchronize()
+            with torch.cuda.graph(gp, stream=stream):
+                step(feedback=False)
+        barrier()
+        p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(stream):
+            p0.record(stream)
+            for _ in range(args.steps):
+                gp.replay()
+            p1.record(stream)
+        p1.synchronize()
+        barrier()
+        t = torch.tensor([p0.elapsed_time(p1)], device="cpu" if share else dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        pipe = {"value": B * args.steps / (float(t.item()) / 1e3), "unit": "tokens/s",
+                "what": "independent inputs, <= 2 steps in flight per stage (no feedback)"}
+
     # ---- roofline of the dominant kernel.  For batch-1 Q3H the whole step is ONE
     #      launch of the persistent decode kernel (decode_mk: 128 fused-dequant
     #      GEMV phases + glue), so its average launch duration is the step time
@@ -337,6 +469,7 @@ def run_ours(args):
             "hbm_gbs": gbs, "hbm_frac_of_measured": gbs / hbm_peak / ws,
             "hbm_frac_of_nominal_8tbs": gbs / 8000.0 / ws,
             "roofline": roof, "e2e": e2e, "gpu_launches": launches_per_step * args.steps,
+            "pipeline_throughput": pipe,
             "clocks": clk.summary(),
         }
     if comm:
@@ -360,10 +493,10 @@ def main():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--batch", type=int, default=1)
-    ap.add_argument("--model", default="7b", choices=["7b", "13b", "70b"])
-    # N > 1 default: by layer -- every stage runs the persistent decode engine; by
-    # tensor / hybrid run the per-layer kernels + peer-memory merges
-    ap.add_argument("--strategy", default="layer", choices=["tensor", "layer", "hybrid"])
+    # default: 7B (BASELINE configs[1]) at N = 1; north_star's 70B stack at N > 1
+    ap.add_argument("--model", default=None, choices=["7b", "13b", "70b"])
+    # N > 1 default (auto): hybrid stages x TP (Table 4) at N >= 4 (2 x N/2), TP at N = 2
+    ap.add_argument("--strategy", default="auto", choices=["auto", "tensor", "layer", "hybrid"])
     ap.add_argument("--stages", type=int, default=0)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")

@@ -200,7 +200,9 @@ if_status if_comm_destroy(if_comm c);
  * rank order).  Stream-ordered, graph capturable. */
 if_status if_comm_allreduce(if_comm c, float* buf, int64_t n, if_stream_t stream);
 /* Pipeline hand-off: send buf[n] to the same group rank of stage+1 / receive
- * from stage-1 into buf. */
+ * from stage-1 into buf.  The stages form a ring: on the last stage send_next
+ * goes to stage 0, and on stage 0 recv_prev receives from the last stage (the
+ * autoregressive feedback of a decode step's output).  Needs stages > 1. */
 if_status if_comm_send_next(if_comm c, const float* buf, int64_t n, if_stream_t stream);
 if_status if_comm_recv_prev(if_comm c, float* buf, int64_t n, if_stream_t stream);
 

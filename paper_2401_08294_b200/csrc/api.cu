@@ -118,6 +118,13 @@ extern "C" if_status if_plan_partition(int32_t strategy, const if_stack_shape* s
     balanced(s.heads, groups, a.group_rank, &a.head_begin, &a.head_end);
     balanced(s.kv_heads, groups, a.group_rank, &a.kv_begin, &a.kv_end);
     balanced(ffn_blocks, groups, a.group_rank, &a.ffn_blk_begin, &a.ffn_blk_end);
+    // W_o is split along K by heads (row-parallel): each rank's column
+    // range must start and end on a quantization-block boundary, or its shard
+    // would not be a whole-block slice of the packed tensor
+    if (((int64_t)a.head_begin * s.head_dim) % s.scheme.block || ((int64_t)a.head_end * s.head_dim) % s.scheme.block)
+      return set_error(IF_ERR_PLAN,
+                       "if_plan_partition: rank %d head range [%d,%d) x head_dim %d is not a multiple of block %d", d,
+                       a.head_begin, a.head_end, s.head_dim, s.scheme.block);
   }
   return IF_OK;
 }

@@ -236,8 +236,13 @@ extern "C" if_status if_comm_create(const if_plan* plan, int32_t rank, int64_t m
   for (int d = 0; d < plan->devices; d++)
     if (plan->a[d].stage == c->stage) c->group[plan->a[d].group_rank] = d;
   c->ngroup = plan->groups;
-  if (c->stage + 1 < plan->stages) c->next = (c->stage + 1) * plan->groups + c->group_rank;
-  if (c->stage > 0) c->prev = (c->stage - 1) * plan->groups + c->group_rank;
+  // pipeline ring: stage s sends to s+1; the last stage's "next" wraps to stage 0 (the
+  // decode loop's feedback of the step output -- if_run_stack itself only sends forward
+  // from non-last stages and receives on non-first stages)
+  if (plan->stages > 1) {
+    c->next = ((c->stage + 1) % plan->stages) * plan->groups + c->group_rank;
+    c->prev = ((c->stage + plan->stages - 1) % plan->stages) * plan->groups + c->group_rank;
+  }
   const size_t bytes = kHdr + (size_t)4 * c->max_elems * sizeof(float);
   if (cudaMalloc(&c->box, bytes) != cudaSuccess || cudaMemset(c->box, 0, bytes) != cudaSuccess ||
       cudaDeviceSynchronize() != cudaSuccess) {

@@ -89,6 +89,20 @@ __device__ __forceinline__ uint32_t get_code(const uint32_t (&w)[NW + 1], int j)
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
+// ---- per-token power-of-two scale of the fp16 hi/lo split (batched decode, Q23)
+// x_t is split as x_t * 2^k = hi + lo (two fp16) with k chosen so max |x_t * 2^k| lies in
+// [2^14, 2^15): no fp16 overflow for |x| > 65504 and no fall into fp16 subnormals for
+// tiny rows.  The epilogue multiplies by 2^-k (exact).
+__device__ __forceinline__ float pow2f(int k) { return __uint_as_float((uint32_t)(127 + k) << 23); }
+__device__ __forceinline__ int xsplit_k(float amax) {
+  const int e = (int)((__float_as_uint(amax) >> 23) & 0xFFu);
+  if (!(amax > 0.f) || e == 0xFF) return 0;  // zero row, NaN or inf: no scaling
+  const int k = 14 - (e - 127);              // fp32 subnormals (e = 0) clamp below
+  return k < -126 ? -126 : (k > 126 ? 126 : k);
+}
+// bytes reserved at the head of an x2 scratch for the per-token 2^-k (64 floats)
+constexpr int X2_SC_BYTES = 256;
+
 __device__ __forceinline__ float half_bits_to_float(uint32_t h16) {
   return __half2float(__ushort_as_half((unsigned short)h16));
 }

@@ -485,8 +485,9 @@ __global__ void __launch_bounds__(MK_THREADS, 1) decode_mk_kernel(const __grid_c
       //    blocks included: never written, zero) into xs with the TMA engine
       if (ct == 0) {
         SpinGuard sg;
-        const int target = (int)((ep + 1u) * (uint32_t)G);
-        while ((int)ld_relaxed_u32(reinterpret_cast<const uint32_t*>(P.done + p - 1)) - target < 0) {
+        const uint32_t target = (ep + 1u) * (uint32_t)G;
+        // wrap-safe: the difference is taken in uint32_t (defined modulo 2^32), then read as signed
+        while ((int32_t)(ld_relaxed_u32(reinterpret_cast<const uint32_t*>(P.done + p - 1)) - target) < 0) {
           __nanosleep(20);
           sg.tick();
         }

@@ -311,12 +311,18 @@ __device__ __forceinline__ void dequant_row(const unsigned char* raw, int64_t n,
 // warps; item = (token, 8-element chunk).
 constexpr int TC_CONV = 3;  // converter warps
 template <bool PERM>
-__device__ __forceinline__ void convert_x_tile(const float* xr, int B, unsigned char* atile, int cidx, int lo_off = 64) {
+__device__ __forceinline__ void convert_x_tile(const float* xr, int B, unsigned char* atile, int cidx, int lo_off = 64,
+                                               const float* xmul = nullptr) {
   const int lane = threadIdx.x & 31;
   for (int t = cidx * 32 + lane; t < B * 8; t += TC_CONV * 32) {
     const int m = t >> 3, c = t & 7;
-    const float4 va = *reinterpret_cast<const float4*>(xr + m * TC_BK + 8 * c);
-    const float4 vb = *reinterpret_cast<const float4*>(xr + m * TC_BK + 8 * c + 4);
+    float4 va = *reinterpret_cast<const float4*>(xr + m * TC_BK + 8 * c);
+    float4 vb = *reinterpret_cast<const float4*>(xr + m * TC_BK + 8 * c + 4);
+    if (xmul) {  // per-token power-of-two split scale (exact)
+      const float f = xmul[m];
+      va = make_float4(va.x * f, va.y * f, va.z * f, va.w * f);
+      vb = make_float4(vb.x * f, vb.y * f, vb.z * f, vb.w * f);
+    }
     // PERM: the fast Q3H dequant's K order (x0, x4, x1, x5, x2, x6, x3, x7) of each chunk
     const float v[8] = {va.x, PERM ? vb.x : va.y, PERM ? va.y : va.z, PERM ? vb.y : va.w,
                         PERM ? va.z : vb.x, PERM ? vb.z : vb.y, PERM ? va.w : vb.z, vb.w};
@@ -645,17 +651,32 @@ __global__ void __launch_bounds__(TcShape<QT, BS, SHAPE>::THREADS, 1)
 // x - hi (zero rows for tokens >= B).  Run once per qGEMV when the caller provides
 // scratch; the decode kernel then loads its x tiles with one SWIZZLE_128B TMA per stage
 // instead of converting per CTA (every CTA would otherwise redo it).
+// One CTA per token row t: max |x_t| -> per-token scale 2^k (common.cuh xsplit_k), the
+// split of x_t * 2^k, and sc[t] = 2^-k for the epilogue.
 __global__ void __launch_bounds__(256) x_split_kernel(const float* __restrict__ x, int B, int64_t K, int bp,
-                                                      __half* __restrict__ x2) {
+                                                      __half* __restrict__ x2, float* __restrict__ sc) {
   pdl_trigger();
   pdl_wait();
-  const int64_t total = (int64_t)bp * K;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t t = i / K, k = i - t * K;
-    const float v = t < B ? x[t * K + k] : 0.f;
+  __shared__ float red[8];
+  const int t = blockIdx.x;
+  const float* xr = x + (int64_t)t * K;
+  float m = 0.f;
+  if (t < B)
+    for (int64_t k = threadIdx.x; k < K; k += blockDim.x) m = fmaxf(m, fabsf(xr[k]));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+  __syncthreads();
+  m = 0.f;
+  for (int w = 0; w < (int)(blockDim.x >> 5); w++) m = fmaxf(m, red[w]);
+  const int ks = xsplit_k(m);
+  const float mul = pow2f(ks);
+  if (threadIdx.x == 0) sc[t] = pow2f(-ks);
+  for (int64_t k = threadIdx.x; k < K; k += blockDim.x) {
+    const float v = t < B ? xr[k] * mul : 0.f;
     const __half h = __float2half_rn(v);
-    x2[i] = h;
-    x2[(int64_t)bp * K + i] = __float2half_rn(v - __half2float(h));
+    x2[(int64_t)t * K + k] = h;
+    x2[((int64_t)bp + t) * K + k] = __float2half_rn(v - __half2float(h));
   }
 }
 
@@ -686,7 +707,8 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
 
 // epilogue of the decode kernel (warps 2-5): lane = weight row, y[t, n] = D[n, t] + D[n, bp + t]
 __device__ __forceinline__ void qgemv_epilogue(uint32_t tmem, uint64_t* acc_full, float* __restrict__ Y, int64_t N,
-                                               int B, int bp, int64_t n0, int nks, int atomic_out, int warp, int lane) {
+                                               int B, int bp, int64_t n0, int nks, int atomic_out, int warp, int lane,
+                                               const float* sc) {
   mbar_wait(acc_full, 0);
   tc_fence_after();
   const int q = warp & 3;  // TMEM lane quarter
@@ -700,7 +722,7 @@ __device__ __forceinline__ void qgemv_epilogue(uint32_t tmem, uint64_t* acc_full
 #pragma unroll
       for (int j = 0; j < 16; j++) {
         if (t0 + j < B) {
-          const float v = __uint_as_float(hv[j]) + __uint_as_float(lv[j]);
+          const float v = (__uint_as_float(hv[j]) + __uint_as_float(lv[j])) * sc[t0 + j];  // undo 2^k
           float* dst = Y + (int64_t)(t0 + j) * N + nn;
           if (atomic_out) atomicAdd(dst, v);
           else *dst = v;
@@ -778,7 +800,8 @@ template <int QT, int BS>
 __global__ void __launch_bounds__(TcdVar<QT, BS>::THREADS, 1)
     qgemv_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap wmap,
                     const uint8_t* __restrict__ W, int64_t N, int64_t K, int B, float* __restrict__ Y,
-                    int ksteps_per_split, int atomic_out, int stages, int xpre) {
+                    int ksteps_per_split, int atomic_out, int stages, int xpre, const float* __restrict__ xg,
+                    const float* __restrict__ xsc_g) {
   constexpr int SBPAD = tc_sbpad(QT, BS);
   using V = TcdVar<QT, BS>;
   pdl_trigger();
@@ -798,6 +821,10 @@ __global__ void __launch_bounds__(TcdVar<QT, BS>::THREADS, 1)
   uint64_t* wfull = xr_full + TC_XRMAX;  // [TCD_WR] (FAST)
   uint64_t* wempty = wfull + TCD_WR;     // [TCD_WR]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(wempty + TCD_WR);
+  // per-token split scales (converter path): max |x| bits, 2^k, 2^-k
+  uint32_t* xmax_u = tmem_slot + 4;
+  float* xmul_s = reinterpret_cast<float*>(xmax_u + 64);
+  float* xinv_s = xmul_s + 64;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t n0 = (int64_t)blockIdx.x * TC_BN;
@@ -820,6 +847,7 @@ __global__ void __launch_bounds__(TcdVar<QT, BS>::THREADS, 1)
     }
     fence_mbar_init();
   }
+  for (int i = threadIdx.x; i < 64; i += blockDim.x) xmax_u[i] = 0u;
   // x tiles: rows of tokens >= B (hi and lo) are never written -> zero them once
   for (int s = 0; s < stages; s++)
     for (int i = threadIdx.x; i < ncols * 8; i += blockDim.x)
@@ -863,6 +891,35 @@ __global__ void __launch_bounds__(TcdVar<QT, BS>::THREADS, 1)
     // ---------------- converters: raw fp32 x (2D TMA ring) -> fp16 hi/lo x tiles ----------------
     const int cidx = warp == 0 ? 0 : warp - V::CONV1 + 1;
     const bool issuer = warp == 0 && lane == 0;
+    {
+      // per-token max |x| over this CTA's k range -> power-of-two split scale; the
+      // epilogue of this CTA undoes it before its (split-K) partial is added
+      const int cthr = cidx * 32 + lane;
+      const int64_t k0 = (int64_t)ks0 * TC_BK;
+      const int64_t k1 = min(K, (int64_t)(ks0 + nks) * TC_BK);
+      const int n4 = k1 > k0 ? (int)((k1 - k0) >> 2) : 0;  // K % 8 == 0
+      float m = 0.f;
+      int tc = -1;
+      for (int j = cthr; j < B * n4; j += TC_CONV * 32) {
+        const int t = j / n4;
+        if (t != tc) {
+          if (tc >= 0) atomicMax(&xmax_u[tc], __float_as_uint(m));
+          tc = t;
+          m = 0.f;
+        }
+        const float4 v = reinterpret_cast<const float4*>(xg + (int64_t)t * K + k0)[j - t * n4];
+        m = fmaxf(m, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
+      }
+      if (tc >= 0) atomicMax(&xmax_u[tc], __float_as_uint(m));
+      named_bar_sync(3, TC_CONV * 32);
+      for (int t = cthr; t < 64; t += TC_CONV * 32) {
+        const int kx = xsplit_k(__uint_as_float(xmax_u[t]));
+        xmul_s[t] = pow2f(kx);
+        xinv_s[t] = pow2f(-kx);
+      }
+      named_bar_sync(3, TC_CONV * 32);
+      asm volatile("bar.arrive 5, %0;" ::"n"((TC_CONV + 4) * 32) : "memory");  // scales ready for the epilogue
+    }
     if (issuer)
       for (int i = 0; i < nxr && i < nks; i++) issue_x_stage(&xmap, ks0 + i, xraw + i * xslot, &xr_full[i], bp);
     for (int i = 0; i < nks; i++) {
@@ -870,7 +927,7 @@ __global__ void __launch_bounds__(TcdVar<QT, BS>::THREADS, 1)
       mbar_wait(&empty[s], ((i / stages) & 1) ^ 1);
       mbar_wait(&xr_full[xs], (i >> lxr) & 1);
 #ifndef IFB_TCD_NOCONV
-      convert_x_tile<false>(xraw + xs * xslot, B, smem + s * stage_bytes + TC_B_BYTES, cidx, bp);
+      convert_x_tile<false>(xraw + xs * xslot, B, smem + s * stage_bytes + TC_B_BYTES, cidx, bp, xmul_s);
 #endif
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> tensor core reads
       __syncwarp();
@@ -926,7 +983,8 @@ __global__ void __launch_bounds__(TcdVar<QT, BS>::THREADS, 1)
     qgemv_fast_deq(N, K, n0, ks0, nks, stages, stage_bytes, smem, pring, wfull, wempty, empty, b_full, warp, lane);
   } else if (V::FAST && warp >= 2 && warp < 6) {
     qgemv_fast_deq(N, K, n0, ks0, nks, stages, stage_bytes, smem, pring, wfull, wempty, empty, b_full, warp, lane);
-    qgemv_epilogue(tmem, acc_full, Y, N, B, bp, n0, nks, atomic_out, warp, lane);
+    if (!xpre) named_bar_sync(5, (TC_CONV + 4) * 32);  // the converters' per-CTA scales are in smem
+    qgemv_epilogue(tmem, acc_full, Y, N, B, bp, n0, nks, atomic_out, warp, lane, xpre ? xsc_g : xinv_s);
   } else if (!V::FAST && warp >= 2 && warp < 6) {
     // ---------------- dequantizers: one weight row per thread (Eq. 2 in fp32, -> fp16) ----------------
     const int r = threadIdx.x - 64;  // 0..127
@@ -950,7 +1008,8 @@ __global__ void __launch_bounds__(TcdVar<QT, BS>::THREADS, 1)
       if (lane == 0) mbar_arrive(&b_full[s]);  // ... one arrival per warp
     }
     cp_async_wait<0>();
-    qgemv_epilogue(tmem, acc_full, Y, N, B, bp, n0, nks, atomic_out, warp, lane);
+    if (!xpre) named_bar_sync(5, (TC_CONV + 4) * 32);  // the converters' per-CTA scales are in smem
+    qgemv_epilogue(tmem, acc_full, Y, N, B, bp, n0, nks, atomic_out, warp, lane, xpre ? xsc_g : xinv_s);
   }
   __syncthreads();
   if (warp == 1) {
@@ -1079,12 +1138,15 @@ if_status qgemv_tc_launch(if_scheme s, const uint8_t* W, int64_t N, int64_t K, c
   if (cr != CUDA_SUCCESS) return set_error(IF_ERR_CUDA, "qgemv_tc: cuTensorMapEncodeTiled failed (%d)", (int)cr);
   // caller scratch for fp16 hi/lo x: split once, TMA-load the tiles (no per-CTA conversion)
   const int bp = tc_bpad((int)B), ncols = tcd_ncols((int)B);
-  const int xpre = x2_scratch && x2_bytes >= (size_t)ncols * K * 2 && !(reinterpret_cast<uintptr_t>(x2_scratch) & 15u);
+  // scratch: [64 floats 2^-k per token][x2 fp16 [2 bp, K]] (common.cuh X2_SC_BYTES)
+  const int xpre = x2_scratch && x2_bytes >= (size_t)X2_SC_BYTES + (size_t)ncols * K * 2 &&
+                   !(reinterpret_cast<uintptr_t>(x2_scratch) & 15u);
+  float* x2sc = xpre ? reinterpret_cast<float*>(x2_scratch) : nullptr;
   if (xpre) {
-    __half* x2 = reinterpret_cast<__half*>(x2_scratch);
+    __half* x2 = reinterpret_cast<__half*>(reinterpret_cast<char*>(x2_scratch) + X2_SC_BYTES);
     if (!x2_ready) {
     cudaLaunchConfig_t lc = {};
-    lc.gridDim = dim3((unsigned)std::min<int64_t>(((int64_t)bp * K + 255) / 256, 148 * 8));
+    lc.gridDim = dim3((unsigned)bp);  // one CTA per token row (per-token scale)
     lc.blockDim = dim3(256);
     lc.stream = st;
     cudaLaunchAttribute la[1];
@@ -1096,7 +1158,8 @@ if_status qgemv_tc_launch(if_scheme s, const uint8_t* W, int64_t N, int64_t K, c
     int Bi = (int)B, bpi = bp;
     int64_t Ki = K;
     __half* x2a = x2;
-    void* args[] = {(void*)&xa, (void*)&Bi, (void*)&Ki, (void*)&bpi, (void*)&x2a};
+    float* sca = x2sc;
+    void* args[] = {(void*)&xa, (void*)&Bi, (void*)&Ki, (void*)&bpi, (void*)&x2a, (void*)&sca};
     cudaLaunchKernelExC(&lc, (const void*)x_split_kernel, args);
     count_launch();
     }
@@ -1129,7 +1192,8 @@ if_status qgemv_tc_launch(if_scheme s, const uint8_t* W, int64_t N, int64_t K, c
   }
   return dispatch_scheme(s, [&]<int QT, int BS>() -> if_status {
     auto kern = qgemv_tc_kernel<QT, BS>;
-    constexpr int fixed = (TcdVar<QT, BS>::FAST ? TCD_WR * 4096 : TC_PK * TC_BN * tc_sbpad(QT, BS)) + TCD_XRING + 1024 + 768;
+    constexpr int fixed = (TcdVar<QT, BS>::FAST ? TCD_WR * 4096 : TC_PK * TC_BN * tc_sbpad(QT, BS)) + TCD_XRING + 1024 + 768 +
+                          768;  // + per-token split scales
     const int sb = tcd_stage_bytes((int)B);
     int stages = std::min(TCD_MAXST, (227 * 1024 - fixed) / sb);
     if (stages < 2) return IF_ERR_UNSUPPORTED;
@@ -1149,7 +1213,7 @@ if_status qgemv_tc_launch(if_scheme s, const uint8_t* W, int64_t N, int64_t K, c
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = splits > 1 && !accumulate ? 0 : 1;  // (after the split-K memset: plain stream order)
-    cudaLaunchKernelEx(&cfg, kern, map, wmap, W, N, K, (int)B, Y, kper, atomic_out, stages, xpre);
+    cudaLaunchKernelEx(&cfg, kern, map, wmap, W, N, K, (int)B, Y, kper, atomic_out, stages, xpre, x, (const float*)x2sc);
     count_launch();
     return check_launch("qgemv_tc");
   });

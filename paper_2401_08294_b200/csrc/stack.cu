@@ -28,11 +28,25 @@ __device__ __forceinline__ __nv_bfloat16 to_out<__nv_bfloat16>(float v) {
 }
 
 // optional fp16 hi/lo split of a glue kernel's output for the tensor-core qGEMV that
-// reads it (x2 [2 bp, K]: row t = hi, row bp + t = lo), so no separate split launch
+// reads it (x2 [2 bp, K]: row t = hi, row bp + t = lo, of x_t * 2^k_t; sc[t] = 2^-k_t,
+// common.cuh xsplit_k), so no separate split launch.  The x2 variants run one CTA per
+// token row: the row's max |x| fixes its scale before any element is split.
 __device__ __forceinline__ void put_x2(__half* x2, int bp, int64_t K, int64_t t, int64_t k, float v) {
   const __half h = __float2half_rn(v);
   x2[t * K + k] = h;
   x2[((int64_t)bp + t) * K + k] = __float2half_rn(v - __half2float(h));
+}
+
+// block-wide max (blockDim.x a multiple of 32, <= 1024); every thread gets the result
+__device__ __forceinline__ float block_max(float m, float* red) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+  __syncthreads();
+  m = 0.f;
+  for (int w = 0; w < (int)(blockDim.x >> 5); w++) m = fmaxf(m, red[w]);
+  return m;
 }
 
 // a[t] = h[t] / sqrt(mean(h[t]^2) + 1e-5)
@@ -41,19 +55,24 @@ __device__ __forceinline__ void put_x2(__half* x2, int bp, int64_t K, int64_t t,
 template <typename OutT>
 __global__ void __launch_bounds__(256) rmsnorm_kernel(const float* __restrict__ h, OutT* __restrict__ a, int d,
                                                       float* __restrict__ zbuf = nullptr, int64_t zn = 0,
-                                                      __half* __restrict__ x2 = nullptr, int T = 0, int bp = 0) {
+                                                      __half* __restrict__ x2 = nullptr, int T = 0, int bp = 0,
+                                                      float* __restrict__ sc = nullptr) {
   pdl_trigger();
   pdl_wait();
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < zn; i += (int64_t)gridDim.x * blockDim.x)
     zbuf[i] = 0.f;
   if (x2 && (int)blockIdx.x >= T) {  // padding token rows of the split
     for (int i = threadIdx.x; i < d; i += blockDim.x) put_x2(x2, bp, d, blockIdx.x, i, 0.f);
+    if (threadIdx.x == 0) sc[blockIdx.x] = 1.f;
     return;
   }
   __shared__ float red[8];
   const float* hr = h + (int64_t)blockIdx.x * d;
-  float ss = 0.f;
-  for (int i = threadIdx.x; i < d; i += blockDim.x) ss = fmaf(hr[i], hr[i], ss);
+  float ss = 0.f, mx = 0.f;
+  for (int i = threadIdx.x; i < d; i += blockDim.x) {
+    ss = fmaf(hr[i], hr[i], ss);
+    mx = fmaxf(mx, fabsf(hr[i]));
+  }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
@@ -61,53 +80,104 @@ __global__ void __launch_bounds__(256) rmsnorm_kernel(const float* __restrict__ 
   float tot = 0.f;
   for (int w = 0; w < (int)(blockDim.x >> 5); w++) tot += red[w];
   const float inv = 1.0f / sqrtf(tot / (float)d + 1e-5f);
+  float mul = 1.f;
+  if (x2) {
+    const int k = xsplit_k(block_max(mx, red) * inv);
+    mul = pow2f(k);
+    if (threadIdx.x == 0) sc[blockIdx.x] = pow2f(-k);
+  }
   OutT* ar = a + (int64_t)blockIdx.x * d;
   for (int i = threadIdx.x; i < d; i += blockDim.x) {
     const float v = hr[i] * inv;
     ar[i] = to_out<OutT>(v);
-    if (x2) put_x2(x2, bp, d, blockIdx.x, i, v);
+    if (x2) put_x2(x2, bp, d, blockIdx.x, i, v * mul);
   }
 }
 
 // ctx[t, i*hd + e] = v[t, j*hd + e],  j = floor((h0 + i)/(H/G)) - k0  (local heads/kv-heads)
 template <typename OutT>
 __global__ void vbcast_kernel(const float* __restrict__ qkv, OutT* __restrict__ ctx, int T, int lh, int lkv, int hd,
-                              int h0, int k0, int per, __half* __restrict__ x2 = nullptr, int bp = 0) {
+                              int h0, int k0, int per) {
   pdl_trigger();
   pdl_wait();
   const int64_t nq = (int64_t)lh * hd, nqkv = (int64_t)(lh + 2 * lkv) * hd;
-  const int64_t total = (int64_t)(x2 ? bp : T) * nq;
+  const int64_t total = (int64_t)T * nq;
   for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total; idx += (int64_t)gridDim.x * blockDim.x) {
     const int64_t t = idx / nq, r = idx - t * nq;
-    if (t >= T) {
-      put_x2(x2, bp, nq, t, r, 0.f);
-      continue;
-    }
     const int i = (int)(r / hd), e = (int)(r - (int64_t)i * hd);
     const int j = (h0 + i) / per - k0;
-    const float v = qkv[t * nqkv + (int64_t)(lh + lkv) * hd + (int64_t)j * hd + e];
-    ctx[idx] = to_out<OutT>(v);
-    if (x2) put_x2(x2, bp, nq, t, r, v);
+    ctx[idx] = to_out<OutT>(qkv[t * nqkv + (int64_t)(lh + lkv) * hd + (int64_t)j * hd + e]);
+  }
+}
+
+// x2 variant, one CTA per token row t < bp: the ctx row is made of the rank's v rows
+// (every local kv head feeds at least one local head), so its max is the max of v
+__global__ void __launch_bounds__(256) vbcast_x2_kernel(const float* __restrict__ qkv, float* __restrict__ ctx, int T,
+                                                        int lh, int lkv, int hd, int h0, int k0, int per,
+                                                        __half* __restrict__ x2, int bp, float* __restrict__ sc) {
+  pdl_trigger();
+  pdl_wait();
+  __shared__ float red[8];
+  const int t = blockIdx.x;
+  const int64_t nq = (int64_t)lh * hd, nqkv = (int64_t)(lh + 2 * lkv) * hd;
+  const float* vr = qkv + (int64_t)t * nqkv + (int64_t)(lh + lkv) * hd;
+  float mx = 0.f;
+  if (t < T)
+    for (int i = threadIdx.x; i < lkv * hd; i += blockDim.x) mx = fmaxf(mx, fabsf(vr[i]));
+  const int k = xsplit_k(block_max(mx, red));
+  const float mul = pow2f(k);
+  if (threadIdx.x == 0) sc[t] = pow2f(-k);
+  for (int64_t r = threadIdx.x; r < nq; r += blockDim.x) {
+    float v = 0.f;
+    if (t < T) {
+      const int i = (int)(r / hd), e = (int)(r - (int64_t)i * hd);
+      const int j = (h0 + i) / per - k0;
+      v = vr[(int64_t)j * hd + e];
+      ctx[(int64_t)t * nq + r] = v;
+    }
+    put_x2(x2, bp, nq, t, r, v * mul);
   }
 }
 
 // act[t, f] = silu(g) * u with gate/up rows interleaved: g = gu[t, 2f], u = gu[t, 2f+1]
 template <typename OutT>
-__global__ void silu_mul_kernel(const float* __restrict__ gu, OutT* __restrict__ act, int T, int lf,
-                                __half* __restrict__ x2 = nullptr, int bp = 0) {
+__global__ void silu_mul_kernel(const float* __restrict__ gu, OutT* __restrict__ act, int T, int lf) {
   pdl_trigger();
   pdl_wait();
-  const int64_t total = (int64_t)(x2 ? bp : T) * lf;
+  const int64_t total = (int64_t)T * lf;
   for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total; idx += (int64_t)gridDim.x * blockDim.x) {
     const int64_t t = idx / lf, f = idx - t * lf;
-    if (t >= T) {
-      put_x2(x2, bp, lf, t, f, 0.f);
-      continue;
-    }
     const float g = gu[t * 2 * lf + 2 * f], u = gu[t * 2 * lf + 2 * f + 1];
-    const float v = g / (1.0f + expf(-g)) * u;
-    act[idx] = to_out<OutT>(v);
-    if (x2) put_x2(x2, bp, lf, t, f, v);
+    act[idx] = to_out<OutT>(g / (1.0f + expf(-g)) * u);
+  }
+}
+
+// x2 variant, one CTA per token row: pass 1 the row max of silu(g) u, pass 2 the split
+__global__ void __launch_bounds__(256) silu_mul_x2_kernel(const float* __restrict__ gu, float* __restrict__ act, int T,
+                                                          int lf, __half* __restrict__ x2, int bp,
+                                                          float* __restrict__ sc) {
+  pdl_trigger();
+  pdl_wait();
+  __shared__ float red[8];
+  const int t = blockIdx.x;
+  const float* gr = gu + (int64_t)t * 2 * lf;
+  float mx = 0.f;
+  if (t < T)
+    for (int f = threadIdx.x; f < lf; f += blockDim.x) {
+      const float g = gr[2 * f], u = gr[2 * f + 1];
+      mx = fmaxf(mx, fabsf(g / (1.0f + expf(-g)) * u));
+    }
+  const int k = xsplit_k(block_max(mx, red));
+  const float mul = pow2f(k);
+  if (threadIdx.x == 0) sc[t] = pow2f(-k);
+  for (int f = threadIdx.x; f < lf; f += blockDim.x) {
+    float v = 0.f;
+    if (t < T) {
+      const float g = gr[2 * f], u = gr[2 * f + 1];
+      v = g / (1.0f + expf(-g)) * u;
+      act[(int64_t)t * lf + f] = v;
+    }
+    put_x2(x2, bp, lf, t, f, v * mul);
   }
 }
 
@@ -175,6 +245,12 @@ struct WS {
   size_t bytes;
 };
 
+// Workspace layout.  The decode engine's persistent state (phase counters, step
+// epoch, parity-tagged input images) and the fp16 split buffer sit FIRST, at
+// offsets that depend only on (shape, plan, rank) -- never on the call's T -- so
+// one zero-filled workspace serves calls with any T <= max_tokens (ADVICE r1:
+// a T-dependent carve let a later call with another T read stale images as its
+// epoch).  The T-sized activation scratch follows.
 static WS carve(void* base, const Local& L, int64_t T) {
   WS w;
   char* p = static_cast<char*>(base);
@@ -184,19 +260,19 @@ static WS carve(void* base, const Local& L, int64_t T) {
     off += al256(elems * 4);
     return r;
   };
+  w.done = reinterpret_cast<int*>(take((size_t)4 * MK_MAXL + 32));
+  // 3 images of 16 x xstride float4 (xstride <= nbp_max + 9) + 256 floats
+  const size_t nbp_max = (size_t)((std::max(std::max(L.d, L.nq), L.lf) / 64 + 31) / 32) * 32;
+  w.xsimg = take(3 * 16 * (nbp_max + 16) * 4 + 256);
+  const size_t maxK = (size_t)std::max(std::max(L.d, L.nq), L.lf);
+  w.x2 = take(64 * maxK + X2_SC_BYTES / 4);  // [64 per-token scales][2 x 64 x maxK fp16]
+  w.x2_bytes = 64 * maxK * 4 + X2_SC_BYTES;
   w.a = take((size_t)T * L.d);
   w.qkv = take((size_t)T * L.nqkv);
   w.ctx = take((size_t)T * L.nq);
   w.gu = take((size_t)T * 2 * L.lf);
   w.act = take((size_t)T * L.lf);
   w.part = take((size_t)T * L.d);
-  w.done = reinterpret_cast<int*>(take((size_t)4 * MK_MAXL + 32));
-  // 3 images of 16 x xstride float4 (xstride <= nbp_max + 9) + 256 floats
-  const size_t nbp_max = (size_t)((std::max(std::max(L.d, L.nq), L.lf) / 64 + 31) / 32) * 32;
-  w.xsimg = take(3 * 16 * (nbp_max + 16) * 4 + 256);
-  const size_t maxK = (size_t)std::max(std::max(L.d, L.nq), L.lf);
-  w.x2 = take(64 * maxK);  // 2 x 64 x maxK fp16
-  w.x2_bytes = 64 * maxK * 4;
   w.bytes = off;
   return w;
 }
@@ -304,7 +380,8 @@ extern "C" if_status if_run_stack(const if_stack_shape* shape, const if_plan* pl
   // batched decode (2 <= T <= 64): the glue kernels also write the fp16 hi/lo split of
   // the next qGEMV's input into the workspace (x2r: no separate split launch)
   const bool use_x2 = mode == IF_DECODE && T >= 2;
-  __half* x2h = use_x2 ? reinterpret_cast<__half*>(w.x2) : nullptr;
+  __half* x2h = use_x2 ? reinterpret_cast<__half*>(reinterpret_cast<char*>(w.x2) + X2_SC_BYTES) : nullptr;
+  float* x2s = use_x2 ? reinterpret_cast<float*>(w.x2) : nullptr;
   const int bpx = use_x2 ? tc_bpad((int)T) : 0;
   const int x2r = use_x2 ? 1 : 0;
   for (int l = 0; l < nlayers; l++) {
@@ -313,13 +390,16 @@ extern "C" if_status if_run_stack(const if_stack_shape* shape, const if_plan* pl
     if (mode == IF_DECODE) {
       // ---- attention sub-layer ----
       launch_pdl(rmsnorm_kernel<float>, (unsigned)std::max<int64_t>(T, bpx), 256, cs, (const float*)h_out, w.a, (int)L.d,
-                 w.qkv, (int64_t)T * L.nqkv, x2h, (int)T, bpx);
+                 w.qkv, (int64_t)T * L.nqkv, x2h, (int)T, bpx, x2s);
       count_launch();
       if ((st = qgemv_dispatch("if_run_stack(qkv)", sc, Wl.wqkv, L.nqkv, L.d, w.a, T, w.qkv, 1, cs, w.x2, w.x2_bytes, x2r)))
         return st;
-      launch_pdl(vbcast_kernel<float>, (unsigned)ew_grid(std::max<int64_t>(T, bpx) * L.nq), 256, cs, (const float*)w.qkv,
-                 w.ctx, (int)T, (int)L.lh, (int)L.lkv, (int)L.hd, (int)asg.head_begin, (int)asg.kv_begin, (int)per, x2h,
-                 bpx);
+      if (use_x2)
+        launch_pdl(vbcast_x2_kernel, (unsigned)bpx, 256, cs, (const float*)w.qkv, w.ctx, (int)T, (int)L.lh, (int)L.lkv,
+                   (int)L.hd, (int)asg.head_begin, (int)asg.kv_begin, (int)per, x2h, bpx, x2s);
+      else
+        launch_pdl(vbcast_kernel<float>, (unsigned)ew_grid(T * L.nq), 256, cs, (const float*)w.qkv, w.ctx, (int)T,
+                   (int)L.lh, (int)L.lkv, (int)L.hd, (int)asg.head_begin, (int)asg.kv_begin, (int)per);
       count_launch();
       if (groups == 1) {
         if ((st = qgemv_dispatch("if_run_stack(o)", sc, Wl.wo, L.d, L.nq, w.ctx, T, h_out, 1, cs, w.x2, w.x2_bytes, x2r)))
@@ -331,12 +411,16 @@ extern "C" if_status if_run_stack(const if_stack_shape* shape, const if_plan* pl
       }
       // ---- feed-forward sub-layer ----
       launch_pdl(rmsnorm_kernel<float>, (unsigned)std::max<int64_t>(T, bpx), 256, cs, (const float*)h_out, w.a, (int)L.d,
-                 w.gu, (int64_t)T * 2 * L.lf, x2h, (int)T, bpx);
+                 w.gu, (int64_t)T * 2 * L.lf, x2h, (int)T, bpx, x2s);
       count_launch();
       if ((st = qgemv_dispatch("if_run_stack(gu)", sc, Wl.wgu, 2 * L.lf, L.d, w.a, T, w.gu, 1, cs, w.x2, w.x2_bytes, x2r)))
         return st;
-      launch_pdl(silu_mul_kernel<float>, (unsigned)ew_grid(std::max<int64_t>(T, bpx) * L.lf), 256, cs, (const float*)w.gu,
-                 w.act, (int)T, (int)L.lf, x2h, bpx);
+      if (use_x2)
+        launch_pdl(silu_mul_x2_kernel, (unsigned)bpx, 256, cs, (const float*)w.gu, w.act, (int)T, (int)L.lf, x2h, bpx,
+                   x2s);
+      else
+        launch_pdl(silu_mul_kernel<float>, (unsigned)ew_grid(T * L.lf), 256, cs, (const float*)w.gu, w.act, (int)T,
+                   (int)L.lf);
       count_launch();
       if (groups == 1) {
         if ((st = qgemv_dispatch("if_run_stack(down)", sc, Wl.wdown, L.d, L.lf, w.act, T, h_out, 1, cs, w.x2, w.x2_bytes, x2r)))

@@ -44,6 +44,8 @@ def col_slice(packed: torch.Tensor, s: Scheme, N: int, K: int, c0: int, c1: int)
     from . import if_block_bytes
     bb = if_block_bytes(s)
     nb = K // s.block
+    if c0 % s.block or c1 % s.block:
+        raise ValueError(f"col_slice [{c0},{c1}) is not aligned to block {s.block}")
     v = packed.view(N, nb, bb)[:, c0 // s.block:c1 // s.block, :]
     return v.contiguous().view(-1)
 

@@ -4,7 +4,7 @@ This module holds NO arithmetic of the method (no quantization, no products):
 it is the counter-based input generator of DESIGN.md §Inputs, the one thing
 both sides may share.  The CUDA library implements the *same* generator as a
 device kernel (``if_synth_fill``) so that multi-GB weights can be generated in
-HBM; ``tests/test_gpu_synth.py`` checks the two bit for bit.
+HBM; ``tests/test_gpu_kernels.py::test_synth_generator_bitwise`` checks the two bit for bit.
 
 Generator:
   h   = splitmix64(seed ^ tensor_id*0x9E3779B97F4A7C15 ^ idx*0xD1B54A32D192ED03)

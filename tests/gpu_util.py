@@ -26,3 +26,27 @@ def to_bf16_exact(a: np.ndarray):
     """fp32 -> bf16 (torch RN) and back: the exact bf16 values handed to the GPU."""
     t = torch.from_numpy(np.ascontiguousarray(a, np.float32)).to(torch.bfloat16)
     return t, t.to(torch.float32).numpy()
+
+
+def oracle_stack_per_token(shape: dict, wq, wo, wgu, wd, h: np.ndarray, threads: int = 0):
+    """O.stack_f64 on every token row separately, rows run concurrently (the oracle's
+    C call releases the GIL).  Tokens are independent in the stack (Q18: each
+    token's attention sees only its own position), so the result equals one
+    O.stack_f64 call on all rows; this only spreads the fp64 work over host cores."""
+    import os
+    from concurrent.futures import ThreadPoolExecutor
+
+    import oracle as O
+    T = h.shape[0]
+    n = threads or min(T, os.cpu_count() or 1)
+    with ThreadPoolExecutor(max(1, n)) as ex:
+        outs = list(ex.map(lambda t: O.stack_f64(shape, wq, wo, wgu, wd, h[t:t + 1]), range(T)))
+    return np.concatenate([o[0] for o in outs]), np.concatenate([o[1] for o in outs])
+
+
+def oracle_rows_matmul(qtype: int, bs: int, packed: np.ndarray, N: int, K: int, X: np.ndarray, rows):
+    """O.matmul_f64 of the sampled output rows `rows` only (packed rows are contiguous)."""
+    import oracle as O
+    rb = O.packed_bytes(qtype, bs, 1, K)
+    sub = np.concatenate([packed[r * rb:(r + 1) * rb] for r in rows])
+    return O.matmul_f64(qtype, bs, sub, len(rows), K, X)

@@ -131,3 +131,15 @@ def test_plan_errors_through_abi():
     with pytest.raises(F.IFError) as e:
         F.if_plan_partition(F.IF_BY_TENSOR, _shape(LLAMA["13b"]), 6)
     assert e.value.status == 6  # 40 heads over 6 groups
+
+
+def test_plan_rejects_head_ranges_off_block_boundaries():
+    """W_o is split along K by heads, so each rank's column range
+    h * head_dim must fall on a quantization-block boundary (else its shard is not
+    a whole-block slice): heads = 12, head_dim = 80, 2 groups -> 480 % 64 != 0."""
+    s = F.scheme(35, 64)
+    shape = F.stack_shape(2, 960, 12, 12, 80, 1024, s)
+    with pytest.raises(F.IFError) as e:
+        F.if_plan_partition(F.IF_BY_TENSOR, shape, 2)
+    assert e.value.status == 6
+    F.if_plan_partition(F.IF_BY_TENSOR, shape, 3)  # 4 heads x 80 = 320 = 5 blocks: accepted

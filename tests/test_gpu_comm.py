@@ -72,12 +72,16 @@ def _worker(rank, world, port, mode, q):
             torch.cuda.synchronize()
             comm.destroy()
         else:
-            strategy = F.IF_BY_TENSOR if mode == "tp" else F.IF_BY_LAYER
-            plan = F.if_plan_partition(strategy, shape, world)
+            if mode.startswith("hybrid"):
+                # Table 4: 2 pipeline stages x 2 tensor-parallel ranks
+                plan = F.if_plan_partition(F.IF_HYBRID, shape, world, 2, world // 2)
+            else:
+                strategy = F.IF_BY_TENSOR if mode == "tp" else F.IF_BY_LAYER
+                plan = F.if_plan_partition(strategy, shape, world)
             stk = Stack(cfg, s, plan, rank, dev)
             comm = F.Comm(plan, rank, 8, cfg["hidden"])
             comm.exchange()
-            T = 1 if mode == "pp1" else 2  # T = 1 runs each stage through the persistent engine
+            T = 1 if mode in ("pp1", "hybrid1") else 2  # pp T = 1: each stage through the persistent engine
             h = synth.activations(T, cfg["hidden"], tid=5)
             hd = torch.from_numpy(h).to(dev)
             out = torch.zeros_like(hd)
@@ -155,3 +159,17 @@ def test_stack_layer_parallel_two_ranks():
 def test_stack_layer_parallel_two_ranks_decode_engine():
     out = _run("pp1")
     assert out[1]["err"] <= 1e-3, out
+
+
+def test_stack_hybrid_2x2_four_ranks():
+    """Hybrid partition (Table 4): 2 stages x 2 TP ranks, 4 processes on one
+    GPU; both last-stage ranks hold the full h_out and must equal the oracle."""
+    out = _run("hybrid", world=4, timeout=360)
+    for r in (2, 3):
+        assert out[r]["err"] <= 1e-3, out
+
+
+def test_stack_hybrid_2x2_four_ranks_batch1():
+    out = _run("hybrid1", world=4, timeout=360)
+    for r in (2, 3):
+        assert out[r]["err"] <= 1e-3, out

@@ -1,0 +1,129 @@
+"""GPU parity at BASELINE.json's full sizes (VERDICT r1 "what's weak" #1).
+
+* quantize / dequantize of a full 7B gate/up tensor (22016 x 4096 = 1.41 M
+  Q3H_B64 blocks: past the quantize kernel's grid-stride wrap) against the
+  oracle quantizing the host generator's tensor: bit-exact;
+* the three benchmarked prefill qGEMM shapes at M = 512 (BASELINE configs[2]):
+  sampled output rows against the oracle's fp64 matmul of those rows, 2e-2;
+* 2-layer 13B- and 70B-shaped stacks (full width: d 5120/8192, F 13824/28672,
+  70B's GQA 8 kv heads with 8 q heads per group) at B = 1 (the persistent
+  engine's stack mode at x-strides 233 / 457) and B = 16 (tensor-core path),
+  1e-3 normwise on h_out and last_qkv; the device shards are first checked
+  bit-exact against the oracle quantizing the host generator's rows.
+"""
+import numpy as np
+import pytest
+
+import oracle as O
+import paper_2401_08294_b200 as F
+import synth
+from gpu_util import dev, normwise, oracle_rows_matmul, oracle_stack_per_token, to_bf16_exact, torch
+from paper_2401_08294_b200.model import Stack, deinterleave_rows
+
+pytestmark = pytest.mark.gpu
+
+
+def _device_weight(tid: int, sigma: float, N: int, K: int, d):
+    w = torch.empty(N * K, dtype=torch.float32, device=d)
+    F.if_synth_fill(synth.SEED_WEIGHTS, tid, float(synth.scale(sigma)), w)
+    return w
+
+
+def test_quantize_full_size_7b_gate_up():
+    """1.41 M blocks (> 148*16*128 = 303,104: the grid-stride wrap) vs O.quantize."""
+    d = dev()
+    Fd, D = 11008, 4096
+    s = F.scheme(35, 64)
+    W = torch.empty(2 * Fd * D, dtype=torch.float32, device=d)
+    F.if_synth_fill(synth.SEED_WEIGHTS, synth.tensor_id(0, "gate"), float(synth.scale(1 / 64)), W[:Fd * D])
+    F.if_synth_fill(synth.SEED_WEIGHTS, synth.tensor_id(0, "up"), float(synth.scale(1 / 64)), W[Fd * D:])
+    p = torch.empty(F.if_packed_bytes(s, 2 * Fd, D), dtype=torch.uint8, device=d)
+    st = torch.zeros(1, dtype=torch.int32, device=d)
+    F.if_quantize(s, W, 2 * Fd, D, p, st)
+    torch.cuda.synchronize()
+    assert int(st.item()) == 0
+    del W
+    host = np.concatenate([synth.weight(0, "gate", Fd, D, D), synth.weight(0, "up", Fd, D, D)])
+    ref = O.quantize(35, 64, host)
+    del host
+    assert (2 * Fd * D) // 64 > 148 * 16 * 128
+    assert np.array_equal(p.cpu().numpy(), ref)
+    Wd = torch.empty(2 * Fd, D, dtype=torch.float32, device=d)
+    F.if_dequantize(s, p, 2 * Fd, D, Wd, st)
+    torch.cuda.synchronize()
+    assert int(st.item()) == 0
+    assert np.array_equal(Wd.cpu().numpy().view(np.uint32), O.dequantize(35, 64, ref, 2 * Fd, D).view(np.uint32))
+
+
+@pytest.mark.parametrize("N,K", [(12288, 4096), (22016, 4096), (4096, 11008)])
+def test_prefill_qgemm_full_shapes(N, K):
+    """BASELINE configs[2] shapes at M = 512, Q3H_B64, as bench/prof time them."""
+    d = dev()
+    M = 512
+    s = F.scheme(35, 64)
+    tid = 1000 + N // 64
+    W = _device_weight(tid, 1 / 64, N, K, d)
+    p = torch.empty(F.if_packed_bytes(s, N, K), dtype=torch.uint8, device=d)
+    F.if_quantize(s, W, N, K, p)
+    del W
+    Xb, Xf = to_bf16_exact(synth.activations(M, K, tid=7))
+    Y = torch.empty(M, N, device=d)
+    F.if_qgemm(s, p, N, K, Xb.to(d).view(torch.int16), M, Y)
+    torch.cuda.synchronize()
+    rng = np.random.default_rng(N + K)
+    rows = sorted(set([0, 1, 127, 128, N - 1] + rng.choice(N, 187, replace=False).tolist()))
+    ph = p.cpu().numpy()
+    rb = F.if_packed_bytes(s, 1, K)
+    # the sampled rows were quantized bit-exactly (oracle on the host generator's rows)
+    for r in rows[:8]:
+        wr = synth.matrix(synth.SEED_WEIGHTS, tid, 1 / 64, N, K, r, r + 1)
+        assert np.array_equal(ph[r * rb:(r + 1) * rb], O.quantize(35, 64, wr))
+    ref = oracle_rows_matmul(35, 64, ph, N, K, Xf, rows)  # [M, len(rows)]
+    got = Y.cpu().numpy()[:, rows]
+    assert normwise(got, ref) <= 2e-2
+
+
+def _host_layer_rows_check(cfg, stk, rows_per=3):
+    """Sampled rows of layer 0's device shards == O.quantize of the host generator's rows."""
+    d, H, G, hd, Fd = cfg["hidden"], cfg["heads"], cfg["kv_heads"], cfg["head_dim"], cfg["ffn"]
+    wqkv, wo, wgu, wdn = [t.cpu().numpy() for t in stk.layers[0]]
+    rb_d = O.packed_bytes(35, 64, 1, d)
+    rng = np.random.default_rng(d)
+    for r in rng.choice(H * hd, rows_per, replace=False):
+        assert np.array_equal(wqkv[r * rb_d:(r + 1) * rb_d], O.quantize(35, 64, synth.weight(0, "q", H * hd, d, d, r, r + 1)))
+    for r in rng.choice(G * hd, rows_per, replace=False):
+        rr = H * hd + G * hd + r  # rows: q, then k, then v
+        assert np.array_equal(wqkv[rr * rb_d:(rr + 1) * rb_d], O.quantize(35, 64, synth.weight(0, "v", G * hd, d, d, r, r + 1)))
+    for f in rng.choice(Fd, rows_per, replace=False):
+        assert np.array_equal(wgu[(2 * f + 1) * rb_d:(2 * f + 2) * rb_d], O.quantize(35, 64, synth.weight(0, "up", Fd, d, d, f, f + 1)))
+    rb_f = O.packed_bytes(35, 64, 1, Fd)
+    for r in rng.choice(d, rows_per, replace=False):
+        assert np.array_equal(wdn[r * rb_f:(r + 1) * rb_f], O.quantize(35, 64, synth.weight(0, "down", d, Fd, d, r, r + 1)))
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("model", ["13b", "70b"])
+@pytest.mark.parametrize("T", [1, 16])
+def test_stack_full_width_two_layers(model, T):
+    d = dev()
+    cfg = dict(synth.LLAMA[model], layers=2)
+    s = F.scheme(35, 64)
+    shape = F.stack_shape(*[cfg[k] for k in ("layers", "hidden", "heads", "kv_heads", "head_dim", "ffn")], s)
+    plan = F.if_plan_partition(F.IF_BY_LAYER, shape, 1)
+    stk = Stack(cfg, s, plan, 0, d)
+    if T == 1:
+        _host_layer_rows_check(cfg, stk)
+    h = synth.activations(T, cfg["hidden"], tid=4)
+    hd_ = torch.from_numpy(h).to(d)
+    out = torch.empty_like(hd_)
+    nqkv = (cfg["heads"] + 2 * cfg["kv_heads"]) * cfg["head_dim"]
+    qkv = torch.empty(T, nqkv, device=d)
+    ws = torch.zeros(F.if_stack_workspace_bytes(shape, plan, 0, T, F.IF_DECODE), dtype=torch.uint8, device=d)
+    F.if_run_stack(shape, plan, 0, None, stk.arr, hd_, T, F.IF_DECODE, out, qkv, ws)
+    torch.cuda.synchronize()
+    host = [[t.cpu().numpy() for t in layer] for layer in stk.layers]
+    del stk
+    ho, qo = oracle_stack_per_token(dict(cfg, qtype=35, block=64), [l[0] for l in host], [l[1] for l in host],
+                                    [deinterleave_rows(l[2], 2 * cfg["ffn"]) for l in host], [l[3] for l in host], h)
+    assert normwise(out.cpu().numpy(), ho) <= 1e-3
+    assert normwise(qkv.cpu().numpy(), qo) <= 1e-3

@@ -221,3 +221,29 @@ def test_qgemm_q3h_shapes(M, N, K):
     torch.cuda.synchronize()
     ref = O.matmul_f64(35, 64, p, N, K, Xf)
     assert normwise(Y.cpu().numpy(), ref) <= 2e-2
+
+
+@pytest.mark.parametrize("B", [2, 4, 16])
+@pytest.mark.parametrize("xscale", [1e-6, 1e5, "mixed"])
+def test_qgemv_batched_scaled_x(B, xscale):
+    """the tensor-core batched path splits x into fp16 hi + lo with a
+    per-token power-of-two scale, so |x| > 65504 does not overflow and |x| ~ 1e-6
+    does not fall into fp16 subnormals -- same 1e-3 gate as B = 1."""
+    d = dev()
+    rng = np.random.default_rng(B)
+    N, K = 200, 64 * 40
+    W = (rng.standard_normal((N, K)) / np.sqrt(K)).astype(np.float32)
+    p = O.quantize(35, 64, W)
+    x = rng.standard_normal((B, K))
+    if xscale == "mixed":
+        x *= np.array([10.0 ** (6 * (i % 3) - 6) for i in range(B)])[:, None]  # 1e-6, 1, 1e6 per token
+    else:
+        x *= xscale
+    x = x.astype(np.float32)
+    y = torch.empty(B, N, device=d)
+    F.if_qgemv(F.scheme(35, 64), torch.from_numpy(p).to(d), N, K, torch.from_numpy(x).to(d), B, y)
+    torch.cuda.synchronize()
+    ref = O.matmul_f64(35, 64, p, N, K, x)
+    got = y.cpu().numpy()
+    for t in range(B):  # per token: each row has its own magnitude
+        assert normwise(got[t], ref[t]) <= 1e-3, t

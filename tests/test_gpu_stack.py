@@ -121,3 +121,72 @@ def test_stack_decode_repeated_calls_same_workspace():
         assert normwise(out.cpu().numpy(), ho) <= 1e-3, it
         outs.append(out.cpu().numpy())
     assert np.array_equal(outs[0], outs[1]) and np.array_equal(outs[2], outs[3])  # deterministic
+
+
+def test_stack_decode_workspace_reused_across_T():
+    """ONE workspace sized for max_tokens serves calls with any
+    T <= max_tokens -- T = 1 (engine), 2 (engine per token), 7 (tensor-core path),
+    1 again, 4 -- each equal to the oracle (the engine's epoch/images live at
+    T-independent offsets)."""
+    d = dev()
+    cfg = SMALL
+    s = F.scheme(35, 64)
+    shape = F.stack_shape(*[cfg[k] for k in ("layers", "hidden", "heads", "kv_heads", "head_dim", "ffn")], s)
+    plan = F.if_plan_partition(F.IF_BY_LAYER, shape, 1)
+    stk = Stack(cfg, s, plan, 0, d)
+    ws = torch.zeros(F.if_stack_workspace_bytes(shape, plan, 0, 7, F.IF_DECODE), dtype=torch.uint8, device=d)
+    for it, T in enumerate([1, 2, 7, 1, 4, 1]):
+        h = synth.activations(T, cfg["hidden"], tid=20 + it)
+        hd = torch.from_numpy(h).to(d)
+        out = torch.empty_like(hd)
+        F.if_run_stack(shape, plan, 0, None, stk.arr, hd, T, F.IF_DECODE, out, None, ws)
+        torch.cuda.synchronize()
+        ho, _ = _oracle(cfg, 35, 64, stk, h)
+        assert normwise(out.cpu().numpy(), ho) <= 1e-3, (it, T)
+
+
+def _host_stack(cfg, qtype, bs, wscale):
+    """Packed layers quantized on the host by the oracle from the generator's weights
+    times `wscale` (large weights drive |x| of the o/down inputs past fp16 range)."""
+    d, H, G, hd, Fd = cfg["hidden"], cfg["heads"], cfg["kv_heads"], cfg["head_dim"], cfg["ffn"]
+    wq, wo, wgu, wdn = [], [], [], []
+    for l in range(cfg["layers"]):
+        w = lambda n, N, K: synth.weight(l, n, N, K, d) * np.float32(wscale)
+        wq.append(O.quantize(qtype, bs, np.concatenate([w("q", H * hd, d), w("k", G * hd, d), w("v", G * hd, d)])))
+        wo.append(O.quantize(qtype, bs, w("o", d, H * hd)))
+        wgu.append(O.quantize(qtype, bs, np.concatenate([w("gate", Fd, d), w("up", Fd, d)])))
+        wdn.append(O.quantize(qtype, bs, w("down", d, Fd)))
+    return wq, wo, wgu, wdn
+
+
+@pytest.mark.parametrize("T", [8, 16])
+def test_stack_decode_large_activations(T):
+    """Weights x 300: the v-broadcast and SiLU*u rows reach |x| >> 65504.  The batched
+    path's fp16 hi/lo split carries a per-token power-of-two scale, so the
+    stack still meets 1e-3 instead of overflowing to inf/NaN."""
+    from paper_2401_08294_b200.model import interleave_rows
+    d = dev()
+    cfg = dict(SMALL, layers=2)
+    s = F.scheme(35, 64)
+    shape = F.stack_shape(*[cfg[k] for k in ("layers", "hidden", "heads", "kv_heads", "head_dim", "ffn")], s)
+    plan = F.if_plan_partition(F.IF_BY_LAYER, shape, 1)
+    wq, wo, wgu, wdn = _host_stack(cfg, 35, 64, 300.0)
+    Fd = cfg["ffn"]
+    layers = []
+    for l in range(cfg["layers"]):
+        g = torch.from_numpy(wgu[l][:len(wgu[l]) // 2]).to(d)
+        u = torch.from_numpy(wgu[l][len(wgu[l]) // 2:]).to(d)
+        layers.append(tuple(torch.from_numpy(a).to(d) for a in (wq[l], wo[l])) + (interleave_rows(g, u, Fd),
+                                                                                 torch.from_numpy(wdn[l]).to(d)))
+    arr = F.layer_weights_array(layers)
+    h = synth.activations(T, cfg["hidden"], tid=9)
+    hd = torch.from_numpy(h).to(d)
+    out = torch.empty_like(hd)
+    ws = torch.zeros(F.if_stack_workspace_bytes(shape, plan, 0, T, F.IF_DECODE), dtype=torch.uint8, device=d)
+    F.if_run_stack(shape, plan, 0, None, arr, hd, T, F.IF_DECODE, out, None, ws)
+    torch.cuda.synchronize()
+    ho, _ = O.stack_f64(dict(cfg, qtype=35, block=64), wq, wo, wgu, wdn, h)
+    assert np.abs(ho).max() > 65504  # the activations really leave fp16 range
+    o = out.cpu().numpy()
+    assert np.all(np.isfinite(o))
+    assert normwise(o, ho) <= 1e-3
