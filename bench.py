@@ -312,8 +312,11 @@ def run_ours(args):
     stk = Stack(cfg, s, plan, rank, dev)
     comm = None
     if ws > 1:
-        comm = F.Comm(plan, rank, max(B, 64), cfg["hidden"])
-        comm.exchange()
+        if args.comm == "nccl":  # library-collective baseline (if_comm_init)
+            comm = F.Comm.nccl(plan, rank)
+        else:  # peer-memory communicator (CUDA IPC over NVLink, deterministic)
+            comm = F.Comm(plan, rank, max(B, 64), cfg["hidden"])
+            comm.exchange()
     d = cfg["hidden"]
     h_in = torch.from_numpy(synth.activations(B, d)).to(dev)
     h_out = torch.empty_like(h_in)
@@ -464,6 +467,7 @@ def run_ours(args):
             "data": "synthetic (counter-based Irwin-Hall weights sigma=1/sqrt(d), activations sigma=1)",
             "config": {"workload": f"llama2-{args.model}-stack q3h_b64 decode b={B}", "model": f"llama2-{args.model}-shaped",
                        "global_batch": B, "seq_len": 1, "parallelism": strategy, "scheme": "Q3H_B64 (4.0 bits/weight)",
+                       "comm": (args.comm if ws > 1 else None),
                        "weight_bytes_per_step": total_bytes,
                        "l2": f"inputs larger than L2 ({total_bytes / 1e9:.2f} GB of weights per step vs 126 MB L2)"},
             "hbm_gbs": gbs, "hbm_frac_of_measured": gbs / hbm_peak / ws,
@@ -498,6 +502,7 @@ def main():
     # N > 1 default (auto): hybrid stages x TP (Table 4) at N >= 4 (2 x N/2), TP at N = 2
     ap.add_argument("--strategy", default="auto", choices=["auto", "tensor", "layer", "hybrid"])
     ap.add_argument("--stages", type=int, default=0)
+    ap.add_argument("--comm", default="peer", choices=["peer", "nccl"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()

@@ -47,7 +47,7 @@ typedef enum {
   IF_ERR_PLAN = 6,    /* indivisible heads/kv-heads/FFN, layers < stages     */
   IF_ERR_GRID = 7,    /* devices != stages x groups                          */
   IF_ERR_CUDA = 8,    /* CUDA launch / runtime failure                               */
-  IF_ERR_COMM = 9,    /* peer-memory communicator failure                            */
+  IF_ERR_COMM = 9,    /* communicator failure (peer memory or NCCL; SURVEY's IF_ERR_NCCL) */
   IF_ERR_UNSUPPORTED = 10
 } if_status;
 
@@ -178,8 +178,19 @@ if_status if_plan_partition(int32_t strategy, const if_stack_shape* shape, int32
                             int32_t stages, int32_t groups, if_plan* out);
 
 /* ---------------------------------------------------------------------------
- * Peer-memory communicator for the TP merges (a7, "merged twice") and
- * the pipeline hand-off (a8).  One process per GPU.  Set-up:
+ * Communicators for the TP merges (a7, "merged twice") and the pipeline
+ * hand-off (a8).  One process per GPU.  Two kinds behind one handle:
+ *
+ * NCCL (the library-collective baseline):
+ *   if_comm_nccl_unique_id(id128)                 rank 0 creates the id (host, 128 B);
+ *   (caller broadcasts it, e.g. torch.distributed.broadcast_object_list)
+ *   if_comm_init(plan, rank, id128, &c)           ncclCommInitRank over plan->devices
+ *       ranks + ncclCommSplit by stage (the TP group).  The device is the caller's
+ *       current CUDA device.  all-reduce = ncclAllReduce (sum; NCCL's reduction
+ *       order, Q21), send/recv = ncclSend/ncclRecv.  libnccl.so.2 is dlopen'ed (a
+ *       process that already loaded torch's copy reuses it); IF_ERR_COMM when absent.
+ *
+ * Peer memory (B200-native, deterministic):
  *   if_comm_create(plan, rank, max_tokens, &c)   allocates this rank's
  *       symmetric mailbox (device memory owned by the communicator);
  *   if_comm_ipc_handle(c, out64)                 64-byte CUDA IPC handle of it;
@@ -189,15 +200,18 @@ if_status if_plan_partition(int32_t strategy, const if_stack_shape* shape, int32
  * Set-up calls synchronise the device.  devices == 1 needs no peers.
  * ------------------------------------------------------------------------- */
 typedef struct if_comm_s* if_comm;
+if_status if_comm_nccl_unique_id(uint8_t* id128 /* host, 128 bytes */);
+if_status if_comm_init(const if_plan* plan, int32_t rank, const uint8_t* nccl_unique_id /* host, 128 B */,
+                       if_comm* out);
 if_status if_comm_create(const if_plan* plan, int32_t rank, int64_t max_tokens, int32_t hidden,
                          if_comm* out);
 if_status if_comm_ipc_handle(if_comm c, uint8_t* handle64 /* host, 64 bytes */);
 if_status if_comm_open_peers(if_comm c, const uint8_t* handles /* host, devices*64 bytes */);
 if_status if_comm_destroy(if_comm c);
 
-/* In-place all-reduce(sum) of buf[n] fp32 over this rank's TP group, through
- * peer memory; every rank of the group ends with bit-identical sums (fixed
- * rank order).  Stream-ordered, graph capturable. */
+/* In-place all-reduce(sum) of buf[n] fp32 over this rank's TP group.  Peer
+ * memory: every rank of the group ends with bit-identical sums (fixed rank
+ * order); NCCL: ncclAllReduce.  Stream-ordered, graph capturable. */
 if_status if_comm_allreduce(if_comm c, float* buf, int64_t n, if_stream_t stream);
 /* Pipeline hand-off: send buf[n] to the same group rank of stage+1 / receive
  * from stage-1 into buf.  The stages form a ring: on the last stage send_next

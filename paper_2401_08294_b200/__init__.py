@@ -112,15 +112,37 @@ def if_plan_partition(strategy: int, shape: StackShape, devices: int, stages: in
 
 
 # ---- communicator -------------------------------------------------------------
+def if_comm_nccl_unique_id() -> bytes:
+    buf = (ctypes.c_uint8 * 128)()
+    _check(lib().if_comm_nccl_unique_id(buf), "if_comm_nccl_unique_id")
+    return bytes(buf)
+
+
 class Comm:
     """Peer-memory communicator (if_comm_*).  Handles are exchanged through
     torch.distributed.all_gather_object (plumbing only)."""
 
-    def __init__(self, plan: Plan, rank: int, max_tokens: int, hidden: int):
+    def __init__(self, plan: Plan, rank: int, max_tokens: int = 0, hidden: int = 0, nccl_id: bytes | None = None):
         self.h = ctypes.c_void_p()
+        self.plan = plan
+        if nccl_id is not None:
+            idb = (ctypes.c_uint8 * 128).from_buffer_copy(nccl_id)
+            _check(lib().if_comm_init(ctypes.byref(plan), rank, idb, ctypes.byref(self.h)), "if_comm_init")
+            self.kind = "nccl"
+            return
         _check(lib().if_comm_create(ctypes.byref(plan), rank, max_tokens, hidden, ctypes.byref(self.h)),
                "if_comm_create")
-        self.plan = plan
+        self.kind = "peer"
+
+    @classmethod
+    def nccl(cls, plan: Plan, rank: int, group=None):
+        """NCCL communicator (if_comm_init); rank 0's unique id is broadcast with
+        torch.distributed (plumbing only)."""
+        import torch.distributed as dist
+        obj = [if_comm_nccl_unique_id() if rank == 0 else None]
+        if dist.is_initialized() and dist.get_world_size(group) > 1:
+            dist.broadcast_object_list(obj, src=0, group=group)
+        return cls(plan, rank, nccl_id=obj[0])
 
     def ipc_handle(self) -> bytes:
         buf = (ctypes.c_uint8 * 64)()
@@ -133,6 +155,8 @@ class Comm:
         _check(lib().if_comm_open_peers(self.h, buf), "if_comm_open_peers")
 
     def exchange(self, group=None):
+        if self.kind == "nccl":  # NCCL set itself up in if_comm_init
+            return
         import torch.distributed as dist
         hs = [None] * dist.get_world_size(group)
         dist.all_gather_object(hs, self.ipc_handle(), group=group)

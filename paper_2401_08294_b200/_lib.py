@@ -49,6 +49,8 @@ _SIGS = {
     "if_qgemv_acc": (i32, [Scheme, vp, i64, i64, vp, i64, vp, vp]),
     "if_qgemm": (i32, [Scheme, vp, i64, i64, vp, i64, vp, vp]),
     "if_plan_partition": (i32, [i32, vp, i32, i32, i32, vp]),
+    "if_comm_nccl_unique_id": (i32, [vp]),
+    "if_comm_init": (i32, [vp, i32, vp, vp]),
     "if_comm_create": (i32, [vp, i32, i64, i32, vp]),
     "if_comm_ipc_handle": (i32, [vp, vp]),
     "if_comm_open_peers": (i32, [vp, vp]),

@@ -18,6 +18,14 @@
 //
 // Each kernel runs a small grid (<= 32 CTAs, all co-resident) and uses an
 // in-mailbox arrival counter as the grid barrier between phases.
+//
+// NCCL mode (if_comm_init, the library-collective baseline of SURVEY §8(b)): the same
+// calls map to ncclAllReduce on the TP group's communicator (ncclCommSplit by stage)
+// and ncclSend/ncclRecv on the world communicator.  NCCL is opened with dlopen at
+// if_comm_init time (no link dependency: a process that already loaded torch's
+// libnccl.so.2 reuses it).
+#include <dlfcn.h>
+#include <nccl.h>
 #include <stdlib.h>
 #include <string.h>
 
@@ -42,6 +50,8 @@ static constexpr size_t kHdr = 256;
 }  // namespace ifb
 
 struct if_comm_s {
+  int kind = 0;  // 0 = peer memory (CUDA IPC), 1 = NCCL
+  ncclComm_t world = nullptr, group_comm = nullptr;
   if_plan plan;
   int rank, stage, group_rank;
   int64_t max_elems;
@@ -174,6 +184,48 @@ __global__ void __launch_bounds__(256) recv_kernel(P2PArgs a, float* __restrict_
   }
 }
 
+// ---- NCCL (dlopen'ed) ---------------------------------------------------------
+struct NcclApi {
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*);
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int);
+  ncclResult_t (*CommSplit)(ncclComm_t, int, int, ncclComm_t*, ncclConfig_t*);
+  ncclResult_t (*CommDestroy)(ncclComm_t);
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t);
+  ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t);
+  ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t);
+  const char* (*GetErrorString)(ncclResult_t);
+  bool ok = false;
+};
+static NcclApi* nccl() {
+  static NcclApi api;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (h) {
+#define IFB_SYM(f) *reinterpret_cast<void**>(&api.f) = dlsym(h, "nccl" #f)
+      IFB_SYM(GetUniqueId); IFB_SYM(CommInitRank); IFB_SYM(CommSplit); IFB_SYM(CommDestroy);
+      IFB_SYM(AllReduce); IFB_SYM(Send); IFB_SYM(Recv); IFB_SYM(GetErrorString);
+#undef IFB_SYM
+      api.ok = api.GetUniqueId && api.CommInitRank && api.CommSplit && api.CommDestroy && api.AllReduce && api.Send &&
+               api.Recv && api.GetErrorString;
+    }
+  }
+  return api.ok ? &api : nullptr;
+}
+static if_status nccl_check(ncclResult_t r, const char* what) {
+  if (r == ncclSuccess) return IF_OK;
+  NcclApi* a = nccl();
+  return set_error(IF_ERR_COMM, "%s: NCCL: %s", what, a ? a->GetErrorString(r) : "?");
+}
+
+// dst[i] += src[i]  (the NCCL path's accumulate: the stack's residual add after a merge)
+__global__ void __launch_bounds__(256) add_into_kernel(const float* __restrict__ src, float* __restrict__ dst, int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] += src[i];
+}
+
 static int comm_grid(int64_t n) {
   int64_t g = (n + 2047) / 2048;
   if (g < 1) g = 1;
@@ -183,6 +235,19 @@ static int comm_grid(int64_t n) {
 
 if_status comm_allreduce_into(if_comm c, const float* src, float* dst, int64_t n, int accumulate, cudaStream_t st) {
   if (!c) return set_error(IF_ERR_ARG, "allreduce: null comm");
+  if (c->kind == 1) {
+    // NCCL: sum in place over the TP group (src is the caller's partial buffer), then
+    // add into dst when accumulating (reduction order is NCCL's, Q21)
+    float* buf = accumulate ? const_cast<float*>(src) : dst;
+    if_status r = nccl_check(nccl()->AllReduce(src, buf, (size_t)n, ncclFloat32, ncclSum, c->group_comm, st),
+                             "allreduce");
+    if (r) return r;
+    if (accumulate) {
+      add_into_kernel<<<comm_grid(n), 256, 0, st>>>(buf, dst, n);
+      count_launch();
+    }
+    return check_launch("allreduce");
+  }
   if (n > c->max_elems) return set_error(IF_ERR_SHAPE, "allreduce: n=%lld > capacity %lld", (long long)n, (long long)c->max_elems);
   ARArgs a;
   a.box = c->box;
@@ -199,6 +264,7 @@ if_status comm_allreduce_into(if_comm c, const float* src, float* dst, int64_t n
 
 if_status comm_send(if_comm c, const float* src, int64_t n, cudaStream_t st) {
   if (!c || c->next < 0) return set_error(IF_ERR_ARG, "send: no next stage");
+  if (c->kind == 1) return nccl_check(nccl()->Send(src, (size_t)n, ncclFloat32, c->next, c->world, st), "send");
   if (n > c->max_elems) return set_error(IF_ERR_SHAPE, "send: n too large");
   if (!c->peer[c->next]) return set_error(IF_ERR_COMM, "send: peer not opened");
   P2PArgs a{c->box, c->peer[c->next], c->max_elems};
@@ -209,6 +275,7 @@ if_status comm_send(if_comm c, const float* src, int64_t n, cudaStream_t st) {
 
 if_status comm_recv(if_comm c, float* dst, int64_t n, cudaStream_t st) {
   if (!c || c->prev < 0) return set_error(IF_ERR_ARG, "recv: no previous stage");
+  if (c->kind == 1) return nccl_check(nccl()->Recv(dst, (size_t)n, ncclFloat32, c->prev, c->world, st), "recv");
   if (n > c->max_elems) return set_error(IF_ERR_SHAPE, "recv: n too large");
   if (!c->peer[c->prev]) return set_error(IF_ERR_COMM, "recv: peer not opened");
   P2PArgs a{c->box, c->peer[c->prev], c->max_elems};
@@ -223,16 +290,11 @@ int comm_group_size(if_comm c) { return c ? c->ngroup : 1; }
 
 using namespace ifb;
 
-extern "C" if_status if_comm_create(const if_plan* plan, int32_t rank, int64_t max_tokens, int32_t hidden, if_comm* out) {
-  if (!plan || !out) return set_error(IF_ERR_ARG, "if_comm_create: null pointer");
-  if (rank < 0 || rank >= plan->devices) return set_error(IF_ERR_ARG, "if_comm_create: rank %d outside plan", rank);
-  if (max_tokens < 1 || hidden < 1) return set_error(IF_ERR_SHAPE, "if_comm_create: max_tokens/hidden");
-  if_comm c = new if_comm_s();
+static void comm_topology(if_comm c, const if_plan* plan, int rank) {
   c->plan = *plan;
   c->rank = rank;
   c->stage = plan->a[rank].stage;
   c->group_rank = plan->a[rank].group_rank;
-  c->max_elems = max_tokens * (int64_t)hidden;
   for (int d = 0; d < plan->devices; d++)
     if (plan->a[d].stage == c->stage) c->group[plan->a[d].group_rank] = d;
   c->ngroup = plan->groups;
@@ -243,6 +305,15 @@ extern "C" if_status if_comm_create(const if_plan* plan, int32_t rank, int64_t m
     c->next = ((c->stage + 1) % plan->stages) * plan->groups + c->group_rank;
     c->prev = ((c->stage + plan->stages - 1) % plan->stages) * plan->groups + c->group_rank;
   }
+}
+
+extern "C" if_status if_comm_create(const if_plan* plan, int32_t rank, int64_t max_tokens, int32_t hidden, if_comm* out) {
+  if (!plan || !out) return set_error(IF_ERR_ARG, "if_comm_create: null pointer");
+  if (rank < 0 || rank >= plan->devices) return set_error(IF_ERR_ARG, "if_comm_create: rank %d outside plan", rank);
+  if (max_tokens < 1 || hidden < 1) return set_error(IF_ERR_SHAPE, "if_comm_create: max_tokens/hidden");
+  if_comm c = new if_comm_s();
+  comm_topology(c, plan, rank);
+  c->max_elems = max_tokens * (int64_t)hidden;
   const size_t bytes = kHdr + (size_t)4 * c->max_elems * sizeof(float);
   if (cudaMalloc(&c->box, bytes) != cudaSuccess || cudaMemset(c->box, 0, bytes) != cudaSuccess ||
       cudaDeviceSynchronize() != cudaSuccess) {
@@ -254,8 +325,42 @@ extern "C" if_status if_comm_create(const if_plan* plan, int32_t rank, int64_t m
   return IF_OK;
 }
 
+extern "C" if_status if_comm_nccl_unique_id(uint8_t* id128) {
+  if (!id128) return set_error(IF_ERR_ARG, "if_comm_nccl_unique_id: null pointer");
+  NcclApi* a = nccl();
+  if (!a) return set_error(IF_ERR_COMM, "if_comm_nccl_unique_id: libnccl.so.2 not loadable");
+  ncclUniqueId id;
+  if_status r = nccl_check(a->GetUniqueId(&id), "ncclGetUniqueId");
+  if (r) return r;
+  static_assert(sizeof(id) == 128, "nccl unique id size");
+  memcpy(id128, &id, 128);
+  return IF_OK;
+}
+
+extern "C" if_status if_comm_init(const if_plan* plan, int32_t rank, const uint8_t* nccl_unique_id, if_comm* out) {
+  if (!plan || !out || !nccl_unique_id) return set_error(IF_ERR_ARG, "if_comm_init: null pointer");
+  if (rank < 0 || rank >= plan->devices) return set_error(IF_ERR_ARG, "if_comm_init: rank %d outside plan", rank);
+  NcclApi* a = nccl();
+  if (!a) return set_error(IF_ERR_COMM, "if_comm_init: libnccl.so.2 not loadable");
+  if_comm c = new if_comm_s();
+  c->kind = 1;
+  comm_topology(c, plan, rank);
+  ncclUniqueId id;
+  memcpy(&id, nccl_unique_id, 128);
+  if_status r = nccl_check(a->CommInitRank(&c->world, plan->devices, id, rank), "ncclCommInitRank");
+  if (!r) r = nccl_check(a->CommSplit(c->world, c->stage, c->group_rank, &c->group_comm, nullptr), "ncclCommSplit");
+  if (r) {
+    if (c->world) a->CommDestroy(c->world);
+    delete c;
+    return r;
+  }
+  *out = c;
+  return IF_OK;
+}
+
 extern "C" if_status if_comm_ipc_handle(if_comm c, uint8_t* handle64) {
   if (!c || !handle64) return set_error(IF_ERR_ARG, "if_comm_ipc_handle: null pointer");
+  if (c->kind != 0) return set_error(IF_ERR_ARG, "if_comm_ipc_handle: not a peer-memory communicator");
   cudaIpcMemHandle_t h;
   if (cudaIpcGetMemHandle(&h, c->box) != cudaSuccess) return check_launch("if_comm_ipc_handle");
   static_assert(sizeof(h) == 64, "ipc handle size");
@@ -265,6 +370,7 @@ extern "C" if_status if_comm_ipc_handle(if_comm c, uint8_t* handle64) {
 
 extern "C" if_status if_comm_open_peers(if_comm c, const uint8_t* handles) {
   if (!c || !handles) return set_error(IF_ERR_ARG, "if_comm_open_peers: null pointer");
+  if (c->kind != 0) return set_error(IF_ERR_ARG, "if_comm_open_peers: not a peer-memory communicator");
   // only the ranks we talk to: my TP group and my pipeline neighbours
   for (int d = 0; d < c->plan.devices; d++) {
     bool need = (c->plan.a[d].stage == c->stage) || d == c->next || d == c->prev;
@@ -283,6 +389,12 @@ extern "C" if_status if_comm_open_peers(if_comm c, const uint8_t* handles) {
 extern "C" if_status if_comm_destroy(if_comm c) {
   if (!c) return IF_OK;
   cudaDeviceSynchronize();
+  if (c->kind == 1) {
+    if (c->group_comm) nccl()->CommDestroy(c->group_comm);
+    if (c->world) nccl()->CommDestroy(c->world);
+    delete c;
+    return IF_OK;
+  }
   for (int d = 0; d < 8; d++)
     if (c->opened[d]) cudaIpcCloseMemHandle(c->peer[d]);
   if (c->box) cudaFree(c->box);

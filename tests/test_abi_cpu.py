@@ -143,3 +143,9 @@ def test_plan_rejects_head_ranges_off_block_boundaries():
         F.if_plan_partition(F.IF_BY_TENSOR, shape, 2)
     assert e.value.status == 6
     F.if_plan_partition(F.IF_BY_TENSOR, shape, 3)  # 4 heads x 80 = 320 = 5 blocks: accepted
+
+
+def test_nccl_unique_id_through_abi():
+    """if_comm_nccl_unique_id (NCCL dlopen'ed by the library): 128 bytes, fresh each call."""
+    a, b = F.if_comm_nccl_unique_id(), F.if_comm_nccl_unique_id()
+    assert len(a) == 128 and len(b) == 128 and a != b

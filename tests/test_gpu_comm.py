@@ -173,3 +173,42 @@ def test_stack_hybrid_2x2_four_ranks_batch1():
     out = _run("hybrid1", world=4, timeout=360)
     for r in (2, 3):
         assert out[r]["err"] <= 1e-3, out
+
+
+def test_nccl_communicator_single_rank_in_graph():
+    """if_comm_init (NCCL baseline): a 1-rank plan; all-reduce is the identity and is
+    captured and replayed inside a CUDA graph; a 1-rank stack with the NCCL comm
+    equals the comm-less run bit for bit."""
+    import paper_2401_08294_b200 as F
+    import synth
+    from paper_2401_08294_b200.model import Stack
+    dev = torch.device("cuda:0")
+    torch.cuda.set_device(dev)
+    cfg = dict(layers=2, hidden=512, heads=8, kv_heads=2, head_dim=64, ffn=1408)
+    s = F.scheme(35, 64)
+    shape = F.stack_shape(*[cfg[k] for k in ("layers", "hidden", "heads", "kv_heads", "head_dim", "ffn")], s)
+    plan = F.if_plan_partition(F.IF_BY_TENSOR, shape, 1)
+    comm = F.Comm(plan, 0, nccl_id=F.if_comm_nccl_unique_id())
+    buf = torch.arange(4096, dtype=torch.float32, device=dev)
+    st = torch.cuda.Stream()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(st):
+        comm.allreduce(buf, st)
+        torch.cuda.synchronize()
+        with torch.cuda.graph(g, stream=st):
+            comm.allreduce(buf, st)
+    for _ in range(3):
+        g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(buf.cpu(), torch.arange(4096, dtype=torch.float32))
+    stk = Stack(cfg, s, plan, 0, dev)
+    h = torch.from_numpy(synth.activations(3, cfg["hidden"])).to(dev)
+    outs = []
+    for c in (None, comm):
+        out = torch.empty_like(h)
+        ws = torch.zeros(F.if_stack_workspace_bytes(shape, plan, 0, 3, F.IF_DECODE), dtype=torch.uint8, device=dev)
+        F.if_run_stack(shape, plan, 0, c, stk.arr, h, 3, F.IF_DECODE, out, None, ws)
+        torch.cuda.synchronize()
+        outs.append(out.cpu())
+    assert torch.equal(outs[0], outs[1])
+    comm.destroy()
