@@ -481,8 +481,8 @@ __global__ void __launch_bounds__(MK_THREADS, 1) decode_mk_kernel(const __grid_c
       const uint32_t par = ver & 1u;
       // 1. one thread waits until every CTA has finished the previous phase (a
       //    relaxed counter: no fence on either side -- the data carries its own
-      //    readiness) and copies the whole image (all 16 quad rows, padding
-      //    blocks included: never written, zero) into xs with the TMA engine
+      //    readiness); IFB_MK_POLL: no counter, every thread polls its own words
+#ifndef IFB_MK_POLL
       if (ct == 0) {
         SpinGuard sg;
         const uint32_t target = (ep + 1u) * (uint32_t)G;
@@ -491,24 +491,29 @@ __global__ void __launch_bounds__(MK_THREADS, 1) decode_mk_kernel(const __grid_c
           __nanosleep(20);
           sg.tick();
         }
-        if (dbg) { dbg[1] = gtimer(); dbg[9] = clock64(); }
-        const uint32_t row_bytes = (uint32_t)g.nbp * 16u;
-        const uint32_t ssq_bytes = rms ? (uint32_t)((G + 3) & ~3) * 4u : 0u;  // the Sigma h^2 partials ride along
-        mbar_arrive_expect_tx(xbar, 16u * row_bytes + ssq_bytes);
-        for (int jj = 0; jj < 16; jj++) bulk_g2s(xs + jj * xstride, img + jj * xstride, row_bytes, xbar, 0ull, false);
-        if (rms) bulk_g2s(ssq_s, P.ssq, ssq_bytes, xbar, 0ull, false);
       }
-      mbar_wait(xbar, xuse & 1);
-      xuse++;
-      // 2. the sum-h^2 partials (parity-checked like the image; fixed order: deterministic)
+      named_bar_sync(1, MK_CT);
+#endif
+      if (dbg && ct == 0) { dbg[1] = gtimer(); dbg[9] = clock64(); }
+      // 2. the sum-h^2 partials, read straight from L2 (ld.relaxed.gpu bypasses L1),
+      //    parity-checked like the image; fixed order: deterministic
       if (rms && cw == MK_NC - 1) {
+        // all loads in flight at once (G <= MK_MAXG = 5 x 32), then check / re-read
+        constexpr int NS = (MK_MAXG + 31) / 32;
+        uint32_t sv[NS];
+#pragma unroll
+        for (int i = 0; i < NS; i++)
+          sv[i] = lane + 32 * i < G ? ld_relaxed_u32(reinterpret_cast<const uint32_t*>(P.ssq) + lane + 32 * i) : par;
         float t = 0.f;
-        for (int c = lane; c < G; c += 32) {
-          uint32_t v = __float_as_uint(ssq_s[c]);
+#pragma unroll
+        for (int i = 0; i < NS; i++) {
+          const int c = lane + 32 * i;
+          uint32_t v = sv[i];
+          if (c >= G) continue;
           if ((v ^ par) & 1u) {
             SpinGuard sg;
             do {
-              __nanosleep(20);
+              __nanosleep(32);
               sg.tick();
               v = ld_relaxed_u32(reinterpret_cast<const uint32_t*>(P.ssq) + c);
             } while ((v ^ par) & 1u);
@@ -520,18 +525,19 @@ __global__ void __launch_bounds__(MK_THREADS, 1) decode_mk_kernel(const __grid_c
         if (lane == 0) red[16] = t;
       }
       if (dbg && ct == 0) { dbg[6] = gtimer(); dbg[14] = clock64(); }
-      // 3. four threads per block b, four quads each: check every word's parity
-      //    (re-read the rare late one from L2), strip it, and form the block sum
-      //    of x (x_e + x_o = xe' + 12 x_o in transformed terms)
+      // 3. four threads per block b, four quads each: load the image words straight
+      //    from L2 into registers (all loads of a thread in flight at once), check
+      //    every word's parity (re-read the late ones), strip it, stage the quads in
+      //    shared memory and form the block sum of x (x_e + x_o = xe' + 12 x_o in
+      //    transformed terms)
       for (int t0 = cw * 32; t0 < 4 * g.nbp; t0 += 2 * MK_CT) {
-        // two items per pass (K > 8192: 2 items per thread), all loads first
         float4 v[2][4];
 #pragma unroll
         for (int u = 0; u < 2; u++) {
           const int t = t0 + u * MK_CT + lane, b = t >> 2, j4 = t & 3;
 #pragma unroll
           for (int i = 0; i < 4; i++)
-            v[u][i] = b < g.nb ? xs[(4 * j4 + i) * xstride + b] : make_float4(0.f, 0.f, 0.f, 0.f);
+            v[u][i] = b < g.nb ? ld_relaxed_f4(img + (4 * j4 + i) * xstride + b) : make_float4(0.f, 0.f, 0.f, 0.f);
         }
 #pragma unroll
         for (int u = 0; u < 2; u++) {
@@ -547,6 +553,7 @@ __global__ void __launch_bounds__(MK_THREADS, 1) decode_mk_kernel(const __grid_c
                 SpinGuard sg;
                 do {
                   if (dbg) atomicAdd(reinterpret_cast<unsigned long long*>(dbg + 7), 1ull);
+                  __nanosleep(32);
                   sg.tick();
                   q = ld_relaxed_f4(img + jj * xstride + b);
                 } while (!par4_ok(q, par));
@@ -648,9 +655,32 @@ __global__ void __launch_bounds__(MK_THREADS, 1) decode_mk_kernel(const __grid_c
       const int U = gps * g.nchunk;                // units per slot
       const int inv_nc = (65536 + g.nchunk - 1) / g.nchunk;
       int u0 = cw;                                 // first unit of this warp in slot sl
+#ifdef IFB_MK_PROF
+      // instrumentation: ring slots of this phase already landed at stream start, and
+      // clocks warp 0 spends waiting for slots (-> dbg[15] = wait << 8 | occupancy)
+      unsigned long long pw = 0;
+      uint32_t occ = 0;
+      if (dbg && ct == 0) {
+        uint32_t s2 = slot, r2 = round;
+        for (int i = 0; i < nslots && i < nslot; i++) {
+          uint32_t ok;
+          asm volatile("{\n\t.reg .pred p;\n\tmbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+                       : "=r"(ok) : "r"(smem_u32(&full[s2])), "r"(r2 & 1) : "memory");
+          if (!ok) break;
+          occ++;
+          if (++s2 == (uint32_t)nslot) { s2 = 0; r2++; }
+        }
+      }
+#endif
       for (int sl = 0; sl < nslots; sl++) {
+#ifdef IFB_MK_PROF
+        const unsigned long long pw0 = clock64();
+#endif
 #ifndef IFB_MK_NOWAIT
         mbar_wait_sleep(&full[slot], round & 1);
+#endif
+#ifdef IFB_MK_PROF
+        pw += clock64() - pw0;
 #endif
         const int n = min(g.rps, nrows - sl * g.rps);
         const unsigned char* sbase = ring + (size_t)slot * MK_SLOT;
@@ -681,6 +711,9 @@ __global__ void __launch_bounds__(MK_THREADS, 1) decode_mk_kernel(const __grid_c
           round++;
         }
       }
+#ifdef IFB_MK_PROF
+      if (dbg && ct == 0) dbg[15] = (pw << 8) | occ;
+#endif
     }
     named_bar_sync(1, MK_CT);
     if (dbg && ct == 0) { dbg[4] = gtimer(); dbg[12] = clock64(); }
@@ -754,6 +787,9 @@ __global__ void __launch_bounds__(MK_THREADS, 1) decode_mk_kernel(const __grid_c
         }
         put_pair(P.xs_h, xstride, pos, g.r0 + rr, hn[0], hn[1], vh & 1u);
       }
+#ifndef IFB_MK_PROF
+      if (dbg && ct == 0) dbg[15] = clock64();  // epilogue rows done (before the sum-h^2 reduction)
+#endif
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
       if (lane == 0) red[cw] = ss;

@@ -74,3 +74,11 @@ for k in range(4):
     print(f"{kinds[k]:5s}" + "".join(f"{v:7.2f}" for v in a))
 tot = np.sum([np.sum(np.array(rows[k]), axis=0) for k in range(4)], axis=0)
 print("sum  " + "".join(f"{v:7.1f}" for v in tot))
+w = dbg.view(G, nph, 16)[:, :, 15].cpu().numpy().astype(np.uint64)
+if w.any():
+    occ = (w & np.uint64(255)).astype(np.float64)
+    wait = (w >> np.uint64(8)).astype(np.float64) / 1965.0
+    print("IFB_MK_PROF: kind  ring-slots-landed-at-start  warp0-slot-wait-us (medians)")
+    for k in range(4):
+        ps = [p for p in range(1, nph) if p % 4 == k]
+        print(f"  {kinds[k]:5s} {np.median(occ[:, ps]):5.1f} {np.median(wait[:, ps]):7.2f}")
