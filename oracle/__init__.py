@@ -77,6 +77,7 @@ def lib():
             L.ref_dequantize.argtypes = [i32, i32, vp, i64, i64, vp]
             L.ref_matmul_f64.argtypes = [i32, i32, vp, i64, i64, vp, i64, vp]
             L.ref_stack_f64.argtypes = [vp, vp, vp, vp, vp, vp, i64, vp, vp]
+            L.ref_stack_kv_f64.argtypes = [vp, vp, vp, vp, vp, vp, i64, vp, vp, i32, i32, vp, vp, vp, vp]
             L.ref_plan.argtypes = [i32] * 8 + [vp] * 10
             L.ref_stack_partitioned_f64.argtypes = [vp, i32, i32, i32, i32, vp, vp, vp, vp, vp, i64, vp]
             _lib = L
@@ -244,6 +245,41 @@ def stack_f64(shape: dict, wqkv, wo, wgu, wdown, h_in: np.ndarray, want_qkv: boo
     )
     _chk(st, "stack_f64")
     return h_out, qkv
+
+
+def stack_kv_f64(shape: dict, wqkv, wo, wgu, wdown, h_in: np.ndarray, slot_ids, positions,
+                 kcache: np.ndarray, vcache: np.ndarray):
+    """ref_stack_kv_f64: the stack with GQA decode attention over a KV cache (Q24).
+    kcache/vcache: fp64 [layers, slots, max_ctx, G, hd], updated in place (the
+    caller's per-sequence state).  Returns (h_out fp64 [T, d], last_qkv fp64 with
+    RoPE applied to q and k)."""
+    s = StackShape(**shape)
+    h_in = np.ascontiguousarray(h_in, dtype=np.float32)
+    if h_in.ndim == 1:
+        h_in = h_in[None, :]
+    T = h_in.shape[0]
+    slot_ids = np.ascontiguousarray(slot_ids, dtype=np.int32)
+    positions = np.ascontiguousarray(positions, dtype=np.int32)
+    assert kcache.dtype == np.float64 and kcache.flags.c_contiguous and vcache.shape == kcache.shape
+    assert vcache.dtype == np.float64 and vcache.flags.c_contiguous
+    L, slots, max_ctx = kcache.shape[:3]
+    nqkv = (shape["heads"] + 2 * shape["kv_heads"]) * shape["head_dim"]
+    h_out = np.zeros((T, shape["hidden"]), np.float64)
+    qkv = np.zeros((T, nqkv), np.float64)
+    P1, k1 = _ptr_array(wqkv)
+    P2, k2 = _ptr_array(wo)
+    P3, k3 = _ptr_array(wgu)
+    P4, k4 = _ptr_array(wdown)
+    st = lib().ref_stack_kv_f64(ctypes.addressof(s), P1, P2, P3, P4, _ptr(h_in), T, _ptr(slot_ids), _ptr(positions),
+                                slots, max_ctx, _ptr(kcache), _ptr(vcache), _ptr(h_out), _ptr(qkv))
+    _chk(st, "stack_kv_f64")
+    return h_out, qkv
+
+
+def kv_cache(shape: dict, slots: int, max_ctx: int):
+    """A fresh (zeroed) oracle KV cache pair for stack_kv_f64."""
+    dims = (shape["layers"], slots, max_ctx, shape["kv_heads"], shape["head_dim"])
+    return np.zeros(dims, np.float64), np.zeros(dims, np.float64)
 
 
 def stack_partitioned_f64(shape: dict, strategy: int, devices: int, stages: int, groups: int,

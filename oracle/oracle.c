@@ -14,7 +14,8 @@
  *                       floor(q/11), q mod 11
  *   two FP16 numbers per block, block sizes
  *   partition strategies (Table 4)
- * Readings where the paper is silent are numbered Q1..Q22 in DESIGN.md.
+ *   grouped-query attention over a KV cache with RoPE (Table 1)
+ * Readings where the paper is silent are numbered Q1..Q24 in DESIGN.md.
  *
  * Parity pins (tests/test_oracle_*.py): Table 2 codes/w'/averages, Table 3
  * bits/weight, exhaustive pair code, half-step bound, containment, brute-force
@@ -22,6 +23,9 @@
  * composition (ref_stack_f64, Q18) has no printed values in the paper:
  * "parity unpinned" by the paper; pinned only by special cases (zero weights
  * → identity, 1-layer hand composition, partition replay equivalence).
+ * ref_stack_kv_f64 (Q24) is pinned by tests/test_oracle_attention.py: position 0
+ * == ref_stack_f64 bitwise, RoPE rotation law, uniform keys -> mean of values,
+ * chunk == token-by-token, batching transparency.
  */
 #include "oracle.h"
 
@@ -423,6 +427,117 @@ int ref_stack_f64(const ref_stack_shape* s, const uint8_t* const* wqkv, const ui
   free(gu);
   free(act);
   free(dh);
+  return st;
+}
+
+/* ------------------------------------------------------------------------ */
+/* the stack with GQA decode attention over a KV cache (NEXT-1, Q24)          */
+/* ------------------------------------------------------------------------ */
+
+/* RoPE (Table 1): rotate consecutive pairs (2m, 2m+1) of one head
+ * vector by the angle pos * theta_m, theta_m = 10000^(-2m/hd) */
+static void rope_f64(double* x, int64_t hd, int64_t pos) {
+  for (int64_t m = 0; m < hd / 2; m++) {
+    double theta = pow(10000.0, -2.0 * (double)m / (double)hd);
+    double ang = (double)pos * theta;
+    double c = cos(ang), sn = sin(ang);
+    double x0 = x[2 * m], x1 = x[2 * m + 1];
+    x[2 * m] = x0 * c - x1 * sn;
+    x[2 * m + 1] = x0 * sn + x1 * c;
+  }
+}
+
+int ref_stack_kv_f64(const ref_stack_shape* s, const uint8_t* const* wqkv, const uint8_t* const* wo,
+                     const uint8_t* const* wgu, const uint8_t* const* wdown, const float* h_in, int64_t T,
+                     const int32_t* slot_ids, const int32_t* positions, int32_t slots, int32_t max_ctx,
+                     double* kcache, double* vcache, double* h_out, double* last_qkv) {
+  int st = check_shape(s);
+  if (st) return st;
+  if (s->head_dim % 2) return 2;
+  for (int64_t t = 0; t < T; t++)
+    if (slot_ids[t] < 0 || slot_ids[t] >= slots || positions[t] < 0 || positions[t] >= max_ctx) return 2;
+  const int64_t d = s->hidden, H = s->heads, G = s->kv_heads, hd = s->head_dim, F = s->ffn;
+  const int64_t nq = H * hd, nkv = G * hd, nqkv = nq + 2 * nkv;
+  const int64_t per_pos = G * hd, per_slot = (int64_t)max_ctx * per_pos, per_layer = (int64_t)slots * per_slot;
+  double* h = h_out;
+  for (int64_t i = 0; i < T * d; i++) h[i] = (double)h_in[i];
+  double* a = (double*)malloc(sizeof(double) * (size_t)(T * d));
+  double* qkv = (double*)malloc(sizeof(double) * (size_t)(T * nqkv));
+  double* ctx = (double*)malloc(sizeof(double) * (size_t)(T * nq));
+  double* gu = (double*)malloc(sizeof(double) * (size_t)(T * 2 * F));
+  double* act = (double*)malloc(sizeof(double) * (size_t)(T * F));
+  double* dh = (double*)malloc(sizeof(double) * (size_t)(T * d));
+  double* sc = (double*)malloc(sizeof(double) * (size_t)max_ctx);
+  for (int l = 0; l < s->layers && !st; l++) {
+    double* K = kcache + (int64_t)l * per_layer;
+    double* V = vcache + (int64_t)l * per_layer;
+    /* attention sub-layer: projections */
+    for (int64_t t = 0; t < T; t++) rmsnorm_f64(h + t * d, d, a + t * d);
+    st = matmul_rows_f64(s->qtype, s->block, wqkv[l], nqkv, d, a, T, qkv);
+    if (st) break;
+    /* RoPE on every q and k head at the token's position; append k, v to the cache */
+    for (int64_t t = 0; t < T; t++) {
+      double* q = qkv + t * nqkv;
+      for (int64_t i = 0; i < H; i++) rope_f64(q + i * hd, hd, positions[t]);
+      for (int64_t j = 0; j < G; j++) rope_f64(q + nq + j * hd, hd, positions[t]);
+      double* kd = K + slot_ids[t] * per_slot + (int64_t)positions[t] * per_pos;
+      double* vd = V + slot_ids[t] * per_slot + (int64_t)positions[t] * per_pos;
+      for (int64_t e = 0; e < nkv; e++) {
+        kd[e] = q[nq + e];
+        vd[e] = q[nq + nkv + e];
+      }
+    }
+    /* scaled dot-product attention of head i against kv group j = floor(i/(H/G)),
+     * causal over the slot's positions 0..p */
+    for (int64_t t = 0; t < T; t++) {
+      const int64_t p = positions[t];
+      const double* Ks = K + slot_ids[t] * per_slot;
+      const double* Vs = V + slot_ids[t] * per_slot;
+      for (int64_t i = 0; i < H; i++) {
+        const int64_t j = i / (H / G);
+        const double* q = qkv + t * nqkv + i * hd;
+        double mx = -INFINITY;
+        for (int64_t tau = 0; tau <= p; tau++) {
+          double dot = 0.0;
+          for (int64_t e = 0; e < hd; e++) dot += q[e] * Ks[tau * per_pos + j * hd + e];
+          sc[tau] = dot / sqrt((double)hd);
+          if (sc[tau] > mx) mx = sc[tau];
+        }
+        double den = 0.0;
+        for (int64_t tau = 0; tau <= p; tau++) {
+          sc[tau] = exp(sc[tau] - mx);
+          den += sc[tau];
+        }
+        for (int64_t e = 0; e < hd; e++) {
+          double acc = 0.0;
+          for (int64_t tau = 0; tau <= p; tau++) acc += sc[tau] * Vs[tau * per_pos + j * hd + e];
+          ctx[t * nq + i * hd + e] = acc / den;
+        }
+      }
+    }
+    st = matmul_rows_f64(s->qtype, s->block, wo[l], d, nq, ctx, T, dh);
+    if (st) break;
+    for (int64_t i = 0; i < T * d; i++) h[i] += dh[i];
+    /* feed-forward sub-layer (as ref_stack_f64) */
+    for (int64_t t = 0; t < T; t++) rmsnorm_f64(h + t * d, d, a + t * d);
+    st = matmul_rows_f64(s->qtype, s->block, wgu[l], 2 * F, d, a, T, gu);
+    if (st) break;
+    for (int64_t t = 0; t < T; t++)
+      for (int64_t f = 0; f < F; f++)
+        act[t * F + f] = silu_f64(gu[t * 2 * F + f]) * gu[t * 2 * F + F + f];
+    st = matmul_rows_f64(s->qtype, s->block, wdown[l], d, F, act, T, dh);
+    if (st) break;
+    for (int64_t i = 0; i < T * d; i++) h[i] += dh[i];
+    if (last_qkv && l == s->layers - 1)
+      memcpy(last_qkv, qkv, sizeof(double) * (size_t)(T * nqkv));
+  }
+  free(a);
+  free(qkv);
+  free(ctx);
+  free(gu);
+  free(act);
+  free(dh);
+  free(sc);
   return st;
 }
 

@@ -69,6 +69,21 @@ int ref_stack_f64(const ref_stack_shape* s, const uint8_t* const* wqkv, const ui
                   const uint8_t* const* wgu, const uint8_t* const* wdown,
                   const float* h_in, int64_t T, double* h_out, double* last_qkv);
 
+/* ---- the stack with decode attention over a KV cache (Q24) ----
+ * As ref_stack_f64, except the single-position stand-in is replaced by scaled
+ * dot-product grouped-query attention over a per-slot KV cache (P:332-337,
+ * P:341-347), with RoPE on q and k (Table 1 P:71 "position_embedding rope";
+ * S:343 consecutive pairs, theta_m = 10000^(-2m/hd)).  Token t of the batch has
+ * cache slot slot_ids[t] and position positions[t]; per layer all T tokens append
+ * their k, v first, then each attends causally to positions 0..positions[t] of its
+ * slot.  kcache/vcache: fp64 [layers][slots][max_ctx][G][hd], caller-owned state.
+ * Returns 2 for a slot or position out of range.  At positions[t] = 0 this equals
+ * ref_stack_f64 (softmax over one key; RoPE at position 0 is the identity). */
+int ref_stack_kv_f64(const ref_stack_shape* s, const uint8_t* const* wqkv, const uint8_t* const* wo,
+                     const uint8_t* const* wgu, const uint8_t* const* wdown, const float* h_in, int64_t T,
+                     const int32_t* slot_ids, const int32_t* positions, int32_t slots, int32_t max_ctx,
+                     double* kcache, double* vcache, double* h_out, double* last_qkv);
+
 /* ---- partition planner (Table 4; Q20) ----------------- */
 /* strategy: 0 by-layer, 1 by-tensor, 2 hybrid.  Output arrays have `devices`
  * entries, 0-based half-open ranges: layer [lb,le), head [hb,he), kv-head [kb,ke),
