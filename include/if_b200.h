@@ -259,6 +259,41 @@ if_status if_run_stack(const if_stack_shape* shape, const if_plan* plan, int32_t
                        int32_t mode, float* h_out, float* last_qkv, void* workspace,
                        if_stream_t stream);
 
+/* ---------------------------------------------------------------------------
+ * The stack with grouped-query decode attention over a KV cache (SURVEY NEXT-1,
+ * DESIGN.md Q24).  Same as if_run_stack, except the single-position stand-in
+ * (ctx_i = v of its kv group) is replaced by, per layer and token t:
+ *   q_i, k_j <- RoPE(., p_t): pair (2m, 2m+1) turned by p_t * 10000^(-2m/hd)
+ *                                          (Table 1 P:71 "rope")
+ *   K[slot_t][p_t] = k, V[slot_t][p_t] = v (every token of the call appends first)
+ *   ctx_i = sum_{tau <= p_t} softmax(q_i . K^j[tau] / sqrt(hd)) V^j[tau],
+ *           j = floor(i / (H/G))
+ * so a decode batch is T independent queries (T distinct slots) and a chunk of
+ * consecutive positions of one slot is causal prefill.  At p_t = 0 it equals
+ * if_run_stack.  last_qkv holds q and k after RoPE.
+ * kv: caller-owned device cache, fp32 k and v arrays of if_kv_cache_bytes() each,
+ *     layout [stage layers][slots][max_ctx][lkv][head_dim] (this rank's kv heads);
+ *     zero-filling is not needed (positions > p_t are never read).
+ * slot_ids, positions: DEVICE int32 [T] (graph replays may change them in place).
+ * An out-of-range slot or position writes IF_ERR_ARG to kv->status (nullable) and
+ * that token's context is zero; the call itself returns IF_OK.
+ * head_dim 64 or 128, heads per kv group <= 8.  Persistent-engine batches (Q3H_B64,
+ * T <= 6, one TP rank) take the per-layer path when a cache is given.
+ * ------------------------------------------------------------------------- */
+typedef struct {
+  float* k;
+  float* v;
+  int32_t slots, max_ctx;
+  int32_t* status; /* device, nullable */
+} if_kv_cache;
+
+if_status if_kv_cache_bytes(const if_stack_shape* shape, const if_plan* plan, int32_t rank, int32_t slots,
+                            int32_t max_ctx, size_t* bytes_each);
+if_status if_run_stack_kv(const if_stack_shape* shape, const if_plan* plan, int32_t rank, if_comm comm,
+                          const if_layer_weights* stage_layers, const float* h_in, int64_t T, int32_t mode,
+                          float* h_out, float* last_qkv, const if_kv_cache* kv, const int32_t* slot_ids,
+                          const int32_t* positions, void* workspace, if_stream_t stream);
+
 /* Thread-local message for the last non-OK status returned on this thread. */
 const char* if_last_error(void);
 

@@ -11,7 +11,7 @@ from __future__ import annotations
 import ctypes
 
 from . import _lib
-from ._lib import Assignment, LayerWeights, Plan, Scheme, StackShape
+from ._lib import Assignment, KvCache, LayerWeights, Plan, Scheme, StackShape
 
 QTYPES = {"Q2": 2, "Q3": 3, "Q3H": 35, "Q4": 4, "Q5": 5, "Q6": 6, "Q8": 8}
 IF_BY_LAYER, IF_BY_TENSOR, IF_HYBRID = 0, 1, 2
@@ -198,6 +198,33 @@ def if_run_stack(shape: StackShape, plan: Plan, rank: int, comm, layers_arr, h_i
     _check(lib().if_run_stack(ctypes.byref(shape), ctypes.byref(plan), rank, comm.h if comm else None, layers_arr,
                               _ptr(h_in), T, mode, _ptr(h_out), _ptr(last_qkv), _ptr(workspace), _stream(stream)),
            "if_run_stack")
+
+
+def if_kv_cache_bytes(shape: StackShape, plan: Plan, rank: int, slots: int, max_ctx: int) -> int:
+    n = ctypes.c_size_t()
+    _check(lib().if_kv_cache_bytes(ctypes.byref(shape), ctypes.byref(plan), rank, slots, max_ctx, ctypes.byref(n)),
+           "if_kv_cache_bytes")
+    return n.value
+
+
+class KV:
+    """A device KV cache (if_kv_cache): two fp32 torch tensors + an optional status word."""
+
+    def __init__(self, shape: StackShape, plan: Plan, rank: int, slots: int, max_ctx: int, device="cuda"):
+        import torch
+        n = if_kv_cache_bytes(shape, plan, rank, slots, max_ctx) // 4
+        self.k = torch.zeros(n, dtype=torch.float32, device=device)
+        self.v = torch.zeros(n, dtype=torch.float32, device=device)
+        self.status = torch.zeros(1, dtype=torch.int32, device=device)
+        self.c = KvCache(self.k.data_ptr(), self.v.data_ptr(), slots, max_ctx, self.status.data_ptr())
+
+
+def if_run_stack_kv(shape: StackShape, plan: Plan, rank: int, comm, layers_arr, h_in, T: int, mode: int, h_out,
+                    last_qkv, kv: "KV", slot_ids, positions, workspace, stream=None):
+    _check(lib().if_run_stack_kv(ctypes.byref(shape), ctypes.byref(plan), rank, comm.h if comm else None, layers_arr,
+                                 _ptr(h_in), T, mode, _ptr(h_out), _ptr(last_qkv), ctypes.byref(kv.c),
+                                 _ptr(slot_ids), _ptr(positions), _ptr(workspace), _stream(stream)),
+           "if_run_stack_kv")
 
 
 def if_launch_count(reset: bool = False) -> int:

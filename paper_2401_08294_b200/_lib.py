@@ -34,6 +34,10 @@ class Plan(ctypes.Structure):
     _fields_ = [("strategy", i32), ("devices", i32), ("stages", i32), ("groups", i32), ("a", Assignment * 8)]
 
 
+class KvCache(ctypes.Structure):
+    _fields_ = [("k", vp), ("v", vp), ("slots", i32), ("max_ctx", i32), ("status", vp)]
+
+
 class LayerWeights(ctypes.Structure):
     _fields_ = [("wqkv", vp), ("wo", vp), ("wgu", vp), ("wdown", vp)]
 
@@ -60,6 +64,8 @@ _SIGS = {
     "if_comm_recv_prev": (i32, [vp, vp, i64, vp]),
     "if_stack_workspace_bytes": (i32, [vp, vp, i32, i64, i32, vp]),
     "if_run_stack": (i32, [vp, vp, i32, vp, vp, vp, i64, i32, vp, vp, vp, vp]),
+    "if_kv_cache_bytes": (i32, [vp, vp, i32, i32, i32, vp]),
+    "if_run_stack_kv": (i32, [vp, vp, i32, vp, vp, vp, i64, i32, vp, vp, vp, vp, vp, vp, vp]),
     "if_last_error": (ctypes.c_char_p, []),
     "if_launch_count": (i64, [i32]),
 }

@@ -1,0 +1,36 @@
+// attn.cuh — internal interface of the KV-cache decode attention (attn.cu).
+#pragma once
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/if_b200.h"
+
+namespace ifb {
+
+constexpr int ATT_MAXSPLIT = 16;  // position splits per (token, kv group)
+
+struct AttnArgs {
+  float* qkv;  // [T, (lh + 2 lkv) hd] this rank's projections; q/k rotated in place
+  int64_t T;
+  int lh, lkv, hd;
+  const int32_t* slot_ids;  // device [T]
+  const int32_t* positions; // device [T]
+  float* k;                 // cache base, [layers][slots][max_ctx][lkv][hd]
+  float* v;
+  int slots, max_ctx, layer;
+  int32_t* status;          // nullable device status (IF_ERR_ARG on an out-of-range slot/position)
+  float* part;              // workspace [T][lh][ATT_MAXSPLIT][hd + 2]
+  float* ctx;               // nullable fp32 [T, lh hd]
+  __nv_bfloat16* ctx16;     // nullable bf16 [T, lh hd] (prefill)
+  __half* x2;               // nullable fp16 hi/lo split [2 bp, lh hd] (batched decode)
+  int bp;
+  float* x2sc;              // per-token 2^-k of the split
+  bool pdl;
+};
+
+if_status attn_run(const AttnArgs& a, cudaStream_t st);
+int attn_nsplit(int64_t T, int lkv, int max_ctx);
+
+}  // namespace ifb

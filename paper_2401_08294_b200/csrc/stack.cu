@@ -8,6 +8,7 @@
 
 #include <algorithm>
 
+#include "attn.cuh"
 #include "comm.cuh"
 #include "common.cuh"
 #include "decode_mk.cuh"
@@ -238,6 +239,7 @@ struct WS {
   float* gu;
   float* act;
   float* part;
+  float* attn;  // KV-cache attention partials [T][lh][ATT_MAXSPLIT][hd + 2]
   int* done;  // decode engine: phase counters [4 * MK_MAXL] + epoch
   float* xsimg;  // 3 transformed-input images + sum-h^2 partials (decode engine)
   void* x2;      // batched decode: fp16 hi/lo split of a qGEMV input (2 x 64 x maxK halves)
@@ -273,6 +275,7 @@ static WS carve(void* base, const Local& L, int64_t T) {
   w.gu = take((size_t)T * 2 * L.lf);
   w.act = take((size_t)T * L.lf);
   w.part = take((size_t)T * L.d);
+  w.attn = take((size_t)T * L.lh * ATT_MAXSPLIT * (L.hd + 2));
   w.bytes = off;
   return w;
 }
@@ -293,9 +296,18 @@ extern "C" if_status if_stack_workspace_bytes(const if_stack_shape* shape, const
   return IF_OK;
 }
 
-extern "C" if_status if_run_stack(const if_stack_shape* shape, const if_plan* plan, int32_t rank, if_comm comm,
-                                  const if_layer_weights* stage_layers, const float* h_in, int64_t T, int32_t mode,
-                                  float* h_out, float* last_qkv, void* workspace, if_stream_t stream) {
+struct KvRun;
+static AttnArgs attn_args(const Local& L, const KvRun* kvr, const WS& w, int64_t T, int nlayers, int l);
+
+struct KvRun {
+  const if_kv_cache* kv;
+  const int32_t* slot_ids;
+  const int32_t* positions;
+};
+
+static if_status run_stack(const if_stack_shape* shape, const if_plan* plan, int32_t rank, if_comm comm,
+                           const if_layer_weights* stage_layers, const float* h_in, int64_t T, int32_t mode,
+                           float* h_out, float* last_qkv, void* workspace, if_stream_t stream, const KvRun* kvr) {
   Local L;
   if_status st = local_dims(shape, plan, rank, &L);
   if (st) return st;
@@ -325,7 +337,7 @@ extern "C" if_status if_run_stack(const if_stack_shape* shape, const if_plan* pl
   // (batch 2..6: one engine launch per token beats the tensor-core path, whose
   //  per-launch cost dominates at small B; both stream the weights from HBM)
   const bool mk = mode == IF_DECODE && T <= 6 && sc.type == IF_Q3H && sc.block == 64 && groups == 1 &&
-                  nlayers <= MK_MAXL && nlayers > 0;
+                  nlayers <= MK_MAXL && nlayers > 0 && !kvr;
   if (mk) {
     static thread_local MkParams P;
     P.mode = MK_MODE_STACK;
@@ -394,7 +406,17 @@ extern "C" if_status if_run_stack(const if_stack_shape* shape, const if_plan* pl
       count_launch();
       if ((st = qgemv_dispatch("if_run_stack(qkv)", sc, Wl.wqkv, L.nqkv, L.d, w.a, T, w.qkv, 1, cs, w.x2, w.x2_bytes, x2r)))
         return st;
-      if (use_x2)
+      if (kvr) {
+        // GQA attention over the KV cache (attn.cu, NEXT-1): RoPE + append, split
+        // partials, combine -> ctx (and its fp16 split for the batched qGEMV)
+        AttnArgs aa = attn_args(L, kvr, w, T, nlayers, l);
+        aa.ctx = w.ctx;
+        aa.x2 = x2h;
+        aa.bp = bpx;
+        aa.x2sc = x2s;
+        aa.pdl = true;
+        if ((st = attn_run(aa, cs))) return st;
+      } else if (use_x2)
         launch_pdl(vbcast_x2_kernel, (unsigned)bpx, 256, cs, (const float*)w.qkv, w.ctx, (int)T, (int)L.lh, (int)L.lkv,
                    (int)L.hd, (int)asg.head_begin, (int)asg.kv_begin, (int)per, x2h, bpx, x2s);
       else
@@ -438,9 +460,15 @@ extern "C" if_status if_run_stack(const if_stack_shape* shape, const if_plan* pl
       count_launch();
       if ((st = qgemm_impl("if_run_stack(qkv)", sc, Wl.wqkv, L.nqkv, L.d, reinterpret_cast<uint16_t*>(a16), T, w.qkv, 0, cs)))
         return st;
-      vbcast_kernel<__nv_bfloat16><<<ew_grid(T * L.nq), 256, 0, cs>>>(w.qkv, c16, (int)T, L.lh, L.lkv, L.hd,
-                                                                     asg.head_begin, asg.kv_begin, per);
-      count_launch();
+      if (kvr) {  // causal attention of the chunk over the cache (all tokens append first)
+        AttnArgs aa = attn_args(L, kvr, w, T, nlayers, l);
+        aa.ctx16 = c16;
+        if ((st = attn_run(aa, cs))) return st;
+      } else {
+        vbcast_kernel<__nv_bfloat16><<<ew_grid(T * L.nq), 256, 0, cs>>>(w.qkv, c16, (int)T, L.lh, L.lkv, L.hd,
+                                                                       asg.head_begin, asg.kv_begin, per);
+        count_launch();
+      }
       if (groups == 1) {
         if ((st = qgemm_impl("if_run_stack(o)", sc, Wl.wo, L.d, L.nq, reinterpret_cast<uint16_t*>(c16), T, h_out, 1, cs)))
           return st;
@@ -473,4 +501,51 @@ extern "C" if_status if_run_stack(const if_stack_shape* shape, const if_plan* pl
     if ((st = comm_send(comm, h_out, nh, cs))) return st;
   }
   return check_launch("if_run_stack");
+}
+
+static AttnArgs attn_args(const Local& L, const KvRun* kvr, const WS& w, int64_t T, int nlayers, int l) {
+  (void)nlayers;
+  AttnArgs a = {};
+  a.qkv = w.qkv;
+  a.T = T;
+  a.lh = L.lh;
+  a.lkv = L.lkv;
+  a.hd = L.hd;
+  a.slot_ids = kvr->slot_ids;
+  a.positions = kvr->positions;
+  a.k = kvr->kv->k;
+  a.v = kvr->kv->v;
+  a.slots = kvr->kv->slots;
+  a.max_ctx = kvr->kv->max_ctx;
+  a.layer = l;
+  a.status = kvr->kv->status;
+  a.part = w.attn;
+  return a;
+}
+
+extern "C" if_status if_run_stack(const if_stack_shape* shape, const if_plan* plan, int32_t rank, if_comm comm,
+                                  const if_layer_weights* stage_layers, const float* h_in, int64_t T, int32_t mode,
+                                  float* h_out, float* last_qkv, void* workspace, if_stream_t stream) {
+  return run_stack(shape, plan, rank, comm, stage_layers, h_in, T, mode, h_out, last_qkv, workspace, stream, nullptr);
+}
+
+extern "C" if_status if_kv_cache_bytes(const if_stack_shape* shape, const if_plan* plan, int32_t rank, int32_t slots,
+                                       int32_t max_ctx, size_t* bytes_each) {
+  Local L;
+  if_status st = local_dims(shape, plan, rank, &L);
+  if (st) return st;
+  if (!bytes_each || slots < 1 || max_ctx < 1) return set_error(IF_ERR_ARG, "if_kv_cache_bytes: slots/max_ctx/null");
+  *bytes_each = (size_t)L.layers * slots * max_ctx * L.lkv * L.hd * sizeof(float);
+  return IF_OK;
+}
+
+extern "C" if_status if_run_stack_kv(const if_stack_shape* shape, const if_plan* plan, int32_t rank, if_comm comm,
+                                     const if_layer_weights* stage_layers, const float* h_in, int64_t T, int32_t mode,
+                                     float* h_out, float* last_qkv, const if_kv_cache* kv, const int32_t* slot_ids,
+                                     const int32_t* positions, void* workspace, if_stream_t stream) {
+  if (!kv || !kv->k || !kv->v || !slot_ids || !positions || kv->slots < 1 || kv->max_ctx < 1)
+    return set_error(IF_ERR_ARG, "if_run_stack_kv: null cache / slot ids / positions");
+  if (shape && shape->head_dim % 2) return set_error(IF_ERR_SHAPE, "if_run_stack_kv: RoPE needs an even head_dim");
+  const KvRun kvr = {kv, slot_ids, positions};
+  return run_stack(shape, plan, rank, comm, stage_layers, h_in, T, mode, h_out, last_qkv, workspace, stream, &kvr);
 }
