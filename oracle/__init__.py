@@ -79,6 +79,7 @@ def lib():
             L.ref_stack_f64.argtypes = [vp, vp, vp, vp, vp, vp, i64, vp, vp]
             L.ref_stack_kv_f64.argtypes = [vp, vp, vp, vp, vp, vp, i64, vp, vp, i32, i32, vp, vp, vp, vp]
             L.ref_plan.argtypes = [i32] * 8 + [vp] * 10
+            L.ref_spec_verify.argtypes = [i32, i32, vp, vp, vp, vp, ctypes.c_float, i32, i32, ctypes.c_float, vp, vp]
             L.ref_stack_partitioned_f64.argtypes = [vp, i32, i32, i32, i32, vp, vp, vp, vp, vp, i64, vp]
             _lib = L
     return _lib
@@ -274,6 +275,23 @@ def stack_kv_f64(shape: dict, wqkv, wo, wgu, wdown, h_in: np.ndarray, slot_ids, 
                                 slots, max_ctx, _ptr(kcache), _ptr(vcache), _ptr(h_out), _ptr(qkv))
     _chk(st, "stack_kv_f64")
     return h_out, qkv
+
+
+def spec_verify(tgt_logits: np.ndarray, draft_probs: np.ndarray, draft_tok, u_acc, u_smp: float,
+                is_top: bool = False, top_k: int = 0, top_p: float = 1.0):
+    """ref_spec_verify: one round of Algorithm 1 -> list of output tokens (accepted + 1)."""
+    tgt_logits = np.ascontiguousarray(tgt_logits, np.float32)
+    draft_probs = np.ascontiguousarray(draft_probs, np.float32)
+    K1, V = tgt_logits.shape
+    K = K1 - 1
+    draft_tok = np.ascontiguousarray(draft_tok, np.int32)
+    u_acc = np.ascontiguousarray(u_acc, np.float32)
+    out = np.zeros(K + 1, np.int32)
+    n = np.zeros(1, np.int32)
+    _chk(lib().ref_spec_verify(K, V, _ptr(tgt_logits), _ptr(draft_probs), _ptr(draft_tok), _ptr(u_acc),
+                               float(u_smp), int(is_top), int(top_k), float(top_p), _ptr(out), _ptr(n)),
+         "spec_verify")
+    return out[:n[0]].tolist()
 
 
 def kv_cache(shape: dict, slots: int, max_ctx: int):

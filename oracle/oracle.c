@@ -542,6 +542,90 @@ int ref_stack_kv_f64(const ref_stack_shape* s, const uint8_t* const* wqkv, const
 }
 
 /* ------------------------------------------------------------------------ */
+/* speculative sampling: one verification round of Algorithm 1     */
+/* ------------------------------------------------------------------------ */
+
+/* q = softmax(logits) in fp64 (temperature 1) */
+static void softmax_f64(const float* logits, int V, double* q) {
+  double mx = -INFINITY, sum = 0.0;
+  for (int i = 0; i < V; i++)
+    if ((double)logits[i] > mx) mx = (double)logits[i];
+  for (int i = 0; i < V; i++) {
+    q[i] = exp((double)logits[i] - mx);
+    sum += q[i];
+  }
+  for (int i = 0; i < V; i++) q[i] /= sum;
+}
+
+/* smallest index whose running sum (index order) exceeds u * total; -1 if total == 0 */
+static int sample_index(const double* w, int V, double u) {
+  double total = 0.0;
+  for (int i = 0; i < V; i++) total += w[i];
+  if (!(total > 0.0)) return -1;
+  double target = u * total, run = 0.0;
+  for (int i = 0; i < V; i++) {
+    run += w[i];
+    if (run > target) return i;
+  }
+  for (int i = V - 1; i >= 0; i--)
+    if (w[i] > 0.0) return i; /* u -> 1 rounding: the last token with weight */
+  return -1;
+}
+
+/* "the draft token is present in the top-k / top-p pools": fewer than k tokens
+ * are strictly more probable, and the mass strictly more probable is below top_p */
+static int in_pool(const double* q, int V, int x, int top_k, double top_p) {
+  int more = 0;
+  double mass = 0.0;
+  for (int i = 0; i < V; i++)
+    if (q[i] > q[x]) {
+      more++;
+      mass += q[i];
+    }
+  if (top_k > 0 && more >= top_k) return 0;
+  if (top_p < 1.0 && mass >= top_p) return 0;
+  return top_k > 0 || top_p < 1.0;
+}
+
+int ref_spec_verify(int K, int V, const float* tgt_logits, const float* draft_probs, const int32_t* draft_tok,
+                    const float* u_acc, float u_smp, int is_top, int top_k, float top_p, int32_t* out_tok,
+                    int32_t* n_out) {
+  if (K < 0 || V < 1) return 2;
+  for (int t = 0; t < K; t++)
+    if (draft_tok[t] < 0 || draft_tok[t] >= V) return 2;
+  double* q = (double*)malloc(sizeof(double) * (size_t)V);
+  double* r = (double*)malloc(sizeof(double) * (size_t)V);
+  int n = 0;
+  for (int t = 0; t < K; t++) {
+    softmax_f64(tgt_logits + (int64_t)t * V, V, q);
+    const float* p = draft_probs + (int64_t)t * V;
+    const int x = draft_tok[t];
+    double ratio = (double)p[x] > 0.0 ? q[x] / (double)p[x] : 1.0;
+    if (ratio > 1.0) ratio = 1.0;
+    if ((is_top && in_pool(q, V, x, top_k, (double)top_p)) || (double)u_acc[t] < ratio) {
+      out_tok[n++] = x; /* x_{n+t} <- draft, n <- n+1 */
+      continue;
+    }
+    /* reject: sample x_{n+t} ~ (q - p)_+ and exit the loop */
+    for (int i = 0; i < V; i++) r[i] = q[i] - (double)p[i] > 0.0 ? q[i] - (double)p[i] : 0.0;
+    int y = sample_index(r, V, (double)u_smp);
+    if (y < 0) y = sample_index(q, V, (double)u_smp);
+    out_tok[n++] = y;
+    *n_out = n;
+    free(q);
+    free(r);
+    return 0;
+  }
+  /* all K accepted: one extra token from the target at position K */
+  softmax_f64(tgt_logits + (int64_t)K * V, V, q);
+  out_tok[n++] = sample_index(q, V, (double)u_smp);
+  *n_out = n;
+  free(q);
+  free(r);
+  return 0;
+}
+
+/* ------------------------------------------------------------------------ */
 /* partition planner (Table 4; Q20)           */
 /* ------------------------------------------------------------------------ */
 

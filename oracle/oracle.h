@@ -84,6 +84,21 @@ int ref_stack_kv_f64(const ref_stack_shape* s, const uint8_t* const* wqkv, const
                      const int32_t* slot_ids, const int32_t* positions, int32_t slots, int32_t max_ctx,
                      double* kcache, double* vcache, double* h_out, double* last_qkv);
 
+/* ---- speculative sampling, one verification round (Algorithm 1, P:351-384;
+ * SURVEY NEXT-3; readings Q25/Q26) ------------------------------------------
+ * Algorithm 1's own notation: the draft model p proposes draft_tok[0..K) with
+ * distributions draft_probs [K][V]; the target q is evaluated "in parallel" at the
+ * K+1 positions, tgt_logits [K+1][V] (q = softmax, temperature 1).  For t < K:
+ * accept draft t when (is_top and it lies in the target's top-k/top-p pool) or
+ * u_acc[t] < min(1, q(x)/p(x)); else sample from (q - p)_+ with u_smp and stop.
+ * All K accepted: sample an extra token from q at position K with u_smp.
+ * Sampling with a uniform u: the smallest index i whose running sum (index order)
+ * exceeds u * total.  top_k <= 0 / top_p >= 1 disable that pool.
+ * out_tok [K+1]; *n_out = accepted + 1.  Returns 2 on bad sizes or tokens. */
+int ref_spec_verify(int K, int V, const float* tgt_logits, const float* draft_probs, const int32_t* draft_tok,
+                    const float* u_acc, float u_smp, int is_top, int top_k, float top_p, int32_t* out_tok,
+                    int32_t* n_out);
+
 /* ---- partition planner (Table 4; Q20) ----------------- */
 /* strategy: 0 by-layer, 1 by-tensor, 2 hybrid.  Output arrays have `devices`
  * entries, 0-based half-open ranges: layer [lb,le), head [hb,he), kv-head [kb,ke),
