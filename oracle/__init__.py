@@ -81,6 +81,9 @@ def lib():
             L.ref_plan.argtypes = [i32] * 8 + [vp] * 10
             L.ref_spec_verify.argtypes = [i32, i32, vp, vp, vp, vp, ctypes.c_float, i32, i32, ctypes.c_float, vp, vp]
             L.ref_stack_partitioned_f64.argtypes = [vp, i32, i32, i32, i32, vp, vp, vp, vp, vp, i64, vp]
+            L.ref_lm_logits_f64.argtypes = [i32, i32, vp, i64, i64, vp, i64, vp]
+            L.ref_argmax_f64.argtypes = [vp, i64]
+            L.ref_argmax_f64.restype = i64
             _lib = L
     return _lib
 
@@ -292,6 +295,45 @@ def spec_verify(tgt_logits: np.ndarray, draft_probs: np.ndarray, draft_tok, u_ac
                                float(u_smp), int(is_top), int(top_k), float(top_p), _ptr(out), _ptr(n)),
          "spec_verify")
     return out[:n[0]].tolist()
+
+
+def lm_logits_f64(qtype: int, block: int, lm_packed: np.ndarray, V: int, d: int, h: np.ndarray) -> np.ndarray:
+    """ref_lm_logits_f64: final RMSNorm then the quantized output projection (Q27).
+    h [T, d] (any float dtype, taken exactly as fp64) -> logits fp64 [T, V]."""
+    h = np.ascontiguousarray(np.atleast_2d(h), np.float64)
+    T = h.shape[0]
+    out = np.zeros((T, V), np.float64)
+    _chk(lib().ref_lm_logits_f64(qtype, block, _ptr(np.ascontiguousarray(lm_packed, np.uint8)), V, d, _ptr(h), T,
+                                 _ptr(out)), "lm_logits_f64")
+    return out
+
+
+def argmax(x: np.ndarray) -> int:
+    """ref_argmax_f64: greedy choice, first index of the maximum."""
+    x = np.ascontiguousarray(x, np.float64)
+    return int(lib().ref_argmax_f64(_ptr(x), x.size))
+
+
+def lm_sequence_f64(shape: dict, wqkv, wo, wgu, wdown, embed: np.ndarray, lm_packed: np.ndarray, V: int,
+                    prompt, continuation, max_ctx: int):
+    """A sequential decode of one query with the plain pieces above (the "direct
+    engine loop without batcher" of S:567): embedding rows of the prompt as one causal
+    chunk at positions 0..n-1, then every continuation token one position at a time;
+    after each call the logits of the last row.  Returns fp64 [1 + len(continuation), V]:
+    row j is the target distribution's logits after prompt + continuation[:j]
+    (teacher forcing with the tokens the caller emitted)."""
+    K, Vc = kv_cache(shape, 1, max_ctx)
+    d = shape["hidden"]
+    qt, bs = shape["qtype"], shape["block"]
+    prompt = list(prompt)
+    rows = []
+    h, _ = stack_kv_f64(shape, wqkv, wo, wgu, wdown, embed[prompt], [0] * len(prompt), list(range(len(prompt))),
+                        K, Vc)
+    rows.append(lm_logits_f64(qt, bs, lm_packed, V, d, h[-1:])[0])
+    for j, tok in enumerate(continuation):
+        h, _ = stack_kv_f64(shape, wqkv, wo, wgu, wdown, embed[[tok]], [0], [len(prompt) + j], K, Vc)
+        rows.append(lm_logits_f64(qt, bs, lm_packed, V, d, h)[0])
+    return np.stack(rows)
 
 
 def kv_cache(shape: dict, slots: int, max_ctx: int):

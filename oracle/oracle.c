@@ -345,7 +345,7 @@ int ref_matmul_f64(int qtype, int block, const uint8_t* packed, int64_t N, int64
                    const float* X, int64_t M, double* Y) {
   if (!ref_scheme_valid(qtype, block)) return 3;
   if (N < 0 || K < 0 || M < 0 || K % block) return 2;
-  double* Xd = (double*)malloc(sizeof(double) * (size_t)(M * K ? M * K : 1));
+  double* Xd = (double*)malloc(sizeof(double) * (size_t)(M * K > 0 ? M * K : 1));
   for (int64_t i = 0; i < M * K; i++) Xd[i] = (double)X[i];
   int st = matmul_rows_f64(qtype, block, packed, N, K, Xd, M, Y);
   free(Xd);
@@ -623,6 +623,34 @@ int ref_spec_verify(int K, int V, const float* tgt_logits, const float* draft_pr
   free(q);
   free(r);
   return 0;
+}
+
+/* ------------------------------------------------------------------------ */
+/* language-model head: the step that turns the stack's output into the next  */
+/* token (NEXT-2 "a set of next tokens"; NEXT-3 target logits,     */
+/* P:362-365; reading Q27)                                                   */
+/* ------------------------------------------------------------------------ */
+
+/* logits[t, v] = sum_i W'_lm[v, i] * rms(h[t])_i: the final RMSNorm (unit gain,
+ * eps 1e-5) then the output projection, block-quantized like every other
+ * matrix (Eq. 2 dequantized in fp32, products and sums in fp64). */
+int ref_lm_logits_f64(int qtype, int block, const uint8_t* lm, int64_t V, int64_t d, const double* h, int64_t T,
+                      double* logits) {
+  if (!ref_scheme_valid(qtype, block)) return 3;
+  if (V < 1 || d < 1 || T < 0 || d % block) return 2;
+  double* a = (double*)malloc(sizeof(double) * (size_t)(T * d > 0 ? T * d : 1));
+  for (int64_t t = 0; t < T; t++) rmsnorm_f64(h + t * d, d, a + t * d);
+  int st = matmul_rows_f64(qtype, block, lm, V, d, a, T, logits);
+  free(a);
+  return st;
+}
+
+/* greedy decoding: the first index holding the largest value */
+int64_t ref_argmax_f64(const double* x, int64_t n) {
+  int64_t best = 0;
+  for (int64_t i = 1; i < n; i++)
+    if (x[i] > x[best]) best = i;
+  return n > 0 ? best : -1;
 }
 
 /* ------------------------------------------------------------------------ */

@@ -99,6 +99,14 @@ int ref_spec_verify(int K, int V, const float* tgt_logits, const float* draft_pr
                     const float* u_acc, float u_smp, int is_top, int top_k, float top_p, int32_t* out_tok,
                     int32_t* n_out);
 
+/* ---- language-model head (reading Q27) ---------------
+ * logits [T][V] = rms(h[t]) . W'_lm[v]  (final RMSNorm, unit gain, eps 1e-5; the
+ * output projection lm [V, d] block-quantized).  h fp64 [T][d]. */
+int ref_lm_logits_f64(int qtype, int block, const uint8_t* lm, int64_t V, int64_t d, const double* h, int64_t T,
+                      double* logits);
+/* greedy choice: first index of the maximum; -1 for n = 0 */
+int64_t ref_argmax_f64(const double* x, int64_t n);
+
 /* ---- partition planner (Table 4; Q20) ----------------- */
 /* strategy: 0 by-layer, 1 by-tensor, 2 hybrid.  Output arrays have `devices`
  * entries, 0-based half-open ranges: layer [lb,le), head [hb,he), kv-head [kb,ke),

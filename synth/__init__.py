@@ -74,6 +74,20 @@ def activations(T: int, d: int, tid: int = 0) -> np.ndarray:
     return matrix(SEED_ACTS, tid, 1.0, T, d)
 
 
+SEED_EMBED = 0x3F
+LM_TID = 7  # slot 7 of layer 0's tensor ids (8*l + 7 is unused by the layers)
+
+
+def embedding(V: int, d: int) -> np.ndarray:
+    """Token embedding table [V, d] fp32, sigma = 1 (the stack's input scale)."""
+    return matrix(SEED_EMBED, 0, 1.0, V, d)
+
+
+def lm_head(V: int, d: int) -> np.ndarray:
+    """Output projection [V, d] fp32, sigma = 1/sqrt(d) like every weight matrix."""
+    return matrix(SEED_WEIGHTS, LM_TID, 1.0 / math.sqrt(d), V, d)
+
+
 # Llama-2 shapes (BASELINE.json configs; SURVEY §8)
 LLAMA = {
     "7b": dict(layers=32, hidden=4096, heads=32, kv_heads=32, head_dim=128, ffn=11008),
