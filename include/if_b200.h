@@ -294,6 +294,95 @@ if_status if_run_stack_kv(const if_stack_shape* shape, const if_plan* plan, int3
                           float* h_out, float* last_qkv, const if_kv_cache* kv, const int32_t* slot_ids,
                           const int32_t* positions, void* workspace, if_stream_t stream);
 
+/* ---------------------------------------------------------------------------
+ * Language-model head (Q27): what turns the stack's output into "a set of
+ * next tokens" and gives the target logits of speculative decoding
+ * (Algorithm 1).  All pointers device, stream-ordered, graph capturable.
+ *
+ * if_embed:      h[t] = table[tokens[t]]   table fp32 [V, d] (16-B aligned, d % 4 == 0),
+ *                tokens int32 [T], h fp32 [T, d].  A token outside [0, V) writes
+ *                IF_ERR_ARG to dev_status (nullable) and a zero row.
+ * if_lm_logits:  logits[b] = rms(h[rows[b]]) . W'_lm^T   (final RMSNorm, unit gain,
+ *                eps 1e-5; then if_qgemv with B = T, 1 <= T <= 64: same
+ *                precision contract, 1e-3 normwise).  lm packed [V, d] in scheme s;
+ *                rows int32 [T] (nullable = 0..T-1) index h's rows; scratch fp32 [T, d].
+ * if_argmax:     tokens[t] = first index of the maximum of logits[t] (greedy).
+ * ------------------------------------------------------------------------- */
+if_status if_embed(const float* table, int32_t V, int32_t d, const int32_t* tokens, int64_t T, float* h,
+                   int32_t* dev_status, if_stream_t stream);
+if_status if_lm_logits(if_scheme s, const uint8_t* lm, int64_t V, int64_t d, const float* h, int64_t T,
+                       const int32_t* rows, float* logits, float* scratch, if_stream_t stream);
+if_status if_argmax(const float* logits, int64_t T, int64_t V, int32_t* tokens, if_stream_t stream);
+
+/* ---------------------------------------------------------------------------
+ * Speculative sampling, one verification round (Algorithm 1; SURVEY
+ * NEXT-3; readings Q25/Q26).  Algorithm 1's notation: the draft model p proposed
+ * draft_tok [K] with distributions draft_probs [K, V]; the target q was evaluated at
+ * the K+1 positions in parallel, tgt_logits [K+1, V] (q = softmax, temperature 1).
+ * For t < K: accept draft t when (is_top and it lies in q's top-k / top-p pool,
+ * fewer than top_k tokens, and less than top_p mass, strictly more
+ * probable) or u_acc[t] < min(1, q(x)/p(x)); else draw from (q - p)_+ with u_smp
+ * and stop.  All K accepted: draw an extra token from q at position K with u_smp.
+ * Draws are inverse-CDF in index order (the smallest i whose running sum exceeds
+ * u * total).  top_k <= 0 / top_p >= 1 disable that pool.  Decisions in fp64.
+ * All arrays device; out_tok [K+1], *n_out = accepted + 1, or -IF_ERR_ARG when a
+ * draft token lies outside [0, V).  0 <= K <= 64; u_smp in [0, 1).
+ * ------------------------------------------------------------------------- */
+if_status if_spec_verify(int32_t K, int64_t V, const float* tgt_logits, const float* draft_probs,
+                         const int32_t* draft_tok, const float* u_acc, float u_smp, int32_t is_top, int32_t top_k,
+                         float top_p, int32_t* out_tok, int32_t* n_out, if_stream_t stream);
+
+/* ---------------------------------------------------------------------------
+ * Dynamic batching (Fig. 3): an inference engine with the
+ * paper's two-function interface over one rank's stack (plan by_layer, 1 device).
+ *   if_engine_add_query(S)  add query S (host prompt tokens) to the query pool;
+ *                           FIFO admission when a KV slot is free
+ *   if_engine_infer()       ONE step over the pool: admits queued queries, runs the
+ *                           prompts of new queries (causal chunks, continued over
+ *                           later steps when they exceed the token budget) and one
+ *                           decode token of every running query in a single
+ *                           if_run_stack_kv batch, then the LM head and the greedy
+ *                           choice -> (query id, next token) for every query whose
+ *                           prompt is complete.  A query finishes at eos, after
+ *                           max_new tokens, or at max_ctx; its slot is released.
+ * Example (Fig. 3): S1, S2 decoding, AddQuery(S3) at T3 -> Infer() returns
+ * S1_3, S2_3 and S3's first token in the same step.
+ * if_engine_verify()        speculative decoding's target pass for one running query
+ *                           (NEXT-3): [last token, draft_tok[0..K)] as one causal
+ *                           chunk, logits at all K+1 positions (small-M qGEMV), then
+ *                           if_spec_verify; the accepted tokens + 1 are appended.
+ * The engine owns its device state (KV cache, workspace, logits; allocated at create)
+ * and runs on the caller's stream; infer/verify synchronise it (results are host).
+ * Weights, embedding table and LM head stay caller-owned and must outlive it.
+ * ------------------------------------------------------------------------- */
+typedef struct if_engine_s* if_engine;
+typedef struct {
+  if_stack_shape shape;            /* the stack (scheme = the LM head's too) */
+  const if_layer_weights* layers;  /* host array of shape.layers device weight sets */
+  const float* embed;              /* device fp32 [vocab, hidden] */
+  const uint8_t* lm_head;          /* device packed [vocab, hidden] */
+  int32_t vocab;
+  int32_t slots;                   /* pool capacity (concurrent queries), 1..64 */
+  int32_t max_ctx;                 /* positions per slot */
+  int32_t step_tokens;             /* token budget of one Infer() step, slots..64 */
+} if_engine_config;
+
+if_status if_engine_create(const if_engine_config* cfg, if_engine* out);
+if_status if_engine_add_query(if_engine e, const int32_t* prompt /* host */, int32_t n, int32_t max_new,
+                              int32_t eos /* < 0: none */, int64_t* query_id);
+if_status if_engine_infer(if_engine e, int64_t* ids /* host [cap] */, int32_t* tokens /* host [cap] */, int32_t cap,
+                          int32_t* n_out, if_stream_t stream);
+if_status if_engine_verify(if_engine e, int64_t query_id, int32_t K, const int32_t* draft_tok /* host [K] */,
+                           const float* draft_probs /* device [K, vocab] */, const float* u_acc /* host [K] */,
+                           float u_smp, int32_t is_top, int32_t top_k, float top_p, int32_t* out_tok /* host [K+1] */,
+                           int32_t* n_out, if_stream_t stream);
+/* phase: 0 queued, 1 prefill, 2 decoding, 3 finished, -1 unknown id */
+if_status if_engine_query(if_engine e, int64_t query_id, int32_t* phase, int32_t* generated, int32_t* position);
+/* device logits of the last infer/verify step, [rows, vocab] (engine-owned, valid
+ * until the next call) and the query id of each row */
+if_status if_engine_last_logits(if_engine e, const float** logits, int32_t* rows, int64_t* ids /* host [64] */);
+if_status if_engine_destroy(if_engine e);
+
 /* Thread-local message for the last non-OK status returned on this thread. */
 const char* if_last_error(void);
 

@@ -11,7 +11,7 @@ from __future__ import annotations
 import ctypes
 
 from . import _lib
-from ._lib import Assignment, KvCache, LayerWeights, Plan, Scheme, StackShape
+from ._lib import Assignment, EngineConfig, KvCache, LayerWeights, Plan, Scheme, StackShape
 
 QTYPES = {"Q2": 2, "Q3": 3, "Q3H": 35, "Q4": 4, "Q5": 5, "Q6": 6, "Q8": 8}
 IF_BY_LAYER, IF_BY_TENSOR, IF_HYBRID = 0, 1, 2
@@ -225,6 +225,85 @@ def if_run_stack_kv(shape: StackShape, plan: Plan, rank: int, comm, layers_arr, 
                                  _ptr(h_in), T, mode, _ptr(h_out), _ptr(last_qkv), ctypes.byref(kv.c),
                                  _ptr(slot_ids), _ptr(positions), _ptr(workspace), _stream(stream)),
            "if_run_stack_kv")
+
+
+# ---- language-model head, speculative verification --------------------------------
+def if_embed(table, V: int, d: int, tokens, T: int, h, dev_status=None, stream=None):
+    _check(lib().if_embed(_ptr(table), V, d, _ptr(tokens), T, _ptr(h), _ptr(dev_status), _stream(stream)), "if_embed")
+
+
+def if_lm_logits(s: Scheme, lm, V: int, d: int, h, T: int, rows, logits, scratch, stream=None):
+    _check(lib().if_lm_logits(s, _ptr(lm), V, d, _ptr(h), T, _ptr(rows), _ptr(logits), _ptr(scratch),
+                              _stream(stream)), "if_lm_logits")
+
+
+def if_argmax(logits, T: int, V: int, tokens, stream=None):
+    _check(lib().if_argmax(_ptr(logits), T, V, _ptr(tokens), _stream(stream)), "if_argmax")
+
+
+def if_spec_verify(K: int, V: int, tgt_logits, draft_probs, draft_tok, u_acc, u_smp: float, is_top: bool,
+                   top_k: int, top_p: float, out_tok, n_out, stream=None):
+    _check(lib().if_spec_verify(K, V, _ptr(tgt_logits), _ptr(draft_probs), _ptr(draft_tok), _ptr(u_acc),
+                                float(u_smp), int(is_top), int(top_k), float(top_p), _ptr(out_tok), _ptr(n_out),
+                                _stream(stream)), "if_spec_verify")
+
+
+class Engine:
+    """Dynamic-batching engine (if_engine_*): AddQuery / Infer and the
+    speculative target pass (if_engine_verify).  Marshalling only."""
+
+    def __init__(self, shape: StackShape, layers_arr, embed, lm_head, vocab: int, slots: int, max_ctx: int,
+                 step_tokens: int = 64):
+        self._keep = (layers_arr, embed, lm_head)
+        self.vocab = vocab
+        self.cfg = EngineConfig(shape, ctypes.cast(layers_arr, ctypes.c_void_p), embed.data_ptr(),
+                                lm_head.data_ptr(), vocab, slots, max_ctx, step_tokens)
+        self.h = ctypes.c_void_p()
+        _check(lib().if_engine_create(ctypes.byref(self.cfg), ctypes.byref(self.h)), "if_engine_create")
+
+    def add_query(self, prompt, max_new: int, eos: int = -1) -> int:
+        arr = (ctypes.c_int32 * len(prompt))(*prompt)
+        qid = ctypes.c_int64()
+        _check(lib().if_engine_add_query(self.h, arr, len(prompt), max_new, eos, ctypes.byref(qid)),
+               "if_engine_add_query")
+        return qid.value
+
+    def infer(self, stream=None):
+        ids = (ctypes.c_int64 * 64)()
+        toks = (ctypes.c_int32 * 64)()
+        n = ctypes.c_int32()
+        _check(lib().if_engine_infer(self.h, ids, toks, 64, ctypes.byref(n), _stream(stream)), "if_engine_infer")
+        return [(ids[i], toks[i]) for i in range(n.value)]
+
+    def verify(self, qid: int, draft_tok, draft_probs, u_acc, u_smp: float, is_top: bool = False, top_k: int = 0,
+               top_p: float = 1.0, stream=None):
+        K = len(draft_tok)
+        dt = (ctypes.c_int32 * max(1, K))(*draft_tok)
+        ua = (ctypes.c_float * max(1, K))(*u_acc)
+        out = (ctypes.c_int32 * (K + 1))()
+        n = ctypes.c_int32()
+        _check(lib().if_engine_verify(self.h, qid, K, dt, _ptr(draft_probs), ua, float(u_smp), int(is_top),
+                                      int(top_k), float(top_p), out, ctypes.byref(n), _stream(stream)),
+               "if_engine_verify")
+        return [out[i] for i in range(n.value)]
+
+    def query(self, qid: int):
+        ph, gen, pos = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32()
+        _check(lib().if_engine_query(self.h, qid, ctypes.byref(ph), ctypes.byref(gen), ctypes.byref(pos)),
+               "if_engine_query")
+        return ph.value, gen.value, pos.value
+
+    def last_logits(self):
+        """(device pointer, rows, query ids) of the last step's logits [rows, vocab]."""
+        p, rows = ctypes.c_void_p(), ctypes.c_int32()
+        ids = (ctypes.c_int64 * 64)()
+        _check(lib().if_engine_last_logits(self.h, ctypes.byref(p), ctypes.byref(rows), ids), "if_engine_last_logits")
+        return p.value, rows.value, [ids[i] for i in range(rows.value)]
+
+    def destroy(self):
+        if self.h:
+            _check(lib().if_engine_destroy(self.h), "if_engine_destroy")
+            self.h = ctypes.c_void_p()
 
 
 def if_launch_count(reset: bool = False) -> int:

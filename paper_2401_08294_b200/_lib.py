@@ -42,6 +42,11 @@ class LayerWeights(ctypes.Structure):
     _fields_ = [("wqkv", vp), ("wo", vp), ("wgu", vp), ("wdown", vp)]
 
 
+class EngineConfig(ctypes.Structure):
+    _fields_ = [("shape", StackShape), ("layers", vp), ("embed", vp), ("lm_head", vp), ("vocab", i32),
+                ("slots", i32), ("max_ctx", i32), ("step_tokens", i32)]
+
+
 _SIGS = {
     "if_block_bytes": (i64, [Scheme]),
     "if_packed_bytes": (i64, [Scheme, i64, i64]),
@@ -66,6 +71,17 @@ _SIGS = {
     "if_run_stack": (i32, [vp, vp, i32, vp, vp, vp, i64, i32, vp, vp, vp, vp]),
     "if_kv_cache_bytes": (i32, [vp, vp, i32, i32, i32, vp]),
     "if_run_stack_kv": (i32, [vp, vp, i32, vp, vp, vp, i64, i32, vp, vp, vp, vp, vp, vp, vp]),
+    "if_embed": (i32, [vp, i32, i32, vp, i64, vp, vp, vp]),
+    "if_lm_logits": (i32, [Scheme, vp, i64, i64, vp, i64, vp, vp, vp, vp]),
+    "if_argmax": (i32, [vp, i64, i64, vp, vp]),
+    "if_spec_verify": (i32, [i32, i64, vp, vp, vp, vp, f32, i32, i32, f32, vp, vp, vp]),
+    "if_engine_create": (i32, [vp, vp]),
+    "if_engine_add_query": (i32, [vp, vp, i32, i32, i32, vp]),
+    "if_engine_infer": (i32, [vp, vp, vp, i32, vp, vp]),
+    "if_engine_verify": (i32, [vp, i64, i32, vp, vp, vp, f32, i32, i32, f32, vp, vp, vp]),
+    "if_engine_query": (i32, [vp, i64, vp, vp, vp]),
+    "if_engine_last_logits": (i32, [vp, vp, vp, vp]),
+    "if_engine_destroy": (i32, [vp]),
     "if_last_error": (ctypes.c_char_p, []),
     "if_launch_count": (i64, [i32]),
 }

@@ -43,7 +43,15 @@ def _newest(paths):
 def _compile(src: str, force: bool) -> str:
     obj = os.path.join(BUILD, os.path.basename(src)[:-3] + ".o")
     if force or not os.path.exists(obj) or os.path.getmtime(obj) < max(os.path.getmtime(src), _newest(_headers())):
-        cmd = [NVCC, *FLAGS, *EXTRA, "-c", src, "-o", obj + ".tmp"]
+        flags = list(FLAGS)
+        with open(src) as f:  # per-file override, e.g. "// ifb-build: -std=c++17" on line 1..5
+            for line in [f.readline() for _ in range(5)]:
+                if line.startswith("// ifb-build:"):
+                    for opt in line.split(":", 1)[1].split():
+                        if opt.startswith("-std="):
+                            flags = [x for x in flags if not x.startswith("-std=")]
+                        flags.append(opt)
+        cmd = [NVCC, *flags, *EXTRA, "-c", src, "-o", obj + ".tmp"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"nvcc failed for {src}:\n{r.stdout}\n{r.stderr}")

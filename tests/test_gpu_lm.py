@@ -1,0 +1,229 @@
+"""GPU parity of the language-model head, the speculative verification and the
+dynamic-batching engine (lm.cu, engine.cu; Q25-Q27)
+against the oracle, through the C ABI.
+
+  * if_embed: bitwise gather; out-of-range token -> status + zero row.
+  * if_lm_logits: final RMSNorm + quantized projection within 1e-3 normwise of
+    O.lm_logits_f64 fed the same fp32 hidden states (B = 1 engine GEMV, B >= 2 tensor
+    cores, ragged vocab).
+  * if_argmax: exact first-maximum index (ties included).
+  * if_spec_verify: the output token list equals O.spec_verify's on the same logits
+    and draft distributions for K = 0..8, vocabularies up to 32000, with and without
+    the top-k / top-p pools (integer decisions, taken in fp64 on both sides).
+  * Engine (Fig. 3 scenario): every emitted token is the oracle's greedy
+    choice along the same sequence (teacher forced; a near-tie within the fp32 logit
+    tolerance may pick either), the late query's first token arrives in the step it
+    was added, logits rows within 1e-3 of the oracle; the verification pass's K+1
+    logits rows match the oracle's sequential target distributions and its tokens
+    equal O.spec_verify on them.
+"""
+import numpy as np
+import pytest
+
+import oracle as O
+import paper_2401_08294_b200 as F
+import synth
+from gpu_util import dev, normwise, torch
+from paper_2401_08294_b200.model import Stack, deinterleave_rows
+
+pytestmark = pytest.mark.gpu
+
+QT, BS = 35, 64
+
+
+def test_embed_gather_bitwise():
+    d = dev()
+    V, D = 300, 512
+    E = synth.embedding(V, D)
+    tok = np.array([0, 299, 17, 17, 150], np.int32)
+    Ed = torch.from_numpy(E).to(d)
+    h = torch.empty(len(tok), D, device=d)
+    st = torch.zeros(1, dtype=torch.int32, device=d)
+    F.if_embed(Ed, V, D, torch.from_numpy(tok).to(d), len(tok), h, st)
+    torch.cuda.synchronize()
+    assert np.array_equal(h.cpu().numpy(), E[tok]) and int(st.item()) == 0
+    F.if_embed(Ed, V, D, torch.tensor([3, 300], dtype=torch.int32, device=d), 2, h, st)
+    torch.cuda.synchronize()
+    assert int(st.item()) == 1 and float(h[1].abs().max()) == 0.0
+
+
+@pytest.mark.parametrize("V,T", [(4096, 1), (4096, 3), (1000, 8), (32000, 2), (32000, 9)])
+def test_lm_logits_vs_oracle(V, T):
+    d = dev()
+    D = 1024
+    s = F.scheme(QT, BS)
+    lm = O.quantize(QT, BS, synth.lm_head(V, D))
+    h = synth.activations(T, D, tid=40 + T) * np.float32(3.0)
+    rows = np.arange(T, dtype=np.int32)[::-1].copy()  # reversed row selection
+    logits = torch.empty(T, V, device=d)
+    scratch = torch.empty(T, D, device=d)
+    F.if_lm_logits(s, torch.from_numpy(lm).to(d), V, D, torch.from_numpy(h).to(d), T,
+                   torch.from_numpy(rows).to(d), logits, scratch)
+    torch.cuda.synchronize()
+    ref = O.lm_logits_f64(QT, BS, lm, V, D, h[rows])
+    assert normwise(logits.cpu().numpy(), ref) <= 1e-3
+
+
+def test_argmax_first_maximum():
+    d = dev()
+    rng = np.random.default_rng(1)
+    for V in (7, 1000, 32000, 100003):
+        x = rng.integers(-50, 50, size=(5, V)).astype(np.float32)  # heavy ties
+        tok = torch.empty(5, dtype=torch.int32, device=d)
+        F.if_argmax(torch.from_numpy(x).to(d), 5, V, tok)
+        torch.cuda.synchronize()
+        assert tok.cpu().numpy().tolist() == [O.argmax(r) for r in x]
+
+
+def _spec_case(rng, K, V, peaked):
+    logits = (rng.standard_normal((K + 1, V)) * (4.0 if peaked else 1.0)).astype(np.float32)
+    probs = rng.dirichlet(np.full(V, 0.3), size=K).astype(np.float32) if K else np.zeros((0, V), np.float32)
+    toks = np.array([rng.choice(V, p=p / p.sum()) for p in probs.astype(np.float64)], np.int32)
+    return logits, probs, toks
+
+
+@pytest.mark.parametrize("V", [50, 4096, 32000])
+def test_spec_verify_equals_oracle(V):
+    d = dev()
+    rng = np.random.default_rng(V)
+    out = torch.empty(65, dtype=torch.int32, device=d)
+    n = torch.empty(1, dtype=torch.int32, device=d)
+    cases = 0
+    for K in (0, 1, 2, 4, 8):
+        for trial in range(6):
+            logits, probs, toks = _spec_case(rng, K, V, peaked=trial % 2 == 1)
+            u_acc = rng.random(K).astype(np.float32)
+            u_smp = float(np.float32(rng.random()))
+            for is_top, top_k, top_p in ((False, 0, 1.0), (True, 5, 1.0), (True, 0, 0.9), (True, 40, 0.5)):
+                F.if_spec_verify(K, V, torch.from_numpy(logits).to(d), torch.from_numpy(probs).to(d) if K else None,
+                                 torch.from_numpy(toks).to(d) if K else None,
+                                 torch.from_numpy(u_acc).to(d) if K else None, u_smp, is_top, top_k, top_p, out, n)
+                torch.cuda.synchronize()
+                got = out[:int(n.item())].cpu().numpy().tolist()
+                ref = O.spec_verify(logits, probs, toks, u_acc, u_smp, is_top, top_k, top_p)
+                assert got == ref, (K, trial, is_top, top_k, top_p)
+                cases += 1
+    assert cases == 120
+
+
+def test_spec_verify_invalid_draft_token():
+    d = dev()
+    V = 10
+    logits = torch.zeros(3, V, device=d)
+    probs = torch.full((2, V), 0.1, device=d)
+    out = torch.empty(3, dtype=torch.int32, device=d)
+    n = torch.empty(1, dtype=torch.int32, device=d)
+    F.if_spec_verify(2, V, logits, probs, torch.tensor([1, 10], dtype=torch.int32, device=d),
+                     torch.zeros(2, device=d), 0.5, False, 0, 1.0, out, n)
+    torch.cuda.synchronize()
+    assert int(n.item()) == -1
+
+
+CFG = dict(layers=2, hidden=512, heads=8, kv_heads=2, head_dim=64, ffn=1408)
+
+
+class LmRig:
+    def __init__(self, V=512, slots=4, max_ctx=64, step_tokens=16):
+        self.d = dev()
+        s = F.scheme(QT, BS)
+        self.shape = F.stack_shape(*[CFG[k] for k in ("layers", "hidden", "heads", "kv_heads", "head_dim", "ffn")], s)
+        self.plan = F.if_plan_partition(F.IF_BY_LAYER, self.shape, 1)
+        self.stk = Stack(CFG, s, self.plan, 0, self.d)
+        D = CFG["hidden"]
+        self.V = V
+        self.E = synth.embedding(V, D)
+        self.lm = O.quantize(QT, BS, synth.lm_head(V, D))
+        self.eng = F.Engine(self.shape, self.stk.arr, torch.from_numpy(self.E).to(self.d),
+                            torch.from_numpy(self.lm).to(self.d), V, slots, max_ctx, step_tokens)
+        host = [[t.cpu().numpy() for t in layer] for layer in self.stk.layers]
+        self.W = ([l[0] for l in host], [l[1] for l in host],
+                  [deinterleave_rows(l[2], 2 * CFG["ffn"]) for l in host], [l[3] for l in host])
+        self.oshape = dict(CFG, qtype=QT, block=BS)
+        self.max_ctx = max_ctx
+
+    def oracle_rows(self, prompt, emitted):
+        return O.lm_sequence_f64(self.oshape, *self.W, self.E, self.lm, self.V, prompt, emitted[:-1], self.max_ctx)
+
+    def logits_rows(self):
+        """The engine's last-step logits [rows, V] (a device pointer it owns), copied out."""
+        p, rows, ids = self.eng.last_logits()
+
+        class _View:  # zero-copy view of the engine's buffer for torch
+            __cuda_array_interface__ = {"shape": (rows, self.V), "typestr": "<f4", "data": (p, False), "version": 3}
+
+        torch.cuda.synchronize()
+        return torch.as_tensor(_View(), device=self.d).cpu().numpy(), ids
+
+
+def _greedy_ok(row_ref, tok):
+    """tok is the oracle's argmax, or within the fp32 logit tolerance of the maximum."""
+    best = O.argmax(row_ref)
+    if tok == best:
+        return True
+    return row_ref[best] - row_ref[tok] <= 2e-3 * np.abs(row_ref).max()
+
+
+def test_engine_fig3_dynamic_batching_vs_oracle():
+    r = LmRig()
+    e = r.eng
+    prompts = {1: [3, 77, 401, 9], 2: [250, 1, 1], 3: [42, 43, 44, 45, 46, 47, 48]}
+    qid = {1: e.add_query(prompts[1], max_new=8), 2: e.add_query(prompts[2], max_new=8)}
+    emitted = {1: [], 2: [], 3: []}
+    steps = []
+    for step in range(1, 10):
+        if step == 3:  # AddQuery(S3) at T3 (Fig. 3)
+            qid[3] = e.add_query(prompts[3], max_new=5)
+        out = e.infer()
+        inv = {v: k for k, v in qid.items()}
+        steps.append({inv[i]: t for i, t in out})
+        lg, ids = r.logits_rows()
+        for row, (i, t) in enumerate(out):
+            emitted[inv[i]].append(t)
+            ref = r.oracle_rows(prompts[inv[i]], emitted[inv[i]])[-1]
+            assert normwise(lg[row], ref) <= 1e-3, (step, inv[i])
+            assert _greedy_ok(ref, t), (step, inv[i], t, O.argmax(ref))
+    # Fig. 3: S3 added at T3 is answered at T3 together with S1 and S2
+    assert set(steps[2]) == {1, 2, 3}
+    assert [len(emitted[k]) for k in (1, 2, 3)] == [8, 8, 5]
+    assert e.query(qid[3])[0] == 3 and e.query(qid[1])[0] == 3
+    assert e.infer() == []
+
+
+def test_engine_capacity_fifo_and_chunked_prompt():
+    """Two slots, three queries: the third waits for a finish (FIFO); a prompt longer
+    than the step budget is prefilled over two steps before its first token."""
+    r = LmRig(slots=2, step_tokens=8)
+    e = r.eng
+    a = e.add_query([5, 6], max_new=2)
+    b = e.add_query(list(range(10, 22)), max_new=2)  # 12 tokens > budget 8 - 1
+    c = e.add_query([7], max_new=1)
+    seen = [set(dict(e.infer())) for _ in range(5)]
+    # step 1: a's prompt (2) + 6 of b's 12 prompt tokens -> a's first token
+    # step 2: a decodes (its 2nd token: done, slot freed) + b's last 6 -> b's first token
+    # step 3: c admitted into a's slot: b decodes (done) + c's prompt -> c's only token
+    assert seen == [{a}, {a, b}, {b, c}, set(), set()]
+    assert [e.query(q)[:2] for q in (a, b, c)] == [(3, 2), (3, 2), (3, 1)]
+
+
+def test_engine_verify_matches_oracle_target_pass():
+    r = LmRig(V=256)
+    e = r.eng
+    prompt = [11, 22, 33]
+    q = e.add_query(prompt, max_new=40)
+    first = e.infer()[0][1]
+    emitted = [first]
+    rng = np.random.default_rng(5)
+    for rnd in range(4):
+        K = 4
+        probs = rng.dirichlet(np.full(r.V, 0.2), size=K).astype(np.float32)
+        draft = [int(rng.choice(r.V, p=p / p.sum())) for p in probs.astype(np.float64)]
+        u_acc = rng.random(K).astype(np.float32)
+        u_smp = float(np.float32(rng.random()))
+        got = e.verify(q, draft, torch.from_numpy(probs).to(r.d), u_acc, u_smp, is_top=(rnd % 2 == 1), top_k=8)
+        lg, _ = r.logits_rows()
+        # the oracle's K+1 target distributions along prompt + emitted + drafts
+        ref = O.lm_sequence_f64(r.oshape, *r.W, r.E, r.lm, r.V, prompt, emitted + draft, r.max_ctx)[-(K + 1):]
+        assert normwise(lg, ref) <= 1e-3
+        assert got == O.spec_verify(lg, probs, draft, u_acc, u_smp, rnd % 2 == 1, 8, 1.0)
+        emitted += got
+    assert e.query(q)[1] == len(emitted)
