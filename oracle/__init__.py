@@ -84,6 +84,8 @@ def lib():
             L.ref_lm_logits_f64.argtypes = [i32, i32, vp, i64, i64, vp, i64, vp]
             L.ref_argmax_f64.argtypes = [vp, i64]
             L.ref_argmax_f64.restype = i64
+            L.ref_cost_estimate.argtypes = [i32, i32, i32, ctypes.c_double, ctypes.c_double, ctypes.c_double, vp,
+                                             ctypes.c_double, i32, vp, vp]
             _lib = L
     return _lib
 
@@ -334,6 +336,42 @@ def lm_sequence_f64(shape: dict, wqkv, wo, wgu, wdown, embed: np.ndarray, lm_pac
         h, _ = stack_kv_f64(shape, wqkv, wo, wgu, wdown, embed[[tok]], [0], [len(prompt) + j], K, Vc)
         rows.append(lm_logits_f64(qt, bs, lm_packed, V, d, h)[0])
     return np.stack(rows)
+
+
+def cost_estimate(layers: int, stages: int, groups: int, t_fixed: float, layer_bytes: float, bw: float, t_merge,
+                  t_hop: float, micro_batches: int = 1):
+    """ref_cost_estimate (Q29) -> (decode tokens/s, throughput tokens/s).  t_merge:
+    sequence indexed by group size (entry g = latency of one g-way merge)."""
+    tm = np.zeros(9, np.float64)
+    for g, v in enumerate(list(t_merge)[:9]):
+        tm[g] = v
+    dec, thr = ctypes.c_double(), ctypes.c_double()
+    _chk(lib().ref_cost_estimate(layers, stages, groups, float(t_fixed), float(layer_bytes), float(bw), _ptr(tm),
+                                 float(t_hop), micro_batches, ctypes.byref(dec), ctypes.byref(thr)), "cost_estimate")
+    return dec.value, thr.value
+
+
+def plan_auto(objective: str, layers: int, heads: int, kv_heads: int, ffn_blocks: int, devices: int, cost: dict,
+              layer_bytes: float, micro_batches: int = 1):
+    """The grid (stages, groups), stages x groups = devices, that a valid plan admits
+    (ref_plan succeeds) and that maximises the objective ("decode" or "throughput");
+    ties keep the grid found first, in order of increasing groups."""
+    best = None
+    for groups in range(1, devices + 1):
+        if devices % groups:
+            continue
+        stages = devices // groups
+        strategy = 0 if groups == 1 else (1 if stages == 1 else 2)
+        try:
+            plan(strategy, layers, heads, kv_heads, ffn_blocks, devices, stages, groups)
+        except OracleError:
+            continue
+        dec, thr = cost_estimate(layers, stages, groups, cost["t_fixed"], layer_bytes, cost["bw"], cost["t_merge"],
+                                 cost["t_hop"], micro_batches)
+        val = dec if objective == "decode" else thr
+        if best is None or val > best[0]:
+            best = (val, stages, groups, dec, thr)
+    return best
 
 
 def kv_cache(shape: dict, slots: int, max_ctx: int):

@@ -654,6 +654,28 @@ int64_t ref_argmax_f64(const double* x, int64_t n) {
 }
 
 /* ------------------------------------------------------------------------ */
+/* partition cost model (S:629-637 estimate; "merged twice"; Table 5      */
+/* P:224-237; reading Q29)                                                   */
+/* ------------------------------------------------------------------------ */
+
+/* Per-token latency of one decode stream under a (stages x groups) partition:
+ *   L layers, each on a 1/groups shard: t_fixed + (layer_bytes / groups) / bw
+ *   + 2 merges per layer when groups > 1 ("merged twice"): t_merge[groups]
+ *   + (stages - 1) stage hand-offs: t_hop
+ * decode speed = 1 / latency; throughput = decode speed x min(stages, micro_batches)
+ * (a filled pipeline keeps every stage busy, Q22).  Seconds, bytes, bytes/s. */
+int ref_cost_estimate(int layers, int stages, int groups, double t_fixed, double layer_bytes, double bw,
+                      const double* t_merge, double t_hop, int micro_batches, double* decode, double* throughput) {
+  if (layers < 1 || stages < 1 || groups < 1 || groups > 8 || micro_batches < 1 || bw <= 0.0) return 2;
+  double lat = (double)layers * (t_fixed + (layer_bytes / (double)groups) / bw);
+  if (groups > 1) lat += 2.0 * (double)layers * t_merge[groups];
+  lat += (double)(stages - 1) * t_hop;
+  *decode = 1.0 / lat;
+  *throughput = *decode * (double)(micro_batches < stages ? micro_batches : stages);
+  return 0;
+}
+
+/* ------------------------------------------------------------------------ */
 /* partition planner (Table 4; Q20)           */
 /* ------------------------------------------------------------------------ */
 

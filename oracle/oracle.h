@@ -107,6 +107,13 @@ int ref_lm_logits_f64(int qtype, int block, const uint8_t* lm, int64_t V, int64_
 /* greedy choice: first index of the maximum; -1 for n = 0 */
 int64_t ref_argmax_f64(const double* x, int64_t n);
 
+/* ---- partition cost model (Table 5; Q29) --------
+ * latency = L (t_fixed + layer_bytes / groups / bw) + 2 L t_merge[groups] [groups > 1]
+ *         + (stages - 1) t_hop;  decode = 1 / latency;
+ * throughput = decode x min(stages, micro_batches).  t_merge indexed by group size. */
+int ref_cost_estimate(int layers, int stages, int groups, double t_fixed, double layer_bytes, double bw,
+                      const double* t_merge, double t_hop, int micro_batches, double* decode, double* throughput);
+
 /* ---- partition planner (Table 4; Q20) ----------------- */
 /* strategy: 0 by-layer, 1 by-tensor, 2 hybrid.  Output arrays have `devices`
  * entries, 0-based half-open ranges: layer [lb,le), head [hb,he), kv-head [kb,ke),
