@@ -48,7 +48,8 @@ typedef enum {
   IF_ERR_GRID = 7,    /* devices != stages x groups                          */
   IF_ERR_CUDA = 8,    /* CUDA launch / runtime failure                               */
   IF_ERR_COMM = 9,    /* communicator failure (peer memory or NCCL; SURVEY's IF_ERR_NCCL) */
-  IF_ERR_UNSUPPORTED = 10
+  IF_ERR_UNSUPPORTED = 10,
+  IF_ERR_IO = 11      /* container file: cannot open/read/write, malformed, truncated */
 } if_status;
 
 /* Schemes ("2, 3, 4, 5, 6, and 8" bits plus 3.5-bit Q3H). */
@@ -382,6 +383,60 @@ if_status if_engine_query(if_engine e, int64_t query_id, int32_t* phase, int32_t
  * until the next call) and the query id of each row */
 if_status if_engine_last_logits(if_engine e, const float** logits, int32_t* rows, int64_t* ids /* host [64] */);
 if_status if_engine_destroy(if_engine e);
+
+/* ---------------------------------------------------------------------------
+ * Packed-tensor container (S:122-123 section layout; Q28).
+ * File: "IFQC", u32 version 1, u32 tensor count, then per tensor: u16 name length,
+ * name, u8 scheme id (if_qtype), u16 block, u8 ndim, u32 dims[ndim], u32 block count
+ * (= prod(dims) / block; blocks run along the last dim), the packed blocks exactly as
+ * if_quantize writes them.  Integers little-endian.
+ *   if_container_save   dims: n x 8 int64 (row i = tensor i's dims); data[i] host or
+ *                       device (data_on_device) packed bytes; device data goes through
+ *                       a pinned bounce buffer on `stream` (synchronised).
+ *   if_container_open   parses and checks every header (magic, version, scheme, block
+ *                       count vs dims, payload extents, no trailing bytes): IF_ERR_IO
+ *                       with the byte offset in if_last_error() otherwise.
+ *   if_container_load   tensor i -> device memory: pipelined pread into pinned staging
+ *                       buffers by 4 reader threads, async H2D on `stream`.  Returns
+ *                       once every copy is enqueued (stream-ordered completion).
+ *   if_container_read_host  tensor i -> host memory (synchronous).
+ * ------------------------------------------------------------------------- */
+typedef struct if_container_s* if_container;
+if_status if_container_save(const char* path, int32_t n, const char* const* names, const if_scheme* schemes,
+                            const int32_t* ndims, const int64_t* dims, const void* const* data, int32_t data_on_device,
+                            if_stream_t stream);
+if_status if_container_open(const char* path, if_container* out);
+int32_t if_container_count(if_container c);
+if_status if_container_info(if_container c, int32_t i, char* name, int32_t name_cap, if_scheme* s, int32_t* ndim,
+                            int64_t* dims /* [8] */, int64_t* bytes);
+if_status if_container_find(if_container c, const char* name, int32_t* index);
+if_status if_container_load(if_container c, int32_t i, void* dst_device, if_stream_t stream);
+if_status if_container_read_host(if_container c, int32_t i, void* dst_host);
+if_status if_container_close(if_container c);
+
+/* ---------------------------------------------------------------------------
+ * Partition cost model and auto-planner (Table 5
+ * P:224-237; Q29).  Per-token latency of one decode stream:
+ *   L (t_fixed + layer_bytes / groups / bw)           every layer on a 1/groups shard
+ *   + 2 L t_merge[groups]   (groups > 1)              "merged twice" per layer
+ *   + (stages - 1) t_hop                              stage hand-offs
+ * decode = 1 / latency (tokens/s of one stream); throughput = decode x min(stages,
+ * micro_batches) (a filled pipeline, Q22).  layer_bytes = the packed bytes of one
+ * layer in shape's scheme.  The calibrated parameters come from measured B200 runs
+ * (profiles/r2_cost_calibration.json).  if_plan_auto: over every grid stages x groups
+ * = devices that if_plan_partition accepts, the plan maximising decode (objective 0)
+ * or throughput (1); ties keep fewer TP ranks.
+ * ------------------------------------------------------------------------- */
+typedef struct {
+  double t_fixed_s;     /* per layer and token, independent of the shard size */
+  double bw_bytes_s;    /* effective weight-streaming bandwidth of one device */
+  double t_merge_s[9];  /* one all-reduce within a TP group of g ranks, index g */
+  double t_hop_s;       /* one stage-to-stage hand-off */
+} if_cost_model;
+if_status if_cost_estimate(const if_stack_shape* shape, int32_t stages, int32_t groups, const if_cost_model* cm,
+                           int32_t micro_batches, double* decode, double* throughput);
+if_status if_plan_auto(int32_t objective, const if_stack_shape* shape, int32_t devices, const if_cost_model* cm,
+                       int32_t micro_batches, if_plan* out, double* decode, double* throughput);
 
 /* Thread-local message for the last non-OK status returned on this thread. */
 const char* if_last_error(void);

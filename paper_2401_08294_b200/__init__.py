@@ -11,13 +11,13 @@ from __future__ import annotations
 import ctypes
 
 from . import _lib
-from ._lib import Assignment, EngineConfig, KvCache, LayerWeights, Plan, Scheme, StackShape
+from ._lib import Assignment, CostModel, EngineConfig, KvCache, LayerWeights, Plan, Scheme, StackShape
 
 QTYPES = {"Q2": 2, "Q3": 3, "Q3H": 35, "Q4": 4, "Q5": 5, "Q6": 6, "Q8": 8}
 IF_BY_LAYER, IF_BY_TENSOR, IF_HYBRID = 0, 1, 2
 IF_DECODE, IF_PREFILL = 0, 1
 STATUS = {0: "OK", 1: "ARG", 2: "SHAPE", 3: "SCHEME", 4: "INPUT", 5: "DECODE", 6: "PLAN", 7: "GRID",
-          8: "CUDA", 9: "COMM", 10: "UNSUPPORTED"}
+          8: "CUDA", 9: "COMM", 10: "UNSUPPORTED", 11: "IO"}
 
 
 class IFError(RuntimeError):
@@ -304,6 +304,76 @@ class Engine:
         if self.h:
             _check(lib().if_engine_destroy(self.h), "if_engine_destroy")
             self.h = ctypes.c_void_p()
+
+
+# ---- packed-tensor container (NEXT-4) -------------------------------------------------
+def if_container_save(path: str, tensors, on_device: bool, stream=None):
+    """tensors: list of (name, Scheme, dims, packed uint8 tensor / numpy array)."""
+    n = len(tensors)
+    names = (ctypes.c_char_p * max(1, n))(*[t[0].encode() for t in tensors])
+    schemes = (Scheme * max(1, n))(*[t[1] for t in tensors])
+    ndims = (ctypes.c_int32 * max(1, n))(*[len(t[2]) for t in tensors])
+    dims = (ctypes.c_int64 * (8 * max(1, n)))()
+    for i, t in enumerate(tensors):
+        for k, x in enumerate(t[2]):
+            dims[8 * i + k] = int(x)
+    data = (ctypes.c_void_p * max(1, n))(*[(t[3].data_ptr() if on_device else t[3].ctypes.data) for t in tensors])
+    _check(lib().if_container_save(path.encode(), n, names, schemes, ndims, dims, data, int(on_device),
+                                   _stream(stream) if on_device else None), "if_container_save")
+
+
+class Container:
+    def __init__(self, path: str):
+        self.h = ctypes.c_void_p()
+        _check(lib().if_container_open(path.encode(), ctypes.byref(self.h)), "if_container_open")
+
+    def __len__(self):
+        return lib().if_container_count(self.h)
+
+    def info(self, i: int):
+        name = ctypes.create_string_buffer(1024)
+        s, nd, b = Scheme(), ctypes.c_int32(), ctypes.c_int64()
+        dims = (ctypes.c_int64 * 8)()
+        _check(lib().if_container_info(self.h, i, name, 1024, ctypes.byref(s), ctypes.byref(nd), dims, ctypes.byref(b)),
+               "if_container_info")
+        return name.value.decode(), (s.type, s.block), [dims[k] for k in range(nd.value)], b.value
+
+    def find(self, name: str) -> int:
+        i = ctypes.c_int32()
+        _check(lib().if_container_find(self.h, name.encode(), ctypes.byref(i)), "if_container_find")
+        return i.value
+
+    def load(self, i: int, dst, stream=None):
+        _check(lib().if_container_load(self.h, i, _ptr(dst), _stream(stream)), "if_container_load")
+
+    def read_host(self, i: int, dst_numpy):
+        _check(lib().if_container_read_host(self.h, i, dst_numpy.ctypes.data), "if_container_read_host")
+
+    def close(self):
+        if self.h:
+            _check(lib().if_container_close(self.h), "if_container_close")
+            self.h = ctypes.c_void_p()
+
+
+# ---- cost model / auto-planner (NEXT-4) ---------------------------------------------------
+def cost_model(t_fixed_s: float, bw_bytes_s: float, t_merge_s, t_hop_s: float) -> CostModel:
+    tm = (ctypes.c_double * 9)(*([float(x) for x in list(t_merge_s)[:9]] + [0.0] * (9 - min(9, len(t_merge_s)))))
+    return CostModel(float(t_fixed_s), float(bw_bytes_s), tm, float(t_hop_s))
+
+
+def if_cost_estimate(shape: StackShape, stages: int, groups: int, cm: CostModel, micro_batches: int = 1):
+    dec, thr = ctypes.c_double(), ctypes.c_double()
+    _check(lib().if_cost_estimate(ctypes.byref(shape), stages, groups, ctypes.byref(cm), micro_batches,
+                                  ctypes.byref(dec), ctypes.byref(thr)), "if_cost_estimate")
+    return dec.value, thr.value
+
+
+def if_plan_auto(objective: str, shape: StackShape, devices: int, cm: CostModel, micro_batches: int = 1):
+    p = Plan()
+    dec, thr = ctypes.c_double(), ctypes.c_double()
+    _check(lib().if_plan_auto(0 if objective == "decode" else 1, ctypes.byref(shape), devices, ctypes.byref(cm),
+                              micro_batches, ctypes.byref(p), ctypes.byref(dec), ctypes.byref(thr)), "if_plan_auto")
+    return p, dec.value, thr.value
 
 
 def if_launch_count(reset: bool = False) -> int:

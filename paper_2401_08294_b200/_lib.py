@@ -42,6 +42,11 @@ class LayerWeights(ctypes.Structure):
     _fields_ = [("wqkv", vp), ("wo", vp), ("wgu", vp), ("wdown", vp)]
 
 
+class CostModel(ctypes.Structure):
+    _fields_ = [("t_fixed_s", ctypes.c_double), ("bw_bytes_s", ctypes.c_double), ("t_merge_s", ctypes.c_double * 9),
+                ("t_hop_s", ctypes.c_double)]
+
+
 class EngineConfig(ctypes.Structure):
     _fields_ = [("shape", StackShape), ("layers", vp), ("embed", vp), ("lm_head", vp), ("vocab", i32),
                 ("slots", i32), ("max_ctx", i32), ("step_tokens", i32)]
@@ -82,6 +87,16 @@ _SIGS = {
     "if_engine_query": (i32, [vp, i64, vp, vp, vp]),
     "if_engine_last_logits": (i32, [vp, vp, vp, vp]),
     "if_engine_destroy": (i32, [vp]),
+    "if_container_save": (i32, [ctypes.c_char_p, i32, vp, vp, vp, vp, vp, i32, vp]),
+    "if_container_open": (i32, [ctypes.c_char_p, vp]),
+    "if_container_count": (i32, [vp]),
+    "if_container_info": (i32, [vp, i32, vp, i32, vp, vp, vp, vp]),
+    "if_container_find": (i32, [vp, ctypes.c_char_p, vp]),
+    "if_container_load": (i32, [vp, i32, vp, vp]),
+    "if_container_read_host": (i32, [vp, i32, vp]),
+    "if_container_close": (i32, [vp]),
+    "if_cost_estimate": (i32, [vp, i32, i32, vp, i32, vp, vp]),
+    "if_plan_auto": (i32, [i32, vp, i32, vp, i32, vp, vp, vp]),
     "if_last_error": (ctypes.c_char_p, []),
     "if_launch_count": (i64, [i32]),
 }
