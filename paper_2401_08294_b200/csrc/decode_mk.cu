@@ -300,6 +300,18 @@ __device__ __forceinline__ void stage_quad(int q, float4 v, int xstride, float4*
   if (jj == 0) bs[b] = make_float2(sx, 0.f);
 }
 
+// 1 / sqrt(mean(h^2) + 1e-5) from every consumer thread's partial sum of squares
+__device__ __forceinline__ float mk_rms_inv(float ss, float* red, int K, int cw, int lane) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+  if (lane == 0) red[cw] = ss;
+  named_bar_sync(1, MK_CT);
+  float tot = 0.f;
+#pragma unroll
+  for (int w = 0; w < MK_NC; w++) tot += red[w];
+  return 1.0f / sqrtf(tot / (float)K + 1e-5f);
+}
+
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -376,12 +388,9 @@ __global__ void __launch_bounds__(MK_THREADS, 1) decode_mk_kernel(const __grid_c
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)nslot * MK_SLOT);
   uint64_t* empty = full + MK_MAXSLOT;
   float* red = reinterpret_cast<float*>(empty + MK_MAXSLOT);  // [MK_NC] + scalars
-  uint64_t* xbar = reinterpret_cast<uint64_t*>(red + 30);
   float4* xs = reinterpret_cast<float4*>(smem + (size_t)nslot * MK_SLOT + 2 * MK_MAXSLOT * 8 + 128);
   float2* bs = reinterpret_cast<float2*>(xs + 16 * xstride);
-  float* raw_sep = reinterpret_cast<float*>(bs + P.nbp_max);  // raw phase input when not staged in place
-  float* raw = P.raw_max ? raw_sep : reinterpret_cast<float*>(xs);  // TMA bulk-copy target
-  float* h_own = raw_sep + P.raw_max;                         // [MK_MAXOWN] this CTA's residual rows
+  float* h_own = reinterpret_cast<float*>(bs + P.nbp_max);    // [MK_MAXOWN] this CTA's residual rows
   int* pos = reinterpret_cast<int*>(h_own + MK_MAXOWN);       // [32] code positions
   float* ssq_s = reinterpret_cast<float*>(pos + 32);          // [MK_MAXG] sum h^2 partials
   float* part = ssq_s + MK_MAXG;
@@ -392,7 +401,6 @@ __global__ void __launch_bounds__(MK_THREADS, 1) decode_mk_kernel(const __grid_c
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], MK_NC);  // every consumer warp arrives once per fill
     }
-    mbar_init(xbar, 1);
     fence_mbar_init();
   }
   if (threadIdx.x < 32) pos[threadIdx.x] = kQ3hPosTab[threadIdx.x];
@@ -441,7 +449,6 @@ __global__ void __launch_bounds__(MK_THREADS, 1) decode_mk_kernel(const __grid_c
   const int cw = warp - 1;
   const Q3HConst kc = q3h_const();
   uint32_t slot = 0, round = 0;  // ring position (same sequence as the producer)
-  uint32_t xuse = 0;              // completed phases of the input-copy barrier
   // image versions of this launch (decode_mk.cuh): ctx/act are written once per
   // layer, h (and the sum-h^2 partials) twice; version 0 = the zero-filled workspace
   const uint32_t ep = stack ? ld_relaxed_u32(P.epoch) : 0u;
@@ -462,7 +469,7 @@ __global__ void __launch_bounds__(MK_THREADS, 1) decode_mk_kernel(const __grid_c
     // Phase input.  Producers (the previous phase's epilogues) already wrote it in
     // the transformed quad layout into a global xs image: one dependency wait, then
     // 16 bulk copies (one per quad row JJ) + the sum-h^2 partials for RMSNorm.
-    // The first phase (plain h) and the standalone GEMV stage from raw instead.
+    // The first phase (plain h) and the standalone GEMV stage from global memory.
     const bool from_image = stack && p > 0;
     const bool rms = kind == 0 || kind == 2;
     const uint32_t l = (uint32_t)(p >> 2);
@@ -575,72 +582,46 @@ __global__ void __launch_bounds__(MK_THREADS, 1) decode_mk_kernel(const __grid_c
       named_bar_sync(1, MK_CT);
       if (rms) out_scale = 1.0f / sqrtf(red[16] / (float)K + 1e-5f);
     } else {
-      // raw input -> registers -> transformed quads (raw may alias xs)
-      const float* src = stack ? P.h : P.x_in;
-      if (ct == 0) {
-        asm volatile("fence.proxy.async.global;" ::: "memory");
-        mbar_arrive_expect_tx(xbar, (uint32_t)K * 4u);
-        bulk_g2s(raw, src, (uint32_t)K * 4u, xbar, 0ull, false);
-      }
-      mbar_wait(xbar, xuse & 1);
-      xuse++;
-      if (dbg && ct == 0) { dbg[2] = gtimer(); dbg[10] = clock64(); }
-      const float4* raw4 = reinterpret_cast<const float4*>(raw);
+      // plain input (stage input h, or the GEMV's x) read straight from global memory
+      // (coalesced 128-bit loads, L2 hits after the first CTA) and staged as
+      // transformed quads; no shared-memory copy of the raw vector, so the largest
+      // shapes (70B: K up to 28672) fit.  RMSNorm needs the global sum of squares
+      // first: quads stay in registers when they fit, else they are re-read.
+      const float4* src4 = reinterpret_cast<const float4*>(stack ? P.h : P.x_in);
       const int nq = K >> 2, nqp = g.nbp * 16;
-      float inv = 1.f;
-      if (P.raw_max == 0) {
+      if (rms && nqp <= MK_MAXQ * MK_CT) {
         float4 v[MK_MAXQ];
         float ss = 0.f;
 #pragma unroll
         for (int i = 0; i < MK_MAXQ; i++) {
           const int q = ct + i * MK_CT;
-          v[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-          if (q < nq) {
-            v[i] = raw4[q];
-            ss = fmaf(v[i].x, v[i].x, fmaf(v[i].y, v[i].y, fmaf(v[i].z, v[i].z, fmaf(v[i].w, v[i].w, ss))));
-          }
+          v[i] = q < nq ? src4[q] : make_float4(0.f, 0.f, 0.f, 0.f);
+          ss = fmaf(v[i].x, v[i].x, fmaf(v[i].y, v[i].y, fmaf(v[i].z, v[i].z, fmaf(v[i].w, v[i].w, ss))));
         }
-        if (rms) {
+        const float inv = mk_rms_inv(ss, red, K, cw, lane);
 #pragma unroll
-          for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
-          if (lane == 0) red[cw] = ss;
-        }
-        named_bar_sync(1, MK_CT);  // every raw read is done: xs may now overwrite it
-        if (rms) {
-          float tot = 0.f;
-#pragma unroll
-          for (int w = 0; w < MK_NC; w++) tot += red[w];
-          inv = 1.0f / sqrtf(tot / (float)K + 1e-5f);  // a = h / sqrt(mean(h^2) + 1e-5)
-        }
-#pragma unroll
-        for (int i = 0; i < MK_MAXQ; i++) {
+        for (int i = 0; i < MK_MAXQ; i++)
           if (i * MK_CT + (ct & ~31) < nqp) {  // per-warp (nqp is a multiple of 32)
             const float4 a = v[i];
             stage_quad(ct + i * MK_CT, make_float4(a.x * inv, a.y * inv, a.z * inv, a.w * inv), xstride, xs, bs, pos);
           }
-        }
       } else {
+        float inv = 1.f;
         if (rms) {
           float ss = 0.f;
           for (int q = ct; q < nq; q += MK_CT) {
-            const float4 v = raw4[q];
-            ss = fmaf(v.x, v.x, fmaf(v.y, v.y, fmaf(v.z, v.z, fmaf(v.w, v.w, ss))));
+            const float4 a = src4[q];
+            ss = fmaf(a.x, a.x, fmaf(a.y, a.y, fmaf(a.z, a.z, fmaf(a.w, a.w, ss))));
           }
-#pragma unroll
-          for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
-          if (lane == 0) red[cw] = ss;
-          named_bar_sync(1, MK_CT);
-          float tot = 0.f;
-#pragma unroll
-          for (int w = 0; w < MK_NC; w++) tot += red[w];
-          inv = 1.0f / sqrtf(tot / (float)K + 1e-5f);
+          inv = mk_rms_inv(ss, red, K, cw, lane);
         }
         for (int q = ct; q < nqp; q += MK_CT) {
-          float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-          if (q < nq) v = raw4[q];
-          stage_quad(q, make_float4(v.x * inv, v.y * inv, v.z * inv, v.w * inv), xstride, xs, bs, pos);
+          float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (q < nq) a = src4[q];
+          stage_quad(q, make_float4(a.x * inv, a.y * inv, a.z * inv, a.w * inv), xstride, xs, bs, pos);
         }
       }
+      if (dbg && ct == 0) { dbg[2] = gtimer(); dbg[10] = clock64(); }
       named_bar_sync(1, MK_CT);
     }
     if (dbg && ct == 0) { dbg[3] = gtimer(); dbg[11] = clock64(); }
@@ -651,7 +632,7 @@ __global__ void __launch_bounds__(MK_THREADS, 1) decode_mk_kernel(const __grid_c
     {
       const int nrows = g.r1 - g.r0;
       const int nslots = (nrows + g.rps - 1) / g.rps;
-      const int gps = g.rps / g.R;                 // row groups per full slot
+      const int gps = max(1, g.rps / g.R);         // row groups per full slot (rps = 1 < R: one masked group)
       const int U = gps * g.nchunk;                // units per slot
       const int inv_nc = (65536 + g.nchunk - 1) / g.nchunk;
       int u0 = cw;                                 // first unit of this warp in slot sl
@@ -855,14 +836,8 @@ if_status mk_launch(MkParams& P, cudaStream_t st) {
     }
   }
   P.nbp_max = nbp_max;
-  int raw_need = P.mode == MK_MODE_GEMV ? P.gemv_K : std::max(std::max(P.d, P.lkv * P.hd), P.lf);
-  raw_need = (raw_need + 3) & ~3;
-  // stage in place (raw input aliases xs) when every phase's quads fit in registers
-  const bool inplace = nbp_max * 16 <= MK_MAXQ * MK_CT && (size_t)4 * raw_need <= (size_t)16 * 16 * mk_xstride(nbp_max);
-  const int raw_max = inplace ? 0 : raw_need;
-  P.raw_max = raw_max;
-  const size_t fixed = mk_fixed_smem(nbp_max, part_max) + (size_t)4 * raw_max + (size_t)4 * MK_MAXOWN + 128 +
-                       (size_t)4 * MK_MAXG;
+  P.raw_max = 0;  // (no raw-input buffer: plain inputs are staged from global memory)
+  const size_t fixed = mk_fixed_smem(nbp_max, part_max) + (size_t)4 * MK_MAXOWN + 128 + (size_t)4 * MK_MAXG;
   if (P.mode == MK_MODE_STACK && ((P.d + G - 1) / G > MK_MAXOWN || G > MK_MAXG || P.nqkv % 4 || P.d % 4 ||
                                   P.hd % 2))
     return IF_ERR_UNSUPPORTED;

@@ -1,0 +1,8 @@
+IFB_MODEL=70b timeout 300 python scripts/debug_70b.py 2>&1 | tail -2
+timeout 900 python -m pytest tests/test_gpu_fullsize.py tests/test_gpu_stack.py -q 2>&1 | tail -3
+for v in libif_b200 libif_if5 libif_if8 libif_nocomp libif_nocomp_if8; do
+  lib=/root/repo/paper_2401_08294_b200/$v.so
+  for m in 7b 70b; do
+    IFB_LIB_PATH=$lib timeout 600 python bench.py --model $m --steps 30 --warmup 3 --no-cpu-baseline 2>/dev/null | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('$v $m', round(d['value'],1), 'tok/s', round(d['ms_per_step'],3), 'ms frac', round(d['roofline']['frac'],3), 'launches', d['gpu_launches'])"
+  done
+done

@@ -1,0 +1,10 @@
+# 70B regression hunt: current vs round-1 decode_mk, bench + timelines
+for v in libif_b200 libif_r1mk; do
+  lib=/root/repo/paper_2401_08294_b200/$v.so
+  for m in 7b 70b; do
+    IFB_LIB_PATH=$lib timeout 600 python bench.py --model $m --steps 20 --warmup 3 --no-cpu-baseline 2>/dev/null | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('$v $m', round(d['value'],1), 'tok/s', round(d['ms_per_step'],3), 'ms frac', round(d['roofline']['frac'],3), 'launches', d['gpu_launches'])"
+  done
+  IFB_MODEL=70b IFB_LIB_PATH=$lib timeout 300 python scripts/mk_timeline2.py 8 2>&1 | tail -8
+  IFB_MODEL=7b IFB_LIB_PATH=$lib timeout 300 python scripts/mk_timeline2.py 32 2>&1 | tail -8
+done
+timeout 600 python -m pytest tests/test_gpu_lm.py -q -s -k container 2>&1 | grep -E "container load|passed|failed"

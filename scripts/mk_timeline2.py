@@ -20,7 +20,7 @@ dev = torch.device("cuda:0")
 s = F.scheme(35, 64)
 G = torch.cuda.get_device_properties(0).multi_processor_count
 layers = int(sys.argv[1]) if len(sys.argv) > 1 else 32
-cfg = dict(synth.LLAMA["7b"], layers=layers)
+cfg = dict(synth.LLAMA[os.environ.get("IFB_MODEL", "7b")], layers=layers)
 shape = F.stack_shape(*[cfg[k] for k in ("layers", "hidden", "heads", "kv_heads", "head_dim", "ffn")], s)
 plan = F.if_plan_partition(F.IF_BY_LAYER, shape, 1)
 stk = Stack(cfg, s, plan, 0, dev)
