@@ -253,12 +253,13 @@ def test_container_device_roundtrip_and_load_rate(tmp_path):
         assert payload == bytes(data.cpu().numpy())
     c = F.Container(path)
     outs = [torch.empty_like(t[3]) for t in tensors]
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    for i, o in enumerate(outs):
-        c.load(i, o)
-    torch.cuda.synchronize()
-    dt = time.perf_counter() - t0
+    for rep in range(2):  # the first pass also allocates the pinned staging buffers
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for i, o in enumerate(outs):
+            c.load(i, o)
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t0
     total = sum(o.numel() for o in outs)
     print(f"container load: {total / 1e6:.1f} MB in {dt * 1e3:.2f} ms = {total / dt / 1e9:.2f} GB/s (page cache -> HBM)")
     for o, t in zip(outs, tensors):
