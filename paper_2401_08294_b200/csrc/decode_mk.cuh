@@ -35,7 +35,9 @@ struct MkParams {
   float* y_out;
   int gemv_N, gemv_K, acc;
   // filled by mk_launch
-  int nslot, nbp_max, raw_max, xstride;
+  int nslot, nbp_max, raw_max, xstride;  // nbp_max / xstride: the staged input in shared memory (one K-segment)
+  int xg;      // float4 row stride of the global phase images (whole K)
+  int seg_nb;  // K-segment length in 64-blocks (multiple of 32); 0 = whole rows
   unsigned long long* dbg;  // nullable: per-CTA %globaltimer stamps [G][nphase][8] (instrumentation)
   const uint8_t* w[MK_MAXL][4];  // qkv, o, gu (gate/up rows interleaved), down per layer
 };
