@@ -209,6 +209,12 @@ if_status if_comm_create(const if_plan* plan, int32_t rank, int64_t max_tokens, 
 if_status if_comm_ipc_handle(if_comm c, uint8_t* handle64 /* host, 64 bytes */);
 if_status if_comm_open_peers(if_comm c, const uint8_t* handles /* host, devices*64 bytes */);
 if_status if_comm_destroy(if_comm c);
+/* All plan->devices ranks' peer-memory communicators inside ONE process on the
+ * current device (outs: plan->devices handles), peers wired with plain pointers.
+ * For running a multi-rank plan on one GPU as concurrent streams (tests, single-GPU
+ * functional checks): each rank's decode engine then uses SMs / devices CTAs so
+ * that every rank's engine is co-resident (the in-engine TP merges wait on peers). */
+if_status if_comm_create_local(const if_plan* plan, int64_t max_tokens, int32_t hidden, if_comm* outs);
 
 /* In-place all-reduce(sum) of buf[n] fp32 over this rank's TP group.  Peer
  * memory: every rank of the group ends with bit-identical sums (fixed rank
@@ -236,9 +242,10 @@ if_status if_comm_recv_prev(if_comm c, float* buf, int64_t n, if_stream_t stream
  * h_in  device fp32 [T, d] (ignored on stages > 0, which receive from stage-1),
  * h_out device fp32 [T, d] (valid on the last stage), last_qkv device fp32
  * [T, (lh + 2 lkv) head_dim] of the stage's last layer (nullable).
- * mode IF_DECODE (1 <= T <= 64, fp32 activations: Q3H_B64 on one rank with
- * T <= 6 runs the persistent engine -- one launch per token for the whole
- * stage; otherwise per-layer qGEMVs as in if_qgemv) or IF_PREFILL (T <= 4096,
+ * mode IF_DECODE (1 <= T <= 64, fp32 activations: Q3H_B64 with T <= 6 runs the
+ * persistent engine -- one launch per token for the whole stage, with the TP
+ * merges inside it when comm is a peer-memory communicator; otherwise per-layer
+ * qGEMVs as in if_qgemv) or IF_PREFILL (T <= 4096,
  * qGEMM on tcgen05 with bf16 activations).
  * workspace: device, if_stack_workspace_bytes(); ZERO-FILL IT ONCE before the
  * first call (cudaMemset) and keep it with this (shape, plan, rank): it carries

@@ -171,6 +171,21 @@ class Comm:
     def recv_prev(self, buf, stream=None):
         _check(lib().if_comm_recv_prev(self.h, _ptr(buf), buf.numel(), _stream(stream)), "if_comm_recv_prev")
 
+    @classmethod
+    def local(cls, plan: Plan, max_tokens: int, hidden: int):
+        """Every rank's peer-memory communicator in this process on the current device
+        (if_comm_create_local): run a multi-rank plan on one GPU as concurrent streams."""
+        hs = (ctypes.c_void_p * plan.devices)()
+        _check(lib().if_comm_create_local(ctypes.byref(plan), max_tokens, hidden, hs), "if_comm_create_local")
+        out = []
+        for r in range(plan.devices):
+            c = cls.__new__(cls)
+            c.h = ctypes.c_void_p(hs[r])
+            c.plan = plan
+            c.kind = "peer"
+            out.append(c)
+        return out
+
     def destroy(self):
         if self.h:
             _check(lib().if_comm_destroy(self.h), "if_comm_destroy")

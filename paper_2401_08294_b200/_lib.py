@@ -69,6 +69,7 @@ _SIGS = {
     "if_comm_ipc_handle": (i32, [vp, vp]),
     "if_comm_open_peers": (i32, [vp, vp]),
     "if_comm_destroy": (i32, [vp]),
+    "if_comm_create_local": (i32, [vp, i64, i32, vp]),
     "if_comm_allreduce": (i32, [vp, vp, i64, vp]),
     "if_comm_send_next": (i32, [vp, vp, i64, vp]),
     "if_comm_recv_prev": (i32, [vp, vp, i64, vp]),

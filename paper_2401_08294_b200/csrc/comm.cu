@@ -60,6 +60,10 @@ struct if_comm_s {
   bool opened[8] = {false};
   int group[8], ngroup = 0;  // ranks of my TP group in group-rank order
   int next = -1, prev = -1;  // pipeline neighbours (same group rank)
+  int hidden = 0;            // rows of the decode engine's TP exchange region
+  int engine_grid = 0;       // CTAs of this rank's decode engine (0: every SM; ranks sharing a GPU split them)
+  bool local = false;        // if_comm_create_local: every rank in this process, concurrent streams
+  bool shared_gpu = false;   // a peer process maps a mailbox on this same GPU (no concurrency guarantee)
 };
 
 namespace ifb {
@@ -286,6 +290,24 @@ if_status comm_recv(if_comm c, float* dst, int64_t n, cudaStream_t st) {
 
 int comm_group_size(if_comm c) { return c ? c->ngroup : 1; }
 
+// the decode engine's TP exchange regions of my group (group-rank order), or false
+// when this communicator cannot carry them (NCCL kind, peers not opened)
+bool comm_engine(if_comm c, float** boxes, int* ngroup, int* me, int* hidden, int* grid) {
+  // ranks in other processes on this same GPU are time-sliced, never co-resident:
+  // the in-engine merge would wait forever for a peer that cannot run
+  if (!c || c->kind != 0 || c->ngroup < 2 || c->shared_gpu) return false;
+  for (int g = 0; g < c->ngroup; g++) {
+    unsigned char* b = c->peer[c->group[g]];
+    if (!b) return false;
+    boxes[g] = reinterpret_cast<float*>(b + kHdr + (size_t)4 * c->max_elems * sizeof(float));
+  }
+  *ngroup = c->ngroup;
+  *me = c->group_rank;
+  *hidden = c->hidden;
+  *grid = c->engine_grid;
+  return true;
+}
+
 }  // namespace ifb
 
 using namespace ifb;
@@ -307,14 +329,32 @@ static void comm_topology(if_comm c, const if_plan* plan, int rank) {
   }
 }
 
+// Load the communicator's kernels now.  With CUDA's lazy module loading the first
+// launch of a kernel loads its module, which can wait for the device to drain: a
+// first send launched while this rank's decode engine spins on a TP peer that is not
+// running yet would then deadlock.
+static void comm_preload() {
+  static bool done = false;
+  if (done) return;
+  done = true;
+  cudaFuncAttributes fa;
+  cudaFuncGetAttributes(&fa, allreduce_kernel);
+  cudaFuncGetAttributes(&fa, send_kernel);
+  cudaFuncGetAttributes(&fa, recv_kernel);
+  cudaFuncGetAttributes(&fa, add_into_kernel);
+}
+
 extern "C" if_status if_comm_create(const if_plan* plan, int32_t rank, int64_t max_tokens, int32_t hidden, if_comm* out) {
+  comm_preload();
   if (!plan || !out) return set_error(IF_ERR_ARG, "if_comm_create: null pointer");
   if (rank < 0 || rank >= plan->devices) return set_error(IF_ERR_ARG, "if_comm_create: rank %d outside plan", rank);
   if (max_tokens < 1 || hidden < 1) return set_error(IF_ERR_SHAPE, "if_comm_create: max_tokens/hidden");
   if_comm c = new if_comm_s();
   comm_topology(c, plan, rank);
   c->max_elems = max_tokens * (int64_t)hidden;
-  const size_t bytes = kHdr + (size_t)4 * c->max_elems * sizeof(float);
+  c->hidden = hidden;
+  // [header][2 all-reduce slots][2 p2p slots][decode-engine TP exchange: 2 slots x 8 ranks x hidden]
+  const size_t bytes = kHdr + (size_t)4 * c->max_elems * sizeof(float) + (size_t)16 * hidden * sizeof(float);
   if (cudaMalloc(&c->box, bytes) != cudaSuccess || cudaMemset(c->box, 0, bytes) != cudaSuccess ||
       cudaDeviceSynchronize() != cudaSuccess) {
     delete c;
@@ -322,6 +362,28 @@ extern "C" if_status if_comm_create(const if_plan* plan, int32_t rank, int64_t m
   }
   c->peer[rank] = c->box;
   *out = c;
+  return IF_OK;
+}
+
+extern "C" if_status if_comm_create_local(const if_plan* plan, int64_t max_tokens, int32_t hidden, if_comm* outs) {
+  if (!plan || !outs) return set_error(IF_ERR_ARG, "if_comm_create_local: null pointer");
+  int sms = 0, dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  for (int r = 0; r < plan->devices; r++) {
+    if_status st = if_comm_create(plan, r, max_tokens, hidden, &outs[r]);
+    if (st) {
+      for (int q = 0; q < r; q++) if_comm_destroy(outs[q]);
+      return st;
+    }
+  }
+  for (int r = 0; r < plan->devices; r++) {
+    for (int q = 0; q < plan->devices; q++) outs[r]->peer[q] = outs[q]->box;  // same device: plain pointers
+    // every rank's engine grid co-resident on this GPU, leaving two SMs per rank for
+    // the small hand-off kernels (a 227 KB engine CTA cannot share an SM with them)
+    outs[r]->engine_grid = (sms - 2 * plan->devices) / plan->devices;
+    outs[r]->local = true;
+  }
   return IF_OK;
 }
 
@@ -342,6 +404,7 @@ extern "C" if_status if_comm_init(const if_plan* plan, int32_t rank, const uint8
   if (rank < 0 || rank >= plan->devices) return set_error(IF_ERR_ARG, "if_comm_init: rank %d outside plan", rank);
   NcclApi* a = nccl();
   if (!a) return set_error(IF_ERR_COMM, "if_comm_init: libnccl.so.2 not loadable");
+  comm_preload();
   if_comm c = new if_comm_s();
   c->kind = 1;
   comm_topology(c, plan, rank);
@@ -382,6 +445,10 @@ extern "C" if_status if_comm_open_peers(if_comm c, const uint8_t* handles) {
       return set_error(IF_ERR_COMM, "if_comm_open_peers: rank %d: %s", d, cudaGetErrorString(cudaGetLastError()));
     c->peer[d] = static_cast<unsigned char*>(p);
     c->opened[d] = true;
+    cudaPointerAttributes pa;
+    int me = -1;
+    cudaGetDevice(&me);
+    if (cudaPointerGetAttributes(&pa, p) == cudaSuccess && pa.device == me) c->shared_gpu = true;
   }
   return IF_OK;
 }

@@ -10,4 +10,5 @@ if_status comm_allreduce_into(if_comm c, const float* src, float* dst, int64_t n
 if_status comm_send(if_comm c, const float* src, int64_t n, cudaStream_t st);
 if_status comm_recv(if_comm c, float* dst, int64_t n, cudaStream_t st);
 int comm_group_size(if_comm c);
+bool comm_engine(if_comm c, float** boxes, int* ngroup, int* me, int* hidden, int* grid);
 }  // namespace ifb

@@ -359,6 +359,15 @@ __device__ __forceinline__ uint32_t ld_relaxed_u32(const uint32_t* p) {
 __device__ __forceinline__ void st_relaxed_u32(void* p, uint32_t v) {
   asm volatile("st.relaxed.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
+// system-scope relaxed accesses for the TP exchange regions (peer GPU memory over NVLink)
+__device__ __forceinline__ uint32_t ld_relaxed_sys_u32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.relaxed.sys.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed_sys_u32(void* p, uint32_t v) {
+  asm volatile("st.relaxed.sys.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
 // value with its mantissa LSB replaced by the image parity
 __device__ __forceinline__ uint32_t tagp(float v, uint32_t par) { return (__float_as_uint(v) & ~1u) | par; }
 __device__ __forceinline__ bool par4_ok(float4 v, uint32_t par) {
@@ -391,7 +400,7 @@ __device__ __forceinline__ void put_pair(float4* xsg, int xstride, const int* po
   st_relaxed_u32(f + 2 + comp, tagp(fmaf(-11.0f, xo, xe) * 38685626227668133590597632.0f, par));  // * 2^85
 }
 
-template <int XS, bool SEG>
+template <int XS, bool SEG, bool TP = false>
 __global__ void __launch_bounds__(MK_THREADS, 1) decode_mk_kernel(const __grid_constant__ MkParams P) {
   const int xstride = XS > 0 ? XS : P.xstride;  // staged input in shared memory
   const int xg = SEG ? P.xg : xstride;            // global phase images (whole K; = xstride unless segmented)
@@ -1120,6 +1129,56 @@ __global__ void __launch_bounds__(MK_THREADS, 1) decode_mk_kernel(const __grid_c
       // o / down: residual on the rows this CTA owns; sum h^2 partial for RMSNorm
       const uint32_t vh = ep * L2 + 2u * l + (kind == 1 ? 1u : 2u);
       float ss = 0.f;
+      if constexpr (TP) {
+        // tensor-parallel merge: o / down are row-parallel (K split over the
+        // group), so this CTA holds PARTIAL sums for its d-rows.  1) push them, tagged,
+        // into every group peer's exchange region (slot vh & 1, my index; NVLink peer
+        // stores); 2) gather the group's partials for the same rows from the own region
+        // (the peers pushed theirs) and sum them in rank order: every rank computes the
+        // same h, bitwise.  Slots alternate by version, and bit 1 of the version tags
+        // the data: a peer cannot write version v+2 into a slot before this CTA read v
+        // (it first needs this rank's partial v+1, pushed after that read).
+        // exchange version vx = vh + 1 >= 2: the first use of each slot (vx = 2, 3)
+        // carries tag 1, never the zero-filled region's 0
+        const uint32_t vx = vh + 1u;
+        const uint32_t tag = (vx >> 1) & 1u;
+        const size_t so = (size_t)(vx & 1u) * 8;
+        for (int rr = 2 * ct; rr < nr; rr += 2 * MK_CT) {
+#pragma unroll
+          for (int h = 0; h < 2; h++) {
+            float sacc = 0.f;
+            for (int c = 0; c < nc; c++) sacc += part[(rr + h) * nc + c];
+            const uint32_t tv = tagp(sacc, tag);
+            for (int q = 0; q < P.tp; q++)
+              st_relaxed_sys_u32(P.tp_box[q] + (so + P.tp_me) * P.tp_hidden + g.r0 + rr + h, tv);
+          }
+        }
+        for (int rr = 2 * ct; rr < nr; rr += 2 * MK_CT) {
+          float hn[2];
+#pragma unroll
+          for (int h = 0; h < 2; h++) {
+            float sacc = 0.f;
+            for (int q = 0; q < P.tp; q++) {
+              const uint32_t* src = reinterpret_cast<const uint32_t*>(P.tp_box[P.tp_me] + (so + q) * P.tp_hidden + g.r0 + rr + h);
+              uint32_t v = ld_relaxed_sys_u32(src);
+              if ((v ^ tag) & 1u) {
+                SpinGuard sg;
+                do {
+                  __nanosleep(32);
+                  sg.tick();
+                  v = ld_relaxed_sys_u32(src);
+                } while ((v ^ tag) & 1u);
+              }
+              sacc += __uint_as_float(v & ~1u);
+            }
+            hn[h] = h_own[rr + h] + sacc;
+            h_own[rr + h] = hn[h];
+            ss = fmaf(hn[h], hn[h], ss);
+            if (p == nphase - 1) P.h[g.r0 + rr + h] = hn[h];  // stage output
+          }
+          put_pair(P.xs_h, xstride, pos, g.r0 + rr, hn[0], hn[1], vh & 1u);
+        }
+      } else {
       for (int rr = 2 * ct; rr < nr; rr += 2 * MK_CT) {
         float hn[2];
 #pragma unroll
@@ -1132,6 +1191,7 @@ __global__ void __launch_bounds__(MK_THREADS, 1) decode_mk_kernel(const __grid_c
           if (p == nphase - 1) P.h[g.r0 + rr + h] = hn[h];  // stage output
         }
         put_pair(P.xs_h, xstride, pos, g.r0 + rr, hn[0], hn[1], vh & 1u);
+      }
       }
 #ifndef IFB_MK_PROF
       if (dbg && ct == 0) dbg[15] = clock64();  // epilogue rows done (before the sum-h^2 reduction)
@@ -1192,7 +1252,8 @@ static int part_need(int N, int K, int G) {
 constexpr int MK_SEG_NB = 192;
 
 if_status mk_launch(MkParams& P, cudaStream_t st) {
-  const int G = mk_sms();
+  int G = P.grid > 0 ? std::min(P.grid, mk_sms()) : mk_sms();
+  if (const char* e = getenv("IFB_MK_GRID")) G = std::max(1, std::min(atoi(e), G));  // experiments only
   int nbp_max = 0, part_max = 0;
   if (P.mode == MK_MODE_GEMV) {
     nbp_max = nbp_of(P.gemv_K);
@@ -1207,7 +1268,10 @@ if_status mk_launch(MkParams& P, cudaStream_t st) {
   }
   // global images span the whole K; the shared-memory stage spans one K-segment
   P.xg = mk_xstride(nbp_max);
-  P.seg_nb = nbp_max > 224 ? MK_SEG_NB : 0;
+#ifndef IFB_MK_SEG_MIN
+#define IFB_MK_SEG_MIN 224
+#endif
+  P.seg_nb = nbp_max > IFB_MK_SEG_MIN ? MK_SEG_NB : 0;
   if (P.seg_nb) nbp_max = P.seg_nb;
   P.nbp_max = nbp_max;
   P.raw_max = 0;  // (no raw-input buffer: plain inputs are staged from global memory)
@@ -1223,7 +1287,14 @@ if_status mk_launch(MkParams& P, cudaStream_t st) {
   const size_t smem = (size_t)nslot * MK_SLOT + fixed;
   P.xstride = mk_xstride(nbp_max);
   void (*kern)(MkParams);
-  if (P.seg_nb) {  // K-segmented phases (70B down; GEMV with K > 14336)
+  if (P.mode == MK_MODE_STACK && P.tp > 1) {  // in-engine TP merges (whole-K phases)
+    if (P.seg_nb || P.tp > 8 || !P.tp_box[P.tp_me]) return IF_ERR_UNSUPPORTED;
+    switch (P.xstride) {
+      case 137: kern = decode_mk_kernel<137, false, true>; break;  // 13B TP2, 70B TP4/8
+      case 233: kern = decode_mk_kernel<233, false, true>; break;  // 70B TP2
+      default: kern = decode_mk_kernel<0, false, true>; break;
+    }
+  } else if (P.seg_nb) {  // K-segmented phases (70B down; GEMV with K > 14336)
     kern = P.xstride == 201 ? decode_mk_kernel<201, true> : decode_mk_kernel<0, true>;
   } else {
     switch (P.xstride) {
@@ -1234,12 +1305,12 @@ if_status mk_launch(MkParams& P, cudaStream_t st) {
       default: kern = decode_mk_kernel<0, false>; break;
     }
   }
-  static void (*configured[8])(MkParams) = {};
+  static void (*configured[16])(MkParams) = {};
   bool done_cfg = false;
-  for (int i = 0; i < 8 && configured[i]; i++) done_cfg |= configured[i] == kern;
+  for (int i = 0; i < 16 && configured[i]; i++) done_cfg |= configured[i] == kern;
   if (!done_cfg) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)budget);
-    for (int i = 0; i < 8; i++)
+    for (int i = 0; i < 16; i++)
       if (!configured[i]) {
         configured[i] = kern;
         break;

@@ -37,6 +37,12 @@ struct MkParams {
   // filled by mk_launch
   int nslot, nbp_max, raw_max, xstride;  // nbp_max / xstride: the staged input in shared memory (one K-segment)
   int xg;      // float4 row stride of the global phase images (whole K)
+  // tensor parallelism inside the engine ("merged twice"): the o / down
+  // epilogues push their partial rows to every group peer's exchange region and sum
+  // the group's partials in rank order (bit-identical on every rank).  tp = 1: off.
+  int tp, tp_me, tp_hidden;
+  float* tp_box[8];  // exchange regions of the group members (group-rank order; [me] = own)
+  int grid;          // CTAs per launch (0 = one per SM); ranks sharing one GPU split the SMs
   int seg_nb;  // K-segment length in 64-blocks (multiple of 32); 0 = whole rows
   unsigned long long* dbg;  // nullable: per-CTA %globaltimer stamps [G][nphase][8] (instrumentation)
   const uint8_t* w[MK_MAXL][4];  // qkv, o, gu (gate/up rows interleaved), down per layer

@@ -336,7 +336,13 @@ static if_status run_stack(const if_stack_shape* shape, const if_plan* plan, int
   // batch-1 Q3H_B64 decode on one TP rank: the whole stage in ONE persistent launch
   // (batch 2..6: one engine launch per token beats the tensor-core path, whose
   //  per-launch cost dominates at small B; both stream the weights from HBM)
-  const bool mk = mode == IF_DECODE && T <= 6 && sc.type == IF_Q3H && sc.block == 64 && groups == 1 &&
+  // tensor parallelism: the engine merges the o / down partials itself over the
+  // communicator's exchange regions (peer memory); NCCL communicators take the
+  // per-layer path below
+  float* tp_boxes[8] = {nullptr};
+  int tp_n = 1, tp_me = 0, tp_hidden = 0, tp_grid = 0;
+  const bool tp_ok = groups == 1 || (comm_engine(comm, tp_boxes, &tp_n, &tp_me, &tp_hidden, &tp_grid) && tp_hidden >= L.d);
+  const bool mk = mode == IF_DECODE && T <= 6 && sc.type == IF_Q3H && sc.block == 64 && tp_ok &&
                   nlayers <= MK_MAXL && nlayers > 0 && !kvr;
   if (mk) {
     static thread_local MkParams P;
@@ -367,6 +373,11 @@ static if_status run_stack(const if_stack_shape* shape, const if_plan* plan, int
       P.ssq = reinterpret_cast<float*>(P.xs_act + img);
     }
     P.dbg = g_mk_dbg;
+    P.tp = groups > 1 ? tp_n : 1;
+    P.tp_me = tp_me;
+    P.tp_hidden = tp_hidden;
+    for (int q = 0; q < 8; q++) P.tp_box[q] = tp_boxes[q];
+    P.grid = comm ? tp_grid : 0;
     for (int l = 0; l < nlayers; l++) {
       const if_layer_weights& Wl = stage_layers[l];
       if (!Wl.wqkv || !Wl.wo || !Wl.wgu || !Wl.wdown) return set_error(IF_ERR_ARG, "if_run_stack: null weights, layer %d", l);
