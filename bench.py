@@ -293,7 +293,10 @@ def run_ours(args):
     if args.strategy == "auto":  # N > 1: hybrid (Table 4) where the grid allows it, else TP
         args.strategy = "hybrid" if ws >= 4 else "tensor"
     cfg = synth.LLAMA[args.model]
-    s = F.scheme("Q3H", 64)
+    qname, qblock = args.scheme.split("_B")
+    s = F.scheme(qname, int(qblock))
+    bpw = F.if_bits_per_weight(s)
+    scheme_str = f"{args.scheme} ({bpw[0] / bpw[1]:g} bits/weight)"
     shape = F.stack_shape(cfg["layers"], cfg["hidden"], cfg["heads"], cfg["kv_heads"], cfg["head_dim"], cfg["ffn"], s)
     if ws == 1:
         plan = F.if_plan_partition(F.IF_BY_LAYER, shape, 1)
@@ -449,9 +452,9 @@ def run_ours(args):
             "peak_kind": f"{peak_kind} copy bandwidth (MEASURED_PEAKS.json hbm_gbs)",
             "traffic": None, "avg_launch_us": ms_per_step * 1e3 / max(1, launches_mk),
             "algorithmic_bytes_per_launch": rank_bytes // max(1, launches_mk),
-            "algorithmic_bytes": "packed weight bytes (0.5 B/weight incl. two fp16 per 64-block)"}
+            "algorithmic_bytes": f"packed weight bytes of {args.scheme} (incl. two fp16 per block)"}
     prof_path = os.path.join(ROOT, "profiles", "decode_mk_traffic.json")
-    if os.path.exists(prof_path):
+    if os.path.exists(prof_path) and args.scheme == "Q3H_B64" and args.model == "7b" and B == 1 and ws == 1:
         try:
             with open(prof_path) as f:
                 roof["traffic"] = json.load(f).get("dram_bytes_per_launch")
@@ -465,8 +468,8 @@ def run_ours(args):
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
             "scaling": "strong" if ws > 1 else "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (counter-based Irwin-Hall weights sigma=1/sqrt(d), activations sigma=1)",
-            "config": {"workload": f"llama2-{args.model}-stack q3h_b64 decode b={B}", "model": f"llama2-{args.model}-shaped",
-                       "global_batch": B, "seq_len": 1, "parallelism": strategy, "scheme": "Q3H_B64 (4.0 bits/weight)",
+            "config": {"workload": f"llama2-{args.model}-stack {args.scheme.lower()} decode b={B}", "model": f"llama2-{args.model}-shaped",
+                       "global_batch": B, "seq_len": 1, "parallelism": strategy, "scheme": scheme_str,
                        "comm": (args.comm if ws > 1 else None),
                        "weight_bytes_per_step": total_bytes,
                        "l2": f"inputs larger than L2 ({total_bytes / 1e9:.2f} GB of weights per step vs 126 MB L2)"},
@@ -497,6 +500,7 @@ def main():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--batch", type=int, default=1)
+    ap.add_argument("--scheme", default="Q3H_B64", help="Q3H_B64 (3.5-bit, BASELINE) or Q2/Q3/Q4/Q5/Q6/Q8 _B32/_B64")
     # default: 7B (BASELINE configs[1]) at N = 1; north_star's 70B stack at N > 1
     ap.add_argument("--model", default=None, choices=["7b", "13b", "70b"])
     # N > 1 default (auto): hybrid stages x TP (Table 4) at N >= 4 (2 x N/2), TP at N = 2
