@@ -27,11 +27,13 @@
 #include <stdlib.h>
 
 #include <algorithm>
+#include <utility>
 
 #include "common.cuh"
 #include "decode_mk.cuh"
 #include "pipe.cuh"
 #include "simd.cuh"
+#include "mk_scheme.cuh"
 
 namespace ifb {
 
@@ -68,32 +70,34 @@ struct Geo {
 // exceeds seg_nb blocks (70B down: K = 28672) runs in K-segments of seg_nb blocks
 // (a multiple of 32: whole chunks), so the staged input in shared memory and the
 // ring slots stay small; segment s covers blocks [s seg_nb, min(nb, (s+1) seg_nb)).
+template <int BS = 64>
 __device__ __forceinline__ int phase_nseg(int K, int seg_nb) {
-  const int nb = K >> 6;
+  const int nb = BS == 64 ? K >> 6 : K >> 5;
   return seg_nb > 0 ? (nb + seg_nb - 1) / seg_nb : 1;
 }
+template <int BS = 64, int BB = 32, int RMAX = MK_RMAX>
 __device__ __forceinline__ Geo phase_geo(int N, int K, int G, int cta, int unit, int seg_nb = 0, int sgi = 0) {
   Geo g;
   g.N = N;
   g.K = K;
-  const int nb_all = K >> 6;
+  const int nb_all = BS == 64 ? K >> 6 : K >> 5;
   g.nchunk_all = (nb_all + 31) >> 5;
-  g.full_row_bytes = nb_all * 32;
+  g.full_row_bytes = nb_all * BB;
   g.b0 = seg_nb > 0 ? sgi * seg_nb : 0;
   g.nb = seg_nb > 0 ? min(seg_nb, nb_all - g.b0) : nb_all;
   g.coff = g.b0 >> 5;
   g.nchunk = (g.nb + 31) >> 5;
   g.nbp = g.nchunk << 5;
-  g.row_bytes = g.nb * 32;
+  g.row_bytes = g.nb * BB;
   const int units = N / unit;
   const int base = units / G, rem = units % G;
   g.r0 = (cta * base + min(cta, rem)) * unit;
   g.r1 = g.r0 + (base + (cta < rem ? 1 : 0)) * unit;
   int rps = MK_SLOT / g.row_bytes;
-  if (MK_RMAX >= 8 && rps >= 8) {
+  if (RMAX >= 8 && rps >= 8) {
     g.R = 8;
     rps &= ~7;
-  } else if (rps >= 4) {
+  } else if (RMAX >= 4 && rps >= 4) {
     g.R = 4;
     rps &= ~3;
   } else if (rps >= 2) {
@@ -287,6 +291,119 @@ __device__ __forceinline__ void mk_unit_dispatch(const unsigned char* slot_rows,
     mk_unit<R, XS, false>(slot_rows, row_bytes, nrows_valid, c, nb, xs_rt, xs, bs, part_rows, nchunk, kc);
 }
 
+template <int W, int BS, int NWP, int NV, int... V>
+__device__ __forceinline__ void gk_views(std::integer_sequence<int, V...>, const uint32_t (&w)[NWP], uint32_t (&vw)[NV]) {
+  ((vw[V] = gk_view<W, BS, V>(w)), ...);
+}
+// quad J of a k-bit unit: codes 4J..4J+3 of R rows against the staged X of quad J
+template <int W, int BS, int R, int NWP, int NV, int J, int... I>
+__device__ __forceinline__ void gk_quad(std::integer_sequence<int, I...>, const float4& xv, const uint32_t (&wv)[R][NWP],
+                                        const uint32_t (&vw)[R][NV], u64 (&acc)[R / 2][2]) {
+  const float xc[4] = {xv.x, xv.y, xv.z, xv.w};
+  (
+      [&] {
+        constexpr int K = 4 * J + I;
+        const u64 x2 = pack2(xc[I], xc[I]);
+#pragma unroll
+        for (int ip = 0; ip < R / 2; ip++) {
+          const u64 cf = pack2(__uint_as_float(gk_code_bits<W, BS, K>(wv[2 * ip], vw[2 * ip])),
+                               __uint_as_float(gk_code_bits<W, BS, K>(wv[2 * ip + 1], vw[2 * ip + 1])));
+          acc[ip][K & 1] = ffma2(cf, x2, acc[ip][K & 1]);
+        }
+      }(),
+      ...);
+}
+template <int W, int BS, int R, int NWP, int NV, int... J>
+__device__ __forceinline__ void gk_quads(std::integer_sequence<int, J...>, const float4* xa, int xstride, float4& xn,
+                                         const uint32_t (&wv)[R][NWP], const uint32_t (&vw)[R][NV],
+                                         u64 (&acc)[R / 2][2]) {
+  constexpr int NQ = sizeof...(J);
+  (
+      [&] {
+        const float4 xv = xn;
+        if constexpr (J + 1 < NQ) xn = xa[(J + 1) * xstride];  // prefetch the next quad
+        gk_quad<W, BS, R, NWP, NV, J>(std::make_integer_sequence<int, 4>{}, xv, wv, vw, acc);
+      }(),
+      ...);
+}
+
+// ---- k-bit schemes (mk_scheme.cuh): one unit = R rows x one 32-block chunk ----------
+// Lane = block b of the chunk; X_k = x_k 2^(85 - s_k) staged as quads of 4 codes.
+template <int W, int BS, int R, int XS, bool FULL>
+__device__ __forceinline__ void gk_unit(const unsigned char* slot_rows, int row_bytes, int nrows_valid, int c, int nb,
+                                        int xs_rt, const float4* xs, const float2* bs, float* part_rows, int nchunk) {
+  using S = GkScheme<W, BS>;
+  static_assert(R % 2 == 0, "rows are paired in FFMA2 lanes");
+  constexpr int NW = S::NW, NV = S::NV > 0 ? S::NV : 1;
+  const int lane = threadIdx.x & 31;
+  const int b = c * 32 + lane;
+  const bool active = FULL || b < nb;
+  const int xstride = XS > 0 ? XS : xs_rt;
+  uint32_t wv[R][NW + 1];
+#pragma unroll
+  for (int i = 0; i < R; i++) {
+    const bool ok = FULL || (active && i < nrows_valid);
+    const unsigned char* a = slot_rows + i * row_bytes + b * S::BB;
+    if constexpr (S::BB % 16 == 0) {
+#pragma unroll
+      for (int q = 0; q < NW / 4; q++) {
+        uint4 v = ok ? reinterpret_cast<const uint4*>(a)[q] : make_uint4(0u, 0u, 0u, 0u);
+        wv[i][4 * q] = v.x; wv[i][4 * q + 1] = v.y; wv[i][4 * q + 2] = v.z; wv[i][4 * q + 3] = v.w;
+      }
+    } else {
+#pragma unroll
+      for (int q = 0; q < NW; q++) wv[i][q] = ok ? reinterpret_cast<const uint32_t*>(a)[q] : 0u;
+    }
+    wv[i][NW] = 0u;
+  }
+  uint32_t vw[R][NV];
+#pragma unroll
+  for (int i = 0; i < R; i++) gk_views<W, BS>(std::make_integer_sequence<int, S::NV>{}, wv[i], vw[i]);
+  u64 acc[R / 2][2];
+#pragma unroll
+  for (int i = 0; i < R / 2; i++) acc[i][0] = acc[i][1] = 0ull;
+  const float4* xa = xs + b;
+  float4 xn = xa[0];
+  gk_quads<W, BS, R, NW + 1, NV>(std::make_integer_sequence<int, S::NQ>{}, xa, xstride, xn, wv, vw, acc);
+  const float sx = bs[b].x;
+  float v[R];
+#pragma unroll
+  for (int ip = 0; ip < R / 2; ip++) {
+    const float2 a0 = unpack2(acc[ip][0]), a1 = unpack2(acc[ip][1]);
+#pragma unroll
+    for (int h = 0; h < 2; h++) {
+      const int i = 2 * ip + h;
+      const float lo = half_bits_to_float(wv[i][0] & 0xFFFFu);
+      const float hi = half_bits_to_float(wv[i][0] >> 16);
+      // Eq. 2: step = (hi - lo) / D; 2^64 undoes the accumulator scale
+      const float step = (hi - lo) * (18446744073709551616.0f / (float)S::D);
+      const float sq = h ? (a0.y + a1.y) : (a0.x + a1.x);
+      v[i] = active ? fmaf(step, sq, lo * sx) : 0.f;
+    }
+  }
+  const float sum = warp_rows_sum<R>(v);
+  constexpr int SH = R == 8 ? 2 : (R == 4 ? 3 : (R == 2 ? 4 : 5));
+  const int row = lane >> SH;
+  if ((lane & ((1 << SH) - 1)) == 0 && (FULL || row < nrows_valid)) part_rows[row * nchunk + c] = sum;
+}
+
+// scheme-dispatched pieces of the engine: QT = 35 is the paper's 3.5-bit pair code
+// (the subnormal-form pair decode above), QT = k a k-bit scheme (mk_scheme.cuh)
+template <int QT, int BS, int R, int XS>
+__device__ __forceinline__ void sk_unit_dispatch(const unsigned char* slot_rows, int row_bytes, int nrows_valid, int c,
+                                                 int nb, int xs_rt, const float4* xs, const float2* bs,
+                                                 float* part_rows, int nchunk, const Q3HConst& kc) {
+  if constexpr (QT == 35) {
+    mk_unit_dispatch<R, XS>(slot_rows, row_bytes, nrows_valid, c, nb, xs_rt, xs, bs, part_rows, nchunk, kc);
+  } else {
+    constexpr int RR = R > GkScheme<QT, BS>::RMAX ? GkScheme<QT, BS>::RMAX : R;
+    if (nrows_valid >= RR && (c + 1) * 32 <= nb)
+      gk_unit<QT, BS, RR, XS, true>(slot_rows, row_bytes, nrows_valid, c, nb, xs_rt, xs, bs, part_rows, nchunk);
+    else
+      gk_unit<QT, BS, RR, XS, false>(slot_rows, row_bytes, nrows_valid, c, nb, xs_rt, xs, bs, part_rows, nchunk);
+  }
+}
+
 // code bit position s_j of pair j (simd.cuh kQ3hSrc), for the per-pair x scaling;
 // copied to shared memory at kernel start (lanes index it with different j)
 __device__ const int kQ3hPosTab[32] = {0, 7, 14, 0, 7, 3, 10, 17, 0, 7, 6, 13, 0, 7, 2, 9,
@@ -323,6 +440,49 @@ __device__ __forceinline__ float mk_rms_inv(float ss, float* red, int K, int cw,
 #pragma unroll
   for (int w = 0; w < MK_NC; w++) tot += red[w];
   return 1.0f / sqrtf(tot / (float)K + 1e-5f);
+}
+
+// ---- scheme-dispatched staging (sk_*): QT = 35 the pair transform above, else X_k ----
+template <int QT, int BS>
+struct SkTraits {  // staged quads per block, block bytes, code positions kept in shared memory
+  static constexpr int NQ = QT == 35 ? 16 : BS / 4;
+  static constexpr int BB = QT == 35 ? 32 : GkScheme<QT, BS>::BB;
+  static constexpr int NPOS = QT == 35 ? 32 : BS;
+  static constexpr int RMAX = QT == 35 ? MK_RMAX : GkScheme<QT, BS>::RMAX;
+};
+
+// k-bit stage: quad q = weights 4q..4q+3 of the input -> X_k = x_k 2^(85 - s_k)
+template <int QT, int BS>
+__device__ __forceinline__ void sk_stage_quad(int q, float4 v, int xstride, float4* xs, float2* bs, const int* pos) {
+  if constexpr (QT == 35) {
+    stage_quad(q, v, xstride, xs, bs, pos);
+  } else {
+    constexpr int NQ = BS / 4;
+    const int b = q / NQ, jj = q % NQ;
+    const int* p = pos + 4 * jj;
+    xs[jj * xstride + b] = make_float4(v.x * __uint_as_float((uint32_t)(127 + 85 - p[0]) << 23),
+                                       v.y * __uint_as_float((uint32_t)(127 + 85 - p[1]) << 23),
+                                       v.z * __uint_as_float((uint32_t)(127 + 85 - p[2]) << 23),
+                                       v.w * __uint_as_float((uint32_t)(127 + 85 - p[3]) << 23));
+    float sx = (v.x + v.y) + (v.z + v.w);
+#pragma unroll
+    for (int o = NQ / 2; o > 0; o >>= 1) sx += __shfl_xor_sync(0xffffffffu, sx, o);
+    if (jj == 0) bs[b] = make_float2(sx, 0.f);
+  }
+}
+
+// sum of the four x values a staged quad jj encodes (image staging: the block sums)
+template <int QT, int BS>
+__device__ __forceinline__ float sk_quad_sum(float4 w, int jj, const int* pos) {
+  if constexpr (QT == 35) {
+    const float c0 = __uint_as_float((uint32_t)(127 - 85 + pos[2 * jj]) << 23);  // 2^(s - 85)
+    const float c1 = __uint_as_float((uint32_t)(127 - 85 + pos[2 * jj + 1]) << 23);
+    return (w.z + w.w) * 2.5849394142282115e-26f + 12.0f * (w.x * c0 + w.y * c1);
+  } else {
+    const int* p = pos + 4 * jj;
+    return (w.x * __uint_as_float((uint32_t)(127 - 85 + p[0]) << 23) + w.y * __uint_as_float((uint32_t)(127 - 85 + p[1]) << 23)) +
+           (w.z * __uint_as_float((uint32_t)(127 - 85 + p[2]) << 23) + w.w * __uint_as_float((uint32_t)(127 - 85 + p[3]) << 23));
+  }
 }
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -400,8 +560,23 @@ __device__ __forceinline__ void put_pair(float4* xsg, int xstride, const int* po
   st_relaxed_u32(f + 2 + comp, tagp(fmaf(-11.0f, xo, xe) * 38685626227668133590597632.0f, par));  // * 2^85
 }
 
-template <int XS, bool SEG, bool TP = false>
+template <int QT, int BS>
+__device__ __forceinline__ void sk_put_pair(float4* xsg, int xstride, const int* pos, int k, float xe, float xo,
+                                            uint32_t par) {
+  if constexpr (QT == 35) {
+    put_pair(xsg, xstride, pos, k, xe, xo, par);
+  } else {
+    // elements k, k+1 (k even) -> components k % 4, k % 4 + 1 of quad (k % BS) / 4 of block k / BS
+    const int b = k / BS, kk = k % BS, jj = kk >> 2, comp = kk & 3;
+    float* f = reinterpret_cast<float*>(xsg + jj * xstride + b) + comp;
+    st_relaxed_u32(f, tagp(xe * __uint_as_float((uint32_t)(127 + 85 - pos[kk]) << 23), par));
+    st_relaxed_u32(f + 1, tagp(xo * __uint_as_float((uint32_t)(127 + 85 - pos[kk + 1]) << 23), par));
+  }
+}
+
+template <int XS, bool SEG, bool TP = false, int QT = 35, int BS = 64>
 __global__ void __launch_bounds__(MK_THREADS, 1) decode_mk_kernel(const __grid_constant__ MkParams P) {
+  using SK = SkTraits<QT, BS>;
   const int xstride = XS > 0 ? XS : P.xstride;  // staged input in shared memory
   const int xg = SEG ? P.xg : xstride;            // global phase images (whole K; = xstride unless segmented)
   extern __shared__ __align__(1024) unsigned char smem[];
@@ -412,10 +587,10 @@ __global__ void __launch_bounds__(MK_THREADS, 1) decode_mk_kernel(const __grid_c
   uint64_t* empty = full + MK_MAXSLOT;
   float* red = reinterpret_cast<float*>(empty + MK_MAXSLOT);  // [MK_NC] + scalars
   float4* xs = reinterpret_cast<float4*>(smem + (size_t)nslot * MK_SLOT + 2 * MK_MAXSLOT * 8 + 128);
-  float2* bs = reinterpret_cast<float2*>(xs + 16 * xstride);
+  float2* bs = reinterpret_cast<float2*>(xs + SK::NQ * xstride);
   float* h_own = reinterpret_cast<float*>(bs + P.nbp_max);    // [MK_MAXOWN] this CTA's residual rows
   int* pos = reinterpret_cast<int*>(h_own + MK_MAXOWN);       // [32] code positions
-  float* ssq_s = reinterpret_cast<float*>(pos + 32);          // [MK_MAXG] sum h^2 partials
+  float* ssq_s = reinterpret_cast<float*>(pos + SK::NPOS);          // [MK_MAXG] sum h^2 partials
   float* part = ssq_s + MK_MAXG;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -426,7 +601,13 @@ __global__ void __launch_bounds__(MK_THREADS, 1) decode_mk_kernel(const __grid_c
     }
     fence_mbar_init();
   }
-  if (threadIdx.x < 32) pos[threadIdx.x] = kQ3hPosTab[threadIdx.x];
+  if constexpr (QT == 35) {
+    if (threadIdx.x < 32) pos[threadIdx.x] = kQ3hPosTab[threadIdx.x];
+  } else {
+    [&]<int... K>(std::integer_sequence<int, K...>) {
+      ((threadIdx.x == K ? (void)(pos[K] = GkSrc<QT, BS, K>::pos) : (void)0), ...);
+    }(std::make_integer_sequence<int, BS>{});
+  }
   __syncthreads();
   const bool stack = P.mode == MK_MODE_STACK;
   const int nphase = stack ? 4 * P.layers : 1;
@@ -445,9 +626,9 @@ __global__ void __launch_bounds__(MK_THREADS, 1) decode_mk_kernel(const __grid_c
         const uint8_t* W;
         int N, K, kind;
         phase_dims(P, p, &W, &N, &K, &kind);
-        const int nseg = SEG ? phase_nseg(K, P.seg_nb) : 1;
+        const int nseg = SEG ? phase_nseg<BS>(K, P.seg_nb) : 1;
         for (int sgi = 0; sgi < nseg; sgi++) {
-          const Geo g = phase_geo(N, K, G, cta, unit, SEG && nseg > 1 ? P.seg_nb : 0, sgi);
+          const Geo g = phase_geo<BS, SK::BB, SK::RMAX>(N, K, G, cta, unit, SEG && nseg > 1 ? P.seg_nb : 0, sgi);
           for (int r = g.r0; r < g.r1; r += g.rps) {
             const int n = min(g.rps, g.r1 - r);
             const uint32_t bytes = (uint32_t)n * g.row_bytes;
@@ -463,7 +644,7 @@ __global__ void __launch_bounds__(MK_THREADS, 1) decode_mk_kernel(const __grid_c
             } else {  // a K-segment of each row: one copy per row
               for (int i = 0; i < n; i++)
                 bulk_g2s(ring + (size_t)slot * MK_SLOT + (size_t)i * g.row_bytes,
-                         W + (size_t)(r + i) * g.full_row_bytes + (size_t)g.b0 * 32, (uint32_t)g.row_bytes,
+                         W + (size_t)(r + i) * g.full_row_bytes + (size_t)g.b0 * SK::BB, (uint32_t)g.row_bytes,
                          &full[slot], pol);
             }
             if (++slot == (uint32_t)nslot) {
@@ -488,7 +669,7 @@ __global__ void __launch_bounds__(MK_THREADS, 1) decode_mk_kernel(const __grid_c
   const uint32_t L2 = 2u * (uint32_t)P.layers;
   if (stack) {
     // residual rows of this CTA (the o/down row split) from the stage input
-    const Geo go = phase_geo(P.d, P.nq, G, cta, unit);
+    const Geo go = phase_geo<BS, SK::BB, SK::RMAX>(P.d, P.nq, G, cta, unit);
     for (int i = ct; i < go.r1 - go.r0; i += MK_CT) h_own[i] = P.h[go.r0 + i];
   }
   for (int p = 0; p < nphase; p++) {
@@ -496,7 +677,7 @@ __global__ void __launch_bounds__(MK_THREADS, 1) decode_mk_kernel(const __grid_c
     const uint8_t* W;
     int N, K, kind;
     phase_dims(P, p, &W, &N, &K, &kind);
-    const int nseg = SEG ? phase_nseg(K, P.seg_nb) : 1;
+    const int nseg = SEG ? phase_nseg<BS>(K, P.seg_nb) : 1;
     (void)W;
     unsigned long long* dbg = P.dbg ? P.dbg + ((size_t)cta * nphase + p) * 16 : nullptr;
     if (dbg && ct == 0) { dbg[0] = gtimer(); dbg[8] = clock64(); }
@@ -570,7 +751,7 @@ __global__ void __launch_bounds__(MK_THREADS, 1) decode_mk_kernel(const __grid_c
     }
     float plain_inv = 1.f;
     for (int sgi = 0; sgi < nseg; sgi++) {
-    const Geo g = phase_geo(N, K, G, cta, unit, SEG && nseg > 1 ? P.seg_nb : 0, sgi);
+    const Geo g = phase_geo<BS, SK::BB, SK::RMAX>(N, K, G, cta, unit, SEG && nseg > 1 ? P.seg_nb : 0, sgi);
     if (sgi > 0) named_bar_sync(1, MK_CT);  // every warp is done with the previous segment's xs
     if (from_image) {
       // 3. four threads per block b, four quads each: load the image words straight
@@ -578,19 +759,20 @@ __global__ void __launch_bounds__(MK_THREADS, 1) decode_mk_kernel(const __grid_c
       //    every word's parity (re-read the late ones), strip it, stage the quads in
       //    shared memory and form the block sum of x (x_e + x_o = xe' + 12 x_o in
       //    transformed terms)
-      for (int t0 = cw * 32; t0 < 4 * g.nbp; t0 += 2 * MK_CT) {
+      constexpr int TPB = SK::NQ / 4, TPB_LOG = TPB == 4 ? 2 : 1;  // threads per block, 4 quads each
+      for (int t0 = cw * 32; t0 < TPB * g.nbp; t0 += 2 * MK_CT) {
         float4 v[2][4];
 #pragma unroll
         for (int u = 0; u < 2; u++) {
-          const int t = t0 + u * MK_CT + lane, b = t >> 2, j4 = t & 3;
+          const int t = t0 + u * MK_CT + lane, b = t >> TPB_LOG, j4 = t & (TPB - 1);
 #pragma unroll
           for (int i = 0; i < 4; i++)
             v[u][i] = b < g.nb ? ld_relaxed_f4(img + (4 * j4 + i) * xg + g.b0 + b) : make_float4(0.f, 0.f, 0.f, 0.f);
         }
 #pragma unroll
         for (int u = 0; u < 2; u++) {
-          if (t0 + u * MK_CT >= 4 * g.nbp) break;  // warp-uniform
-          const int t = t0 + u * MK_CT + lane, b = t >> 2, j4 = t & 3;
+          if (t0 + u * MK_CT >= TPB * g.nbp) break;  // warp-uniform
+          const int t = t0 + u * MK_CT + lane, b = t >> TPB_LOG, j4 = t & (TPB - 1);
           float sx = 0.f;
           if (b < g.nb) {
 #pragma unroll
@@ -609,13 +791,11 @@ __global__ void __launch_bounds__(MK_THREADS, 1) decode_mk_kernel(const __grid_c
               const float4 w = make_float4(__uint_as_float(__float_as_uint(q.x) & ~1u), __uint_as_float(__float_as_uint(q.y) & ~1u),
                                            __uint_as_float(__float_as_uint(q.z) & ~1u), __uint_as_float(__float_as_uint(q.w) & ~1u));
               xs[jj * xstride + b] = w;
-              const float c0 = __uint_as_float((uint32_t)(127 - 85 + pos[2 * jj]) << 23);  // 2^(s - 85)
-              const float c1 = __uint_as_float((uint32_t)(127 - 85 + pos[2 * jj + 1]) << 23);
-              sx += (w.z + w.w) * 2.5849394142282115e-26f + 12.0f * (w.x * c0 + w.y * c1);
+              sx += sk_quad_sum<QT, BS>(w, jj, pos);
             }
           }
           sx += __shfl_xor_sync(0xffffffffu, sx, 1);
-          sx += __shfl_xor_sync(0xffffffffu, sx, 2);
+          if constexpr (TPB > 2) sx += __shfl_xor_sync(0xffffffffu, sx, 2);
           if (j4 == 0 && b < g.nbp) bs[b] = make_float2(sx, 0.f);
         }
       }
@@ -628,8 +808,8 @@ __global__ void __launch_bounds__(MK_THREADS, 1) decode_mk_kernel(const __grid_c
       // transformed quads; no shared-memory copy of the raw vector, so the largest
       // shapes (70B: K up to 28672) fit.  RMSNorm needs the global sum of squares
       // first: quads stay in registers when they fit, else they are re-read.
-      const float4* src4 = reinterpret_cast<const float4*>(stack ? P.h : P.x_in) + (size_t)g.b0 * 16;
-      const int nq = K >> 2, nqs = g.nb * 16, nqp = g.nbp * 16;
+      const float4* src4 = reinterpret_cast<const float4*>(stack ? P.h : P.x_in) + (size_t)g.b0 * (BS / 4);
+      const int nq = K >> 2, nqs = g.nb * SK::NQ, nqp = g.nbp * SK::NQ;
       if (rms && nseg == 1 && nqp <= MK_MAXQ * MK_CT) {
         float4 v[MK_MAXQ];
         float ss = 0.f;
@@ -645,7 +825,7 @@ __global__ void __launch_bounds__(MK_THREADS, 1) decode_mk_kernel(const __grid_c
           if (i * MK_CT + (ct & ~31) < nqp) {  // per-warp (nqp is a multiple of 32)
             const float4 a = v[i];
             const float inv = plain_inv;
-            stage_quad(ct + i * MK_CT, make_float4(a.x * inv, a.y * inv, a.z * inv, a.w * inv), xstride, xs, bs, pos);
+            sk_stage_quad<QT, BS>(ct + i * MK_CT, make_float4(a.x * inv, a.y * inv, a.z * inv, a.w * inv), xstride, xs, bs, pos);
           }
       } else {
         if (rms && sgi == 0) {
@@ -661,7 +841,7 @@ __global__ void __launch_bounds__(MK_THREADS, 1) decode_mk_kernel(const __grid_c
         for (int q = ct; q < nqp; q += MK_CT) {
           float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
           if (q < nqs) a = src4[q];
-          stage_quad(q, make_float4(a.x * inv, a.y * inv, a.z * inv, a.w * inv), xstride, xs, bs, pos);
+          sk_stage_quad<QT, BS>(q, make_float4(a.x * inv, a.y * inv, a.z * inv, a.w * inv), xstride, xs, bs, pos);
         }
       }
       if (dbg && ct == 0) { dbg[2] = gtimer(); dbg[10] = clock64(); }
@@ -720,11 +900,11 @@ __global__ void __launch_bounds__(MK_THREADS, 1) decode_mk_kernel(const __grid_c
             float* pr = part + (size_t)(sl * g.rps + i0) * g.nchunk_all + g.coff;
             const unsigned char* ua = sbase + (size_t)i0 * g.row_bytes;
             if (MK_RMAX >= 8 && g.R == 8)
-              mk_unit_dispatch<MK_RMAX >= 8 ? 8 : 4, XS>(ua, g.row_bytes, n - i0, c, g.nb, xstride, xs, bs, pr, g.nchunk_all, kc);
+              sk_unit_dispatch<QT, BS, MK_RMAX >= 8 ? 8 : 4, XS>(ua, g.row_bytes, n - i0, c, g.nb, xstride, xs, bs, pr, g.nchunk_all, kc);
             else if (g.R == 4)
-              mk_unit_dispatch<4, XS>(ua, g.row_bytes, n - i0, c, g.nb, xstride, xs, bs, pr, g.nchunk_all, kc);
+              sk_unit_dispatch<QT, BS, 4, XS>(ua, g.row_bytes, n - i0, c, g.nb, xstride, xs, bs, pr, g.nchunk_all, kc);
             else
-              mk_unit_dispatch<2, XS>(ua, g.row_bytes, n - i0, c, g.nb, xstride, xs, bs, pr, g.nchunk_all, kc);
+              sk_unit_dispatch<QT, BS, 2, XS>(ua, g.row_bytes, n - i0, c, g.nb, xstride, xs, bs, pr, g.nchunk_all, kc);
           }
         }
         u0 = u - U;  // continue the round-robin in the next slot
@@ -744,7 +924,7 @@ __global__ void __launch_bounds__(MK_THREADS, 1) decode_mk_kernel(const __grid_c
     if (dbg && ct == 0) { dbg[4] = gtimer(); dbg[12] = clock64(); }
     // ---- 4. combine chunks (fixed order) + epilogue.  Outputs feeding the next
     //         phase are written pre-transformed (put_pair) into its xs image. ----
-    const Geo g = phase_geo(N, K, G, cta, unit);  // whole-K view: rows, all chunks
+    const Geo g = phase_geo<BS, SK::BB, SK::RMAX>(N, K, G, cta, unit);  // whole-K view: rows, all chunks
     const int nr = g.r1 - g.r0;
     const int nc = g.nchunk_all;
     if (!stack) {
@@ -770,7 +950,7 @@ __global__ void __launch_bounds__(MK_THREADS, 1) decode_mk_kernel(const __grid_c
           // silu(g) u with the fast exp / division: a few ulp, far inside the 1e-3 gate
           a[h] = __fdividef(gg, 1.0f + __expf(-gg)) * u;
         }
-        put_pair(P.xs_act, xg, pos, (g.r0 + rr) / 2, a[0], a[1], (ep * (uint32_t)P.layers + l + 1u) & 1u);
+        sk_put_pair<QT, BS>(P.xs_act, xg, pos, (g.r0 + rr) / 2, a[0], a[1], (ep * (uint32_t)P.layers + l + 1u) & 1u);
       }
     } else if (kind == 0) {
       const int v_off = (P.lh + P.lkv) * P.hd;
@@ -793,7 +973,7 @@ __global__ void __launch_bounds__(MK_THREADS, 1) decode_mk_kernel(const __grid_c
           const int jv = hd_log2 >= 0 ? ev >> hd_log2 : ev / P.hd, e = ev - jv * P.hd;
           const int i0 = (jv + P.k0) * P.per - P.h0;
           for (int i = max(i0, 0); i < min(i0 + P.per, P.lh); i++)
-            put_pair(P.xs_ctx, xg, pos, i * P.hd + e, v2[0], v2[1], vctx & 1u);
+            sk_put_pair<QT, BS>(P.xs_ctx, xg, pos, i * P.hd + e, v2[0], v2[1], vctx & 1u);
         }
       }
     } else {
@@ -811,7 +991,7 @@ __global__ void __launch_bounds__(MK_THREADS, 1) decode_mk_kernel(const __grid_c
           ss = fmaf(hn[h], hn[h], ss);
           if (p == nphase - 1) P.h[g.r0 + rr + h] = hn[h];  // stage output
         }
-        put_pair(P.xs_h, xg, pos, g.r0 + rr, hn[0], hn[1], vh & 1u);
+        sk_put_pair<QT, BS>(P.xs_h, xg, pos, g.r0 + rr, hn[0], hn[1], vh & 1u);
       }
 #ifndef IFB_MK_PROF
       if (dbg && ct == 0) dbg[15] = clock64();  // epilogue rows done (before the sum-h^2 reduction)
@@ -836,7 +1016,7 @@ __global__ void __launch_bounds__(MK_THREADS, 1) decode_mk_kernel(const __grid_c
     const uint8_t* W;
     int N, K, kind;
     phase_dims(P, p, &W, &N, &K, &kind);
-    const Geo g = phase_geo(N, K, G, cta, unit);
+    const Geo g = phase_geo<BS, SK::BB, SK::RMAX>(N, K, G, cta, unit);
     (void)W;
     unsigned long long* dbg = P.dbg ? P.dbg + ((size_t)cta * nphase + p) * 16 : nullptr;
     if (dbg && ct == 0) { dbg[0] = gtimer(); dbg[8] = clock64(); }
@@ -911,19 +1091,20 @@ __global__ void __launch_bounds__(MK_THREADS, 1) decode_mk_kernel(const __grid_c
       //    every word's parity (re-read the late ones), strip it, stage the quads in
       //    shared memory and form the block sum of x (x_e + x_o = xe' + 12 x_o in
       //    transformed terms)
-      for (int t0 = cw * 32; t0 < 4 * g.nbp; t0 += 2 * MK_CT) {
+      constexpr int TPB = SK::NQ / 4, TPB_LOG = TPB == 4 ? 2 : 1;  // threads per block, 4 quads each
+      for (int t0 = cw * 32; t0 < TPB * g.nbp; t0 += 2 * MK_CT) {
         float4 v[2][4];
 #pragma unroll
         for (int u = 0; u < 2; u++) {
-          const int t = t0 + u * MK_CT + lane, b = t >> 2, j4 = t & 3;
+          const int t = t0 + u * MK_CT + lane, b = t >> TPB_LOG, j4 = t & (TPB - 1);
 #pragma unroll
           for (int i = 0; i < 4; i++)
             v[u][i] = b < g.nb ? ld_relaxed_f4(img + (4 * j4 + i) * xstride + b) : make_float4(0.f, 0.f, 0.f, 0.f);
         }
 #pragma unroll
         for (int u = 0; u < 2; u++) {
-          if (t0 + u * MK_CT >= 4 * g.nbp) break;  // warp-uniform
-          const int t = t0 + u * MK_CT + lane, b = t >> 2, j4 = t & 3;
+          if (t0 + u * MK_CT >= TPB * g.nbp) break;  // warp-uniform
+          const int t = t0 + u * MK_CT + lane, b = t >> TPB_LOG, j4 = t & (TPB - 1);
           float sx = 0.f;
           if (b < g.nb) {
 #pragma unroll
@@ -942,13 +1123,11 @@ __global__ void __launch_bounds__(MK_THREADS, 1) decode_mk_kernel(const __grid_c
               const float4 w = make_float4(__uint_as_float(__float_as_uint(q.x) & ~1u), __uint_as_float(__float_as_uint(q.y) & ~1u),
                                            __uint_as_float(__float_as_uint(q.z) & ~1u), __uint_as_float(__float_as_uint(q.w) & ~1u));
               xs[jj * xstride + b] = w;
-              const float c0 = __uint_as_float((uint32_t)(127 - 85 + pos[2 * jj]) << 23);  // 2^(s - 85)
-              const float c1 = __uint_as_float((uint32_t)(127 - 85 + pos[2 * jj + 1]) << 23);
-              sx += (w.z + w.w) * 2.5849394142282115e-26f + 12.0f * (w.x * c0 + w.y * c1);
+              sx += sk_quad_sum<QT, BS>(w, jj, pos);
             }
           }
           sx += __shfl_xor_sync(0xffffffffu, sx, 1);
-          sx += __shfl_xor_sync(0xffffffffu, sx, 2);
+          if constexpr (TPB > 2) sx += __shfl_xor_sync(0xffffffffu, sx, 2);
           if (j4 == 0 && b < g.nbp) bs[b] = make_float2(sx, 0.f);
         }
       }
@@ -962,7 +1141,7 @@ __global__ void __launch_bounds__(MK_THREADS, 1) decode_mk_kernel(const __grid_c
       // shapes (70B: K up to 28672) fit.  RMSNorm needs the global sum of squares
       // first: quads stay in registers when they fit, else they are re-read.
       const float4* src4 = reinterpret_cast<const float4*>(stack ? P.h : P.x_in);
-      const int nq = K >> 2, nqp = g.nbp * 16;
+      const int nq = K >> 2, nqp = g.nbp * SK::NQ;
       if (rms && nqp <= MK_MAXQ * MK_CT) {
         float4 v[MK_MAXQ];
         float ss = 0.f;
@@ -977,7 +1156,7 @@ __global__ void __launch_bounds__(MK_THREADS, 1) decode_mk_kernel(const __grid_c
         for (int i = 0; i < MK_MAXQ; i++)
           if (i * MK_CT + (ct & ~31) < nqp) {  // per-warp (nqp is a multiple of 32)
             const float4 a = v[i];
-            stage_quad(ct + i * MK_CT, make_float4(a.x * inv, a.y * inv, a.z * inv, a.w * inv), xstride, xs, bs, pos);
+            sk_stage_quad<QT, BS>(ct + i * MK_CT, make_float4(a.x * inv, a.y * inv, a.z * inv, a.w * inv), xstride, xs, bs, pos);
           }
       } else {
         float inv = 1.f;
@@ -992,7 +1171,7 @@ __global__ void __launch_bounds__(MK_THREADS, 1) decode_mk_kernel(const __grid_c
         for (int q = ct; q < nqp; q += MK_CT) {
           float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
           if (q < nq) a = src4[q];
-          stage_quad(q, make_float4(a.x * inv, a.y * inv, a.z * inv, a.w * inv), xstride, xs, bs, pos);
+          sk_stage_quad<QT, BS>(q, make_float4(a.x * inv, a.y * inv, a.z * inv, a.w * inv), xstride, xs, bs, pos);
         }
       }
       if (dbg && ct == 0) { dbg[2] = gtimer(); dbg[10] = clock64(); }
@@ -1051,11 +1230,11 @@ __global__ void __launch_bounds__(MK_THREADS, 1) decode_mk_kernel(const __grid_c
             float* pr = part + (size_t)(sl * g.rps + i0) * g.nchunk;
             const unsigned char* ua = sbase + (size_t)i0 * g.row_bytes;
             if (MK_RMAX >= 8 && g.R == 8)
-              mk_unit_dispatch<MK_RMAX >= 8 ? 8 : 4, XS>(ua, g.row_bytes, n - i0, c, g.nb, xstride, xs, bs, pr, g.nchunk, kc);
+              sk_unit_dispatch<QT, BS, MK_RMAX >= 8 ? 8 : 4, XS>(ua, g.row_bytes, n - i0, c, g.nb, xstride, xs, bs, pr, g.nchunk, kc);
             else if (g.R == 4)
-              mk_unit_dispatch<4, XS>(ua, g.row_bytes, n - i0, c, g.nb, xstride, xs, bs, pr, g.nchunk, kc);
+              sk_unit_dispatch<QT, BS, 4, XS>(ua, g.row_bytes, n - i0, c, g.nb, xstride, xs, bs, pr, g.nchunk, kc);
             else
-              mk_unit_dispatch<2, XS>(ua, g.row_bytes, n - i0, c, g.nb, xstride, xs, bs, pr, g.nchunk, kc);
+              sk_unit_dispatch<QT, BS, 2, XS>(ua, g.row_bytes, n - i0, c, g.nb, xstride, xs, bs, pr, g.nchunk, kc);
           }
         }
         u0 = u - U;  // continue the round-robin in the next slot
@@ -1099,7 +1278,7 @@ __global__ void __launch_bounds__(MK_THREADS, 1) decode_mk_kernel(const __grid_c
           // silu(g) u with the fast exp / division: a few ulp, far inside the 1e-3 gate
           a[h] = __fdividef(gg, 1.0f + __expf(-gg)) * u;
         }
-        put_pair(P.xs_act, xstride, pos, (g.r0 + rr) / 2, a[0], a[1], (ep * (uint32_t)P.layers + l + 1u) & 1u);
+        sk_put_pair<QT, BS>(P.xs_act, xstride, pos, (g.r0 + rr) / 2, a[0], a[1], (ep * (uint32_t)P.layers + l + 1u) & 1u);
       }
     } else if (kind == 0) {
       const int v_off = (P.lh + P.lkv) * P.hd;
@@ -1122,7 +1301,7 @@ __global__ void __launch_bounds__(MK_THREADS, 1) decode_mk_kernel(const __grid_c
           const int jv = hd_log2 >= 0 ? ev >> hd_log2 : ev / P.hd, e = ev - jv * P.hd;
           const int i0 = (jv + P.k0) * P.per - P.h0;
           for (int i = max(i0, 0); i < min(i0 + P.per, P.lh); i++)
-            put_pair(P.xs_ctx, xstride, pos, i * P.hd + e, v2[0], v2[1], vctx & 1u);
+            sk_put_pair<QT, BS>(P.xs_ctx, xstride, pos, i * P.hd + e, v2[0], v2[1], vctx & 1u);
         }
       }
     } else {
@@ -1176,7 +1355,7 @@ __global__ void __launch_bounds__(MK_THREADS, 1) decode_mk_kernel(const __grid_c
             ss = fmaf(hn[h], hn[h], ss);
             if (p == nphase - 1) P.h[g.r0 + rr + h] = hn[h];  // stage output
           }
-          put_pair(P.xs_h, xstride, pos, g.r0 + rr, hn[0], hn[1], vh & 1u);
+          sk_put_pair<QT, BS>(P.xs_h, xstride, pos, g.r0 + rr, hn[0], hn[1], vh & 1u);
         }
       } else {
       for (int rr = 2 * ct; rr < nr; rr += 2 * MK_CT) {
@@ -1190,7 +1369,7 @@ __global__ void __launch_bounds__(MK_THREADS, 1) decode_mk_kernel(const __grid_c
           ss = fmaf(hn[h], hn[h], ss);
           if (p == nphase - 1) P.h[g.r0 + rr + h] = hn[h];  // stage output
         }
-        put_pair(P.xs_h, xstride, pos, g.r0 + rr, hn[0], hn[1], vh & 1u);
+        sk_put_pair<QT, BS>(P.xs_h, xstride, pos, g.r0 + rr, hn[0], hn[1], vh & 1u);
       }
       }
 #ifndef IFB_MK_PROF
@@ -1231,39 +1410,59 @@ static int mk_sms() {
   return n;
 }
 
-static int nbp_of(int K) { return ((K / 64 + 31) / 32) * 32; }
+static int nbp_of(int K, int bs = 64) { return ((K / bs + 31) / 32) * 32; }
 
 // x row stride (float4 units): >= nbp + 1 for every phase and = 1 (mod 8) so the
 // transposed staging stores are bank-conflict-free.  Common Llama widths are
 // compile-time strides (immediate LDS offsets); others use the runtime stride.
 static int mk_xstride(int nbp_max) { return ((nbp_max + 1 + 7) / 8) * 8 + 1; }
 
-static size_t mk_fixed_smem(int nbp_max, int part_max) {
-  return 2 * MK_MAXSLOT * 8 + 128 + (size_t)16 * 16 * mk_xstride(nbp_max) + (size_t)8 * nbp_max + (size_t)4 * part_max;
+static size_t mk_fixed_smem(int nbp_max, int part_max, int nq = 16) {
+  return 2 * MK_MAXSLOT * 8 + 128 + (size_t)nq * 16 * mk_xstride(nbp_max) + (size_t)8 * nbp_max + (size_t)4 * part_max;
 }
 
-static int part_need(int N, int K, int G) {
+static int part_need(int N, int K, int G, int bs = 64) {
   const int rows = (N + G - 1) / G + 4;
-  return rows * ((K / 64 + 31) / 32);
+  return rows * ((K / bs + 31) / 32);
 }
 
 // K-segment length (blocks) for phases whose staged input would crowd out the ring:
-// 192 blocks = 12288 weights (a 6 KB segment row, four per 24 KB slot)
+// 12288 weights (3.5-bit: a 6 KB segment row, four per 24 KB slot)
 constexpr int MK_SEG_NB = 192;
+
+// the engine instantiations of the k-bit schemes (runtime x stride)
+template <int QT, int BS>
+static void (*gk_kernel(bool seg))(MkParams) {
+  return seg ? decode_mk_kernel<0, true, false, QT, BS> : decode_mk_kernel<0, false, false, QT, BS>;
+}
+static void (*gk_select(int qt, int bs, bool seg))(MkParams) {
+#define IFB_GK(Q, B) \
+  if (qt == Q && bs == B) return gk_kernel<Q, B>(seg);
+  IFB_GK(2, 32) IFB_GK(2, 64) IFB_GK(3, 32) IFB_GK(3, 64) IFB_GK(4, 32) IFB_GK(4, 64) IFB_GK(5, 32) IFB_GK(5, 64)
+  IFB_GK(6, 32) IFB_GK(6, 64) IFB_GK(8, 32) IFB_GK(8, 64)
+#undef IFB_GK
+  return nullptr;
+}
 
 if_status mk_launch(MkParams& P, cudaStream_t st) {
   int G = P.grid > 0 ? std::min(P.grid, mk_sms()) : mk_sms();
   if (const char* e = getenv("IFB_MK_GRID")) G = std::max(1, std::min(atoi(e), G));  // experiments only
+  const int qt = P.qt ? P.qt : 35, bs = P.bs ? P.bs : 64;
+  const bool q3h = qt == 35;
+  if (q3h ? bs != 64 : (bs != 32 && bs != 64)) return IF_ERR_UNSUPPORTED;  // Q3H_B32: 18-byte blocks
+  const int bb = q3h ? 32 : 4 + bs * qt / 8, nq = q3h ? 16 : bs / 4;
   int nbp_max = 0, part_max = 0;
   if (P.mode == MK_MODE_GEMV) {
-    nbp_max = nbp_of(P.gemv_K);
-    part_max = part_need(P.gemv_N, P.gemv_K, G);
+    if (((int64_t)(P.gemv_K / bs) * bb) % 16) return IF_ERR_UNSUPPORTED;  // rows: whole 16-byte bulk copies
+    nbp_max = nbp_of(P.gemv_K, bs);
+    part_max = part_need(P.gemv_N, P.gemv_K, G, bs);
   } else {
     const int Ns[4] = {P.nqkv, P.d, 2 * P.lf, P.d}, Ks[4] = {P.d, P.nq, P.d, P.lf};
     if (P.nq % 64 || P.lf % 64) return IF_ERR_UNSUPPORTED;
     for (int k = 0; k < 4; k++) {
-      nbp_max = std::max(nbp_max, nbp_of(Ks[k]));
-      part_max = std::max(part_max, part_need(Ns[k], Ks[k], G));
+      if (((int64_t)(Ks[k] / bs) * bb) % 16) return IF_ERR_UNSUPPORTED;
+      nbp_max = std::max(nbp_max, nbp_of(Ks[k], bs));
+      part_max = std::max(part_max, part_need(Ns[k], Ks[k], G, bs));
     }
   }
   // global images span the whole K; the shared-memory stage spans one K-segment
@@ -1271,11 +1470,15 @@ if_status mk_launch(MkParams& P, cudaStream_t st) {
 #ifndef IFB_MK_SEG_MIN
 #define IFB_MK_SEG_MIN 224
 #endif
-  P.seg_nb = nbp_max > IFB_MK_SEG_MIN ? MK_SEG_NB : 0;
+  // segment when the staged input would exceed ~60 KB of shared memory
+  const int seg_min = q3h ? IFB_MK_SEG_MIN : (60 * 1024 / (nq * 16) - 10);
+  P.seg_nb = nbp_max > seg_min ? MK_SEG_NB * 64 / bs : 0;
+  if (P.seg_nb && ((int64_t)P.seg_nb * bb) % 16) return IF_ERR_UNSUPPORTED;
   if (P.seg_nb) nbp_max = P.seg_nb;
   P.nbp_max = nbp_max;
   P.raw_max = 0;  // (no raw-input buffer: plain inputs are staged from global memory)
-  const size_t fixed = mk_fixed_smem(nbp_max, part_max) + (size_t)4 * MK_MAXOWN + 128 + (size_t)4 * MK_MAXG;
+  const size_t fixed = mk_fixed_smem(nbp_max, part_max, nq) + (size_t)4 * MK_MAXOWN + 128 + (size_t)4 * MK_MAXG +
+                       (q3h ? 0 : (size_t)4 * bs);  // k-bit code positions
   if (P.mode == MK_MODE_STACK && ((P.d + G - 1) / G > MK_MAXOWN || G > MK_MAXG || P.nqkv % 4 || P.d % 4 ||
                                   P.hd % 2))
     return IF_ERR_UNSUPPORTED;
@@ -1287,7 +1490,11 @@ if_status mk_launch(MkParams& P, cudaStream_t st) {
   const size_t smem = (size_t)nslot * MK_SLOT + fixed;
   P.xstride = mk_xstride(nbp_max);
   void (*kern)(MkParams);
-  if (P.mode == MK_MODE_STACK && P.tp > 1) {  // in-engine TP merges (whole-K phases)
+  if (!q3h) {  // k-bit schemes: runtime stride; TP merges stay on the per-layer path
+    if (P.mode == MK_MODE_STACK && P.tp > 1) return IF_ERR_UNSUPPORTED;
+    kern = gk_select(qt, bs, P.seg_nb != 0);
+    if (!kern) return IF_ERR_UNSUPPORTED;
+  } else if (P.mode == MK_MODE_STACK && P.tp > 1) {  // in-engine TP merges (whole-K phases)
     if (P.seg_nb || P.tp > 8 || !P.tp_box[P.tp_me]) return IF_ERR_UNSUPPORTED;
     switch (P.xstride) {
       case 137: kern = decode_mk_kernel<137, false, true>; break;  // 13B TP2, 70B TP4/8
@@ -1305,12 +1512,12 @@ if_status mk_launch(MkParams& P, cudaStream_t st) {
       default: kern = decode_mk_kernel<0, false>; break;
     }
   }
-  static void (*configured[16])(MkParams) = {};
+  static void (*configured[48])(MkParams) = {};
   bool done_cfg = false;
-  for (int i = 0; i < 16 && configured[i]; i++) done_cfg |= configured[i] == kern;
+  for (int i = 0; i < 48 && configured[i]; i++) done_cfg |= configured[i] == kern;
   if (!done_cfg) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)budget);
-    for (int i = 0; i < 16; i++)
+    for (int i = 0; i < 48; i++)
       if (!configured[i]) {
         configured[i] = kern;
         break;

@@ -43,6 +43,7 @@ struct MkParams {
   int tp, tp_me, tp_hidden;
   float* tp_box[8];  // exchange regions of the group members (group-rank order; [me] = own)
   int grid;          // CTAs per launch (0 = one per SM); ranks sharing one GPU split the SMs
+  int qt, bs;        // scheme (if_qtype, block): 35/64 = the 3.5-bit engine; k-bit schemes too
   int seg_nb;  // K-segment length in 64-blocks (multiple of 32); 0 = whole rows
   unsigned long long* dbg;  // nullable: per-CTA %globaltimer stamps [G][nphase][8] (instrumentation)
   const uint8_t* w[MK_MAXL][4];  // qkv, o, gu (gate/up rows interleaved), down per layer

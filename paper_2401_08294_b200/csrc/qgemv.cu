@@ -133,11 +133,16 @@ static if_status qgemv_impl(const char* fn, if_scheme s, const uint8_t* W, int64
     if_status r = qgemv_tc_launch(s, W, N, K, x, B, y, acc, st, x2_scratch, x2_bytes, x2_ready);
     if (r != IF_ERR_UNSUPPORTED) return r;
   }
-  if (s.type == IF_Q3H && s.block == 64 && (reinterpret_cast<uintptr_t>(W) & 31u) == 0 && N < (1ll << 31)) {
+  // batch 1: the persistent TMA-ring engine for every scheme but Q3H_B32 (18-byte blocks)
+  if (!(s.type == IF_Q3H && s.block == 32) && (reinterpret_cast<uintptr_t>(W) & 31u) == 0 && N < (1ll << 31)) {
     if (B == 1 && K <= 65536) {
       // persistent TMA-ring engine (decode_mk.cu), single-phase mode
       static thread_local MkParams P;  // 4 KB of layer pointers; filled per call
       P.mode = MK_MODE_GEMV;
+      P.qt = s.type;
+      P.bs = s.block;
+      P.tp = 1;
+      P.grid = 0;
       P.layers = 1;
       P.w[0][0] = W;
       P.x_in = x;

@@ -342,11 +342,13 @@ static if_status run_stack(const if_stack_shape* shape, const if_plan* plan, int
   float* tp_boxes[8] = {nullptr};
   int tp_n = 1, tp_me = 0, tp_hidden = 0, tp_grid = 0;
   const bool tp_ok = groups == 1 || (comm_engine(comm, tp_boxes, &tp_n, &tp_me, &tp_hidden, &tp_grid) && tp_hidden >= L.d);
-  const bool mk = mode == IF_DECODE && T <= 6 && sc.type == IF_Q3H && sc.block == 64 && tp_ok &&
+  const bool mk = mode == IF_DECODE && T <= 6 && !(sc.type == IF_Q3H && sc.block == 32) && tp_ok &&
                   nlayers <= MK_MAXL && nlayers > 0 && !kvr;
   if (mk) {
     static thread_local MkParams P;
     P.mode = MK_MODE_STACK;
+    P.qt = sc.type;
+    P.bs = sc.block;
     P.layers = nlayers;
     P.d = L.d;
     P.nq = L.nq;
