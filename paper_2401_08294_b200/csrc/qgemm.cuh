@@ -1,6 +1,7 @@
 // qgemm.cuh — internal interface of the prefill GEMM kernels.
 #pragma once
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
 #include "../../include/if_b200.h"
@@ -18,6 +19,9 @@ if_status qgemm_tc_launch(if_scheme s, const uint8_t* W, int64_t N, int64_t K, c
 if_status qgemv_tc_launch(if_scheme s, const uint8_t* W, int64_t N, int64_t K, const float* x, int64_t B, float* Y,
                           int accumulate, cudaStream_t st, void* x2_scratch = nullptr, size_t x2_bytes = 0,
                           int x2_ready = 0);
+// Q3H_B64, 2 <= B <= 32: warp-level mma.sync with the decode in registers (qgemv_ms.cu)
+if_status qgemv_ms_launch(if_scheme s, const uint8_t* W, int64_t N, int64_t K, const __half* x2, const float* sc,
+                          int64_t B, float* y, int accumulate, cudaStream_t st);
 // if_qgemv / if_qgemv_acc with optional tensor-core scratch (the stack's workspace)
 if_status qgemv_dispatch(const char* fn, if_scheme s, const uint8_t* W, int64_t N, int64_t K, const float* x,
                          int64_t B, float* y, int acc, cudaStream_t st, void* x2_scratch, size_t x2_bytes,

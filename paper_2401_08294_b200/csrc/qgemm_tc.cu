@@ -1169,6 +1169,11 @@ if_status qgemv_tc_launch(if_scheme s, const uint8_t* W, int64_t N, int64_t K, c
     cr = g_encode(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, x2, xd, xs, xb, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (cr != CUDA_SUCCESS) return set_error(IF_ERR_CUDA, "qgemv_tc: x2 tensor map failed (%d)", (int)cr);
+#ifndef IFB_NO_MS
+    // small batches of 3.5-bit weights: the warp-level MMA kernel (decode in registers)
+    const if_status rm = qgemv_ms_launch(s, W, N, K, x2, x2sc, B, Y, accumulate, st);
+    if (rm != IF_ERR_UNSUPPORTED) return rm;
+#endif
   }
   const int ntile = (int)((N + TC_BN - 1) / TC_BN);
   const int ktotal = (int)((K + TC_BK - 1) / TC_BK);

@@ -38,16 +38,131 @@ __device__ __forceinline__ void put_x2(__half* x2, int bp, int64_t K, int64_t t,
   x2[((int64_t)bp + t) * K + k] = __float2half_rn(v - __half2float(h));
 }
 
-// block-wide max (blockDim.x a multiple of 32, <= 1024); every thread gets the result
-__device__ __forceinline__ float block_max(float m, float* red) {
+// ---- x2 glue of the batched decode chain: one CTA of 1024 threads per token row, the
+// row held in registers (<= 32 values per thread: rows up to 32768), so every global
+// load of the row is in flight at once (a strided loop that stores between its loads
+// pays one global latency per element: 13-32 us per launch in round 1's chain).
+constexpr int GX_THREADS = 1024, GX_VMAX = 32;
+
+__device__ __forceinline__ float gx_block_sum(float v, float* red) {
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
   __syncthreads();
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
   __syncthreads();
-  m = 0.f;
-  for (int w = 0; w < (int)(blockDim.x >> 5); w++) m = fmaxf(m, red[w]);
-  return m;
+  float t = 0.f;
+  for (int w = 0; w < GX_THREADS / 32; w++) t += red[w];
+  return t;
+}
+__device__ __forceinline__ float gx_block_max(float v, float* red) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  float t = 0.f;
+  for (int w = 0; w < GX_THREADS / 32; w++) t = fmaxf(t, red[w]);
+  return t;
+}
+// the split of the row (values v[], count n) with its per-token scale, plus the fp32 row
+__device__ __forceinline__ void gx_store_split(const float (&v)[GX_VMAX], int n, int t, int bp, float mx, float* out,
+                                               __half* x2, float* sc) {
+  const int k = xsplit_k(mx);
+  const float mul = pow2f(k);
+  if (threadIdx.x == 0) sc[t] = pow2f(-k);
+#pragma unroll
+  for (int i = 0; i < GX_VMAX; i++) {
+    const int e = threadIdx.x + i * GX_THREADS;
+    if (e < n) {
+      if (out) out[(int64_t)t * n + e] = v[i];
+      put_x2(x2, bp, n, t, e, v[i] * mul);
+    }
+  }
+}
+__device__ __forceinline__ void gx_pad_row(int n, int t, int bp, __half* x2, float* sc) {
+  for (int e = threadIdx.x; e < n; e += GX_THREADS) put_x2(x2, bp, n, t, e, 0.f);
+  if (threadIdx.x == 0) sc[t] = 1.f;
+}
+
+// a[t] = rms(h[t]) and its split; zeroes zbuf[zn] (the next qGEMV accumulates)
+__global__ void __launch_bounds__(GX_THREADS) rmsnorm_x2_kernel(const float* __restrict__ h, float* __restrict__ a, int d,
+                                                                float* __restrict__ zbuf, int64_t zn,
+                                                                __half* __restrict__ x2, int T, int bp,
+                                                                float* __restrict__ sc) {
+  pdl_trigger();
+  pdl_wait();
+  __shared__ float red[GX_THREADS / 32];
+  for (int64_t i = (int64_t)blockIdx.x * GX_THREADS + threadIdx.x; i < zn; i += (int64_t)gridDim.x * GX_THREADS)
+    zbuf[i] = 0.f;
+  const int t = blockIdx.x;
+  if (t >= T) return gx_pad_row(d, t, bp, x2, sc);
+  const float* hr = h + (int64_t)t * d;
+  float v[GX_VMAX];
+  float ss = 0.f, mx = 0.f;
+#pragma unroll
+  for (int i = 0; i < GX_VMAX; i++) {
+    const int e = threadIdx.x + i * GX_THREADS;
+    v[i] = e < d ? hr[e] : 0.f;
+    ss = fmaf(v[i], v[i], ss);
+    mx = fmaxf(mx, fabsf(v[i]));
+  }
+  const float inv = 1.0f / sqrtf(gx_block_sum(ss, red) / (float)d + 1e-5f);
+  mx = gx_block_max(mx, red) * inv;
+#pragma unroll
+  for (int i = 0; i < GX_VMAX; i++) v[i] *= inv;
+  gx_store_split(v, d, t, bp, mx, a, x2, sc);
+}
+
+// ctx[t, i hd + e] = v[t, j hd + e], j = floor((h0 + i)/(H/G)) - k0, and its split
+__global__ void __launch_bounds__(GX_THREADS) vbcast_x2_kernel(const float* __restrict__ qkv, float* __restrict__ ctx,
+                                                               int T, int lh, int lkv, int hd, int h0, int k0, int per,
+                                                               __half* __restrict__ x2, int bp,
+                                                               float* __restrict__ sc) {
+  pdl_trigger();
+  pdl_wait();
+  __shared__ float red[GX_THREADS / 32];
+  const int t = blockIdx.x;
+  const int nq = lh * hd, nqkv = (lh + 2 * lkv) * hd;
+  if (t >= T) return gx_pad_row(nq, t, bp, x2, sc);
+  const float* vr = qkv + (int64_t)t * nqkv + (int64_t)(lh + lkv) * hd;
+  float v[GX_VMAX];
+  float mx = 0.f;
+#pragma unroll
+  for (int i = 0; i < GX_VMAX; i++) {
+    const int r = threadIdx.x + i * GX_THREADS;
+    v[i] = 0.f;
+    if (r < nq) {
+      const int hi = r / hd, e = r - hi * hd;
+      v[i] = vr[(int64_t)((h0 + hi) / per - k0) * hd + e];
+      mx = fmaxf(mx, fabsf(v[i]));
+    }
+  }
+  gx_store_split(v, nq, t, bp, gx_block_max(mx, red), ctx, x2, sc);
+}
+
+// act[t, f] = silu(g) u (gate/up rows interleaved: g = gu[t, 2f], u = gu[t, 2f+1]) and its split
+__global__ void __launch_bounds__(GX_THREADS) silu_mul_x2_kernel(const float* __restrict__ gu, float* __restrict__ act,
+                                                                 int T, int lf, __half* __restrict__ x2, int bp,
+                                                                 float* __restrict__ sc) {
+  pdl_trigger();
+  pdl_wait();
+  __shared__ float red[GX_THREADS / 32];
+  const int t = blockIdx.x;
+  if (t >= T) return gx_pad_row(lf, t, bp, x2, sc);
+  const float2* gr = reinterpret_cast<const float2*>(gu + (int64_t)t * 2 * lf);
+  float v[GX_VMAX];
+  float mx = 0.f;
+#pragma unroll
+  for (int i = 0; i < GX_VMAX; i++) {
+    const int f = threadIdx.x + i * GX_THREADS;
+    v[i] = 0.f;
+    if (f < lf) {
+      const float2 p = gr[f];
+      v[i] = p.x / (1.0f + expf(-p.x)) * p.y;
+      mx = fmaxf(mx, fabsf(v[i]));
+    }
+  }
+  gx_store_split(v, lf, t, bp, gx_block_max(mx, red), act, x2, sc);
 }
 
 // a[t] = h[t] / sqrt(mean(h[t]^2) + 1e-5)
@@ -55,25 +170,15 @@ __device__ __forceinline__ float block_max(float m, float* red) {
 //  no memset node, so the chain stays programmatic)
 template <typename OutT>
 __global__ void __launch_bounds__(256) rmsnorm_kernel(const float* __restrict__ h, OutT* __restrict__ a, int d,
-                                                      float* __restrict__ zbuf = nullptr, int64_t zn = 0,
-                                                      __half* __restrict__ x2 = nullptr, int T = 0, int bp = 0,
-                                                      float* __restrict__ sc = nullptr) {
+                                                      float* __restrict__ zbuf = nullptr, int64_t zn = 0) {
   pdl_trigger();
   pdl_wait();
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < zn; i += (int64_t)gridDim.x * blockDim.x)
     zbuf[i] = 0.f;
-  if (x2 && (int)blockIdx.x >= T) {  // padding token rows of the split
-    for (int i = threadIdx.x; i < d; i += blockDim.x) put_x2(x2, bp, d, blockIdx.x, i, 0.f);
-    if (threadIdx.x == 0) sc[blockIdx.x] = 1.f;
-    return;
-  }
   __shared__ float red[8];
   const float* hr = h + (int64_t)blockIdx.x * d;
-  float ss = 0.f, mx = 0.f;
-  for (int i = threadIdx.x; i < d; i += blockDim.x) {
-    ss = fmaf(hr[i], hr[i], ss);
-    mx = fmaxf(mx, fabsf(hr[i]));
-  }
+  float ss = 0.f;
+  for (int i = threadIdx.x; i < d; i += blockDim.x) ss = fmaf(hr[i], hr[i], ss);
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
@@ -81,18 +186,8 @@ __global__ void __launch_bounds__(256) rmsnorm_kernel(const float* __restrict__ 
   float tot = 0.f;
   for (int w = 0; w < (int)(blockDim.x >> 5); w++) tot += red[w];
   const float inv = 1.0f / sqrtf(tot / (float)d + 1e-5f);
-  float mul = 1.f;
-  if (x2) {
-    const int k = xsplit_k(block_max(mx, red) * inv);
-    mul = pow2f(k);
-    if (threadIdx.x == 0) sc[blockIdx.x] = pow2f(-k);
-  }
   OutT* ar = a + (int64_t)blockIdx.x * d;
-  for (int i = threadIdx.x; i < d; i += blockDim.x) {
-    const float v = hr[i] * inv;
-    ar[i] = to_out<OutT>(v);
-    if (x2) put_x2(x2, bp, d, blockIdx.x, i, v * mul);
-  }
+  for (int i = threadIdx.x; i < d; i += blockDim.x) ar[i] = to_out<OutT>(hr[i] * inv);
 }
 
 // ctx[t, i*hd + e] = v[t, j*hd + e],  j = floor((h0 + i)/(H/G)) - k0  (local heads/kv-heads)
@@ -111,35 +206,6 @@ __global__ void vbcast_kernel(const float* __restrict__ qkv, OutT* __restrict__ 
   }
 }
 
-// x2 variant, one CTA per token row t < bp: the ctx row is made of the rank's v rows
-// (every local kv head feeds at least one local head), so its max is the max of v
-__global__ void __launch_bounds__(256) vbcast_x2_kernel(const float* __restrict__ qkv, float* __restrict__ ctx, int T,
-                                                        int lh, int lkv, int hd, int h0, int k0, int per,
-                                                        __half* __restrict__ x2, int bp, float* __restrict__ sc) {
-  pdl_trigger();
-  pdl_wait();
-  __shared__ float red[8];
-  const int t = blockIdx.x;
-  const int64_t nq = (int64_t)lh * hd, nqkv = (int64_t)(lh + 2 * lkv) * hd;
-  const float* vr = qkv + (int64_t)t * nqkv + (int64_t)(lh + lkv) * hd;
-  float mx = 0.f;
-  if (t < T)
-    for (int i = threadIdx.x; i < lkv * hd; i += blockDim.x) mx = fmaxf(mx, fabsf(vr[i]));
-  const int k = xsplit_k(block_max(mx, red));
-  const float mul = pow2f(k);
-  if (threadIdx.x == 0) sc[t] = pow2f(-k);
-  for (int64_t r = threadIdx.x; r < nq; r += blockDim.x) {
-    float v = 0.f;
-    if (t < T) {
-      const int i = (int)(r / hd), e = (int)(r - (int64_t)i * hd);
-      const int j = (h0 + i) / per - k0;
-      v = vr[(int64_t)j * hd + e];
-      ctx[(int64_t)t * nq + r] = v;
-    }
-    put_x2(x2, bp, nq, t, r, v * mul);
-  }
-}
-
 // act[t, f] = silu(g) * u with gate/up rows interleaved: g = gu[t, 2f], u = gu[t, 2f+1]
 template <typename OutT>
 __global__ void silu_mul_kernel(const float* __restrict__ gu, OutT* __restrict__ act, int T, int lf) {
@@ -154,34 +220,6 @@ __global__ void silu_mul_kernel(const float* __restrict__ gu, OutT* __restrict__
 }
 
 // x2 variant, one CTA per token row: pass 1 the row max of silu(g) u, pass 2 the split
-__global__ void __launch_bounds__(256) silu_mul_x2_kernel(const float* __restrict__ gu, float* __restrict__ act, int T,
-                                                          int lf, __half* __restrict__ x2, int bp,
-                                                          float* __restrict__ sc) {
-  pdl_trigger();
-  pdl_wait();
-  __shared__ float red[8];
-  const int t = blockIdx.x;
-  const float* gr = gu + (int64_t)t * 2 * lf;
-  float mx = 0.f;
-  if (t < T)
-    for (int f = threadIdx.x; f < lf; f += blockDim.x) {
-      const float g = gr[2 * f], u = gr[2 * f + 1];
-      mx = fmaxf(mx, fabsf(g / (1.0f + expf(-g)) * u));
-    }
-  const int k = xsplit_k(block_max(mx, red));
-  const float mul = pow2f(k);
-  if (threadIdx.x == 0) sc[t] = pow2f(-k);
-  for (int f = threadIdx.x; f < lf; f += blockDim.x) {
-    float v = 0.f;
-    if (t < T) {
-      const float g = gr[2 * f], u = gr[2 * f + 1];
-      v = g / (1.0f + expf(-g)) * u;
-      act[(int64_t)t * lf + f] = v;
-    }
-    put_x2(x2, bp, lf, t, f, v * mul);
-  }
-}
-
 // launch with the programmatic-dependent-launch attribute (decode chain)
 template <typename... KArgs, typename... Args>
 static void launch_pdl(void (*kern)(KArgs...), unsigned grid, unsigned block, cudaStream_t st, Args... args) {
@@ -414,8 +452,12 @@ static if_status run_stack(const if_stack_shape* shape, const if_plan* plan, int
     if (!Wl.wqkv || !Wl.wo || !Wl.wgu || !Wl.wdown) return set_error(IF_ERR_ARG, "if_run_stack: null weights, layer %d", l);
     if (mode == IF_DECODE) {
       // ---- attention sub-layer ----
-      launch_pdl(rmsnorm_kernel<float>, (unsigned)std::max<int64_t>(T, bpx), 256, cs, (const float*)h_out, w.a, (int)L.d,
-                 w.qkv, (int64_t)T * L.nqkv, x2h, (int)T, bpx, x2s);
+      if (use_x2)
+        launch_pdl(rmsnorm_x2_kernel, (unsigned)bpx, GX_THREADS, cs, (const float*)h_out, w.a, (int)L.d, w.qkv,
+                   (int64_t)T * L.nqkv, x2h, (int)T, bpx, x2s);
+      else
+        launch_pdl(rmsnorm_kernel<float>, (unsigned)T, 256, cs, (const float*)h_out, w.a, (int)L.d, w.qkv,
+                   (int64_t)T * L.nqkv);
       count_launch();
       if ((st = qgemv_dispatch("if_run_stack(qkv)", sc, Wl.wqkv, L.nqkv, L.d, w.a, T, w.qkv, 1, cs, w.x2, w.x2_bytes, x2r)))
         return st;
@@ -430,7 +472,7 @@ static if_status run_stack(const if_stack_shape* shape, const if_plan* plan, int
         aa.pdl = true;
         if ((st = attn_run(aa, cs))) return st;
       } else if (use_x2)
-        launch_pdl(vbcast_x2_kernel, (unsigned)bpx, 256, cs, (const float*)w.qkv, w.ctx, (int)T, (int)L.lh, (int)L.lkv,
+        launch_pdl(vbcast_x2_kernel, (unsigned)bpx, GX_THREADS, cs, (const float*)w.qkv, w.ctx, (int)T, (int)L.lh, (int)L.lkv,
                    (int)L.hd, (int)asg.head_begin, (int)asg.kv_begin, (int)per, x2h, bpx, x2s);
       else
         launch_pdl(vbcast_kernel<float>, (unsigned)ew_grid(T * L.nq), 256, cs, (const float*)w.qkv, w.ctx, (int)T,
@@ -445,13 +487,17 @@ static if_status run_stack(const if_stack_shape* shape, const if_plan* plan, int
         if ((st = comm_allreduce_into(comm, w.part, h_out, nh, 1, cs))) return st;  // merge #1
       }
       // ---- feed-forward sub-layer ----
-      launch_pdl(rmsnorm_kernel<float>, (unsigned)std::max<int64_t>(T, bpx), 256, cs, (const float*)h_out, w.a, (int)L.d,
-                 w.gu, (int64_t)T * 2 * L.lf, x2h, (int)T, bpx, x2s);
+      if (use_x2)
+        launch_pdl(rmsnorm_x2_kernel, (unsigned)bpx, GX_THREADS, cs, (const float*)h_out, w.a, (int)L.d, w.gu,
+                   (int64_t)T * 2 * L.lf, x2h, (int)T, bpx, x2s);
+      else
+        launch_pdl(rmsnorm_kernel<float>, (unsigned)T, 256, cs, (const float*)h_out, w.a, (int)L.d, w.gu,
+                   (int64_t)T * 2 * L.lf);
       count_launch();
       if ((st = qgemv_dispatch("if_run_stack(gu)", sc, Wl.wgu, 2 * L.lf, L.d, w.a, T, w.gu, 1, cs, w.x2, w.x2_bytes, x2r)))
         return st;
       if (use_x2)
-        launch_pdl(silu_mul_x2_kernel, (unsigned)bpx, 256, cs, (const float*)w.gu, w.act, (int)T, (int)L.lf, x2h, bpx,
+        launch_pdl(silu_mul_x2_kernel, (unsigned)bpx, GX_THREADS, cs, (const float*)w.gu, w.act, (int)T, (int)L.lf, x2h, bpx,
                    x2s);
       else
         launch_pdl(silu_mul_kernel<float>, (unsigned)ew_grid(T * L.lf), 256, cs, (const float*)w.gu, w.act, (int)T,
