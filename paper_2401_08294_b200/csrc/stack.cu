@@ -380,7 +380,12 @@ static if_status run_stack(const if_stack_shape* shape, const if_plan* plan, int
   float* tp_boxes[8] = {nullptr};
   int tp_n = 1, tp_me = 0, tp_hidden = 0, tp_grid = 0;
   const bool tp_ok = groups == 1 || (comm_engine(comm, tp_boxes, &tp_n, &tp_me, &tp_hidden, &tp_grid) && tp_hidden >= L.d);
-  const bool mk = mode == IF_DECODE && T <= 6 && !(sc.type == IF_Q3H && sc.block == 32) && tp_ok &&
+  // batch sizes that run one engine launch per token: 3.5-bit from B = 3 takes the
+  // batched warp-MMA qGEMV chain instead (measured: B = 3..6 954..1877 tok/s vs 902 with
+  // the engine per token); the k-bit schemes up to B = 6 (their batched path is tcgen05)
+  static const char* tenv = getenv("IFB_MK_TMAX");  // experiments only
+  const int mk_tmax = tenv ? atoi(tenv) : (sc.type == IF_Q3H && sc.block == 64 ? 2 : 6);
+  const bool mk = mode == IF_DECODE && T <= mk_tmax && !(sc.type == IF_Q3H && sc.block == 32) && tp_ok &&
                   nlayers <= MK_MAXL && nlayers > 0 && !kvr;
   if (mk) {
     static thread_local MkParams P;
