@@ -86,8 +86,10 @@ __device__ __forceinline__ void ms_pair(uint32_t src0, uint32_t src1, u64 step2,
   out1 = h2_as_u32(__floats2half2_rn(we.y, wo.y));
 }
 
-__device__ __forceinline__ void ms_dequant2(const uint32_t* w0, const uint32_t* w1, int c, uint32_t (&a0)[8],
-                                            uint32_t (&a1)[8]) {
+// o1, o2, o3: word offsets of this lane's code window inside a row (constant per lane;
+// o3 is clamped into the row and its word masked by m3 when the window ends at word 7)
+__device__ __forceinline__ void ms_dequant2(const uint32_t* w0, const uint32_t* w1, int o1, int o2, int o3,
+                                            uint32_t m3, int sh, uint32_t (&a0)[8], uint32_t (&a1)[8]) {
   const uint32_t h0 = w0[0], h1 = w1[0];
   const float lo0 = __half2float(__ushort_as_half((unsigned short)(h0 & 0xFFFFu)));
   const float hi0 = __half2float(__ushort_as_half((unsigned short)(h0 >> 16)));
@@ -95,12 +97,9 @@ __device__ __forceinline__ void ms_dequant2(const uint32_t* w0, const uint32_t* 
   const float hi1 = __half2float(__ushort_as_half((unsigned short)(h1 >> 16)));
   constexpr float k = 0.1f * 38685626227668133590597632.0f;  // (1/10) 2^85
   const u64 step2 = pack2((hi0 - lo0) * k, (hi1 - lo1) * k), lo2 = pack2(lo0, lo1);
-  // this lane's 56 code bits start at byte 4 + 7c of the block
-  const int byte = 4 + 7 * c, wi = byte >> 2, sh = (byte & 3) * 8;
-  const uint32_t u0lo = __funnelshift_r(w0[wi], w0[wi + 1], sh);
-  const uint32_t u0hi = __funnelshift_r(w0[wi + 1], wi + 2 < 8 ? w0[wi + 2] : 0u, sh);
-  const uint32_t u1lo = __funnelshift_r(w1[wi], w1[wi + 1], sh);
-  const uint32_t u1hi = __funnelshift_r(w1[wi + 1], wi + 2 < 8 ? w1[wi + 2] : 0u, sh);
+  const uint32_t a1w = w0[o2], b1w = w1[o2];
+  const uint32_t u0lo = __funnelshift_r(w0[o1], a1w, sh), u0hi = __funnelshift_r(a1w, w0[o3] & m3, sh);
+  const uint32_t u1lo = __funnelshift_r(w1[o1], b1w, sh), u1hi = __funnelshift_r(b1w, w1[o3] & m3, sh);
   const uint32_t v0 = __funnelshift_r(u0lo, u0hi, 21), v1 = __funnelshift_r(u1lo, u1hi, 21);  // pairs 3, 4
   ms_pair<0>(u0lo, u1lo, step2, lo2, a0[0], a1[0]);
   ms_pair<7>(u0lo, u1lo, step2, lo2, a0[1], a1[1]);
@@ -165,15 +164,20 @@ __global__ void __launch_bounds__(MS_THREADS, IFB_MS_MINB) qgemv_ms_kernel(const
   float acc[2 * NT][4];
 #pragma unroll
   for (int t = 0; t < 2 * NT; t++) acc[t][0] = acc[t][1] = acc[t][2] = acc[t][3] = 0.f;
-  const uint32_t* xw = reinterpret_cast<const uint32_t*>(xs);
-  const int pw = pitch / 2;  // words
+  // per-lane constants hoisted out of the block loop: the code window (this lane's 56
+  // bits start at byte 4 + 7c of a block), the x row of every token tile
+  const int byte = 4 + 7 * c, o1 = byte >> 2, o2 = o1 + 1, o3 = o1 + 2 < 8 ? o1 + 2 : 7;
+  const uint32_t m3 = o1 + 2 < 8 ? 0xFFFFFFFFu : 0u;
+  const int sh = (byte & 3) * 8;
+  const uint32_t* xw = reinterpret_cast<const uint32_t*>(xs) + r0 * (pitch / 2) + 8 * c;
+  const int tstride = 8 * (pitch / 2);  // words between token tiles
   int slot = 0;
   for (int kb = kb0; kb < kb1; kb++) {
     asm volatile("cp.async.wait_group %0;" ::"n"(MS_DEPTH - 1) : "memory");  // block kb (this lane's part)
     __syncwarp();                                                             // ... and every lane's
     const uint32_t* wb = ring + slot * 128;
     uint32_t a_lo[8], a_hi[8];
-    ms_dequant2(wb + r0 * 8, wb + (r0 + 8) * 8, c, a_lo, a_hi);
+    ms_dequant2(wb + r0 * 8, wb + (r0 + 8) * 8, o1, o2, o3, m3, sh, a_lo, a_hi);
     __syncwarp();  // the slot is read: refill it with block kb + MS_DEPTH
     if (kb + MS_DEPTH < kb1)
       asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(ring_s + slot * 512),
@@ -181,16 +185,15 @@ __global__ void __launch_bounds__(MS_THREADS, IFB_MS_MINB) qgemv_ms_kernel(const
                    : "memory");
     asm volatile("cp.async.commit_group;" ::: "memory");
     slot = slot + 1 == MS_DEPTH ? 0 : slot + 1;
-    const int xk = (kb - kb0) * 32 + 8 * c;  // word offset of k = 64 kb + 16c in a pitch row
 #pragma unroll
     for (int g = 0; g < 4; g++) {
 #pragma unroll
-      for (int t = 0; t < 2 * NT; t++) {
-        const int j = 8 * t + r0;  // x row: hi tiles [0, NT), then lo tiles (rows BP + 8 (t - NT) + r0)
-        const uint2 b = *reinterpret_cast<const uint2*>(xw + (size_t)j * pw + xk + 2 * g);
+      for (int t = 0; t < 2 * NT; t++) {  // token tile t: x rows 8t + r0 (hi tiles, then lo tiles)
+        const uint2 b = *reinterpret_cast<const uint2*>(xw + t * tstride + 2 * g);
         mma16816(acc[t], a_lo[2 * g], a_hi[2 * g], a_lo[2 * g + 1], a_hi[2 * g + 1], b.x, b.y);
       }
     }
+    xw += 32;  // next block: 64 halves
   }
   asm volatile("cp.async.wait_group 0;" ::: "memory");
   // epilogue: C fragment rows r0, r0+8; columns 2c, 2c+1 of each 8-token tile
