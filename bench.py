@@ -330,13 +330,26 @@ def run_ours(args):
     first, last = asg.stage == 0, asg.stage == plan.stages - 1
     ring = plan.stages > 1
 
+    kv = kv_slots = kv_pos = None
+    kv_bytes = 0
+    if args.kv_pos > 0:  # one KV slot per token, every token attending to kv_pos + 1 cached positions
+        kv = F.KV(shape, plan, rank, B, args.kv_pos + 1, dev)
+        kv_slots = torch.arange(B, dtype=torch.int32, device=dev)
+        kv_pos = torch.full((B,), args.kv_pos, dtype=torch.int32, device=dev)
+        a_ = plan.a[rank]
+        kv_bytes = (a_.layer_end - a_.layer_begin) * B * (args.kv_pos + 1) * 2 * (a_.kv_end - a_.kv_begin) * cfg["head_dim"] * 4
+
     def step(feedback=True):
         # decode speed (Table 5, Q22): step k+1's input is step k's output, so on a
         # pipeline the last stage feeds its h_out back to stage 0 (comm ring,
         # if_b200.h) -- stages cannot run ahead on independent inputs
         if ring and feedback and first:
             comm.recv_prev(h_in, stream)
-        F.if_run_stack(shape, plan, rank, comm, stk.arr, h_in, B, F.IF_DECODE, h_out, None, wsb, stream)
+        if kv is not None:  # NEXT-1: GQA attention over the KV cache at position args.kv_pos
+            F.if_run_stack_kv(shape, plan, rank, comm, stk.arr, h_in, B, F.IF_DECODE, h_out, None, kv, kv_slots,
+                              kv_pos, wsb, stream)
+        else:
+            F.if_run_stack(shape, plan, rank, comm, stk.arr, h_in, B, F.IF_DECODE, h_out, None, wsb, stream)
         if ring and feedback and last:
             comm.send_next(h_out, stream)
 
@@ -384,7 +397,7 @@ def run_ours(args):
     tok_s = B * args.steps / (ms / 1e3)  # tokens of the job (one stream of B tokens per step)
     total_bytes = stack_bytes_total(cfg, s)
     gbs = total_bytes / (ms_per_step / 1e3) / 1e9  # whole-job weight bytes streamed per second
-    rank_bytes = stk.weight_bytes()
+    rank_bytes = stk.weight_bytes() + kv_bytes  # + the KV cache read by the attention (NEXT-1)
     stack_gbs_rank = rank_bytes / (ms_per_step / 1e3) / 1e9
 
     # ---- e2e through the public API: pinned host h_in -> device -> stack -> host h_out
@@ -468,7 +481,8 @@ def run_ours(args):
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
             "scaling": "strong" if ws > 1 else "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (counter-based Irwin-Hall weights sigma=1/sqrt(d), activations sigma=1)",
-            "config": {"workload": f"llama2-{args.model}-stack {args.scheme.lower()} decode b={B}", "model": f"llama2-{args.model}-shaped",
+            "config": {"workload": f"llama2-{args.model}-stack {args.scheme.lower()} decode b={B}" +
+                       (f" kv-attention pos={args.kv_pos}" if args.kv_pos else ""), "model": f"llama2-{args.model}-shaped",
                        "global_batch": B, "seq_len": 1, "parallelism": strategy, "scheme": scheme_str,
                        "comm": (args.comm if ws > 1 else None),
                        "weight_bytes_per_step": total_bytes,
@@ -500,6 +514,8 @@ def main():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--batch", type=int, default=1)
+    ap.add_argument("--kv-pos", type=int, default=0,
+                    help="NEXT-1: decode with GQA attention over a KV cache at this position (0: the Q18 stand-in)")
     ap.add_argument("--scheme", default="Q3H_B64", help="Q3H_B64 (3.5-bit, BASELINE) or Q2/Q3/Q4/Q5/Q6/Q8 _B32/_B64")
     # default: 7B (BASELINE configs[1]) at N = 1; north_star's 70B stack at N > 1
     ap.add_argument("--model", default=None, choices=["7b", "13b", "70b"])

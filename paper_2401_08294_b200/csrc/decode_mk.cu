@@ -574,7 +574,7 @@ __device__ __forceinline__ void sk_put_pair(float4* xsg, int xstride, const int*
   }
 }
 
-template <int XS, bool SEG, bool TP = false, int QT = 35, int BS = 64>
+template <int XS, bool SEG, bool TP = false, int QT = 35, int BS = 64, bool PL = false>
 __global__ void __launch_bounds__(MK_THREADS, 1) decode_mk_kernel(const __grid_constant__ MkParams P) {
   using SK = SkTraits<QT, BS>;
   const int xstride = XS > 0 ? XS : P.xstride;  // staged input in shared memory
@@ -611,6 +611,7 @@ __global__ void __launch_bounds__(MK_THREADS, 1) decode_mk_kernel(const __grid_c
   __syncthreads();
   const bool stack = P.mode == MK_MODE_STACK;
   const int nphase = stack ? 4 * P.layers : 1;
+  const int pb = PL ? P.p_begin : 0, pe = PL ? P.p_end : nphase;  // this launch's phases
   const int unit = stack ? 4 : 1;
 
   if (warp == 0) {
@@ -622,7 +623,7 @@ __global__ void __launch_bounds__(MK_THREADS, 1) decode_mk_kernel(const __grid_c
 #endif
       const uint64_t pol = policy_evict_first();
       uint32_t slot = 0, round = 0, seq = 0;
-      for (int p = 0; p < nphase; p++) {
+      for (int p = pb; p < pe; p++) {
         const uint8_t* W;
         int N, K, kind;
         phase_dims(P, p, &W, &N, &K, &kind);
@@ -672,7 +673,7 @@ __global__ void __launch_bounds__(MK_THREADS, 1) decode_mk_kernel(const __grid_c
     const Geo go = phase_geo<BS, SK::BB, SK::RMAX>(P.d, P.nq, G, cta, unit);
     for (int i = ct; i < go.r1 - go.r0; i += MK_CT) h_own[i] = P.h[go.r0 + i];
   }
-  for (int p = 0; p < nphase; p++) {
+  for (int p = pb; p < pe; p++) {
     if constexpr (SEG) {
     const uint8_t* W;
     int N, K, kind;
@@ -685,7 +686,7 @@ __global__ void __launch_bounds__(MK_THREADS, 1) decode_mk_kernel(const __grid_c
     // the transformed quad layout into a global xs image: one dependency wait, then
     // 16 bulk copies (one per quad row JJ) + the sum-h^2 partials for RMSNorm.
     // The first phase (plain h) and the standalone GEMV stage from global memory.
-    const bool from_image = stack && p > 0;
+    const bool from_image = stack && p > pb;
     const bool rms = kind == 0 || kind == 2;
     const uint32_t l = (uint32_t)(p >> 2);
     float out_scale = 1.f;  // RMSNorm folded into the output: W (s h) = s (W h)
@@ -1024,7 +1025,7 @@ __global__ void __launch_bounds__(MK_THREADS, 1) decode_mk_kernel(const __grid_c
     // the transformed quad layout into a global xs image: one dependency wait, then
     // 16 bulk copies (one per quad row JJ) + the sum-h^2 partials for RMSNorm.
     // The first phase (plain h) and the standalone GEMV stage from global memory.
-    const bool from_image = stack && p > 0;
+    const bool from_image = stack && p > pb;
     const bool rms = kind == 0 || kind == 2;
     const uint32_t l = (uint32_t)(p >> 2);
     float out_scale = 1.f;  // RMSNorm folded into the output: W (s h) = s (W h)
@@ -1140,7 +1141,7 @@ __global__ void __launch_bounds__(MK_THREADS, 1) decode_mk_kernel(const __grid_c
       // transformed quads; no shared-memory copy of the raw vector, so the largest
       // shapes (70B: K up to 28672) fit.  RMSNorm needs the global sum of squares
       // first: quads stay in registers when they fit, else they are re-read.
-      const float4* src4 = reinterpret_cast<const float4*>(stack ? P.h : P.x_in);
+      const float4* src4 = reinterpret_cast<const float4*>(PL && P.x_first && kind != 0 ? P.x_first : (stack ? P.h : P.x_in));
       const int nq = K >> 2, nqp = g.nbp * SK::NQ;
       if (rms && nqp <= MK_MAXQ * MK_CT) {
         float4 v[MK_MAXQ];
@@ -1293,6 +1294,7 @@ __global__ void __launch_bounds__(MK_THREADS, 1) decode_mk_kernel(const __grid_c
           for (int c = 0; c < nc; c++) sacc += part[(rr + h) * nc + c];
           v2[h] = sacc * out_scale;
           if (last_layer && P.last_qkv) P.last_qkv[g.r0 + rr + h] = v2[h];
+          if (PL && P.qkv_out && p == pe - 1) P.qkv_out[g.r0 + rr + h] = v2[h];  // for the KV attention
         }
         const int n = g.r0 + rr;
         if (n >= v_off) {
@@ -1353,7 +1355,7 @@ __global__ void __launch_bounds__(MK_THREADS, 1) decode_mk_kernel(const __grid_c
             hn[h] = h_own[rr + h] + sacc;
             h_own[rr + h] = hn[h];
             ss = fmaf(hn[h], hn[h], ss);
-            if (p == nphase - 1) P.h[g.r0 + rr + h] = hn[h];  // stage output
+            if (p == nphase - 1 || (PL && pe < nphase)) P.h[g.r0 + rr + h] = hn[h];  // stage output
           }
           sk_put_pair<QT, BS>(P.xs_h, xstride, pos, g.r0 + rr, hn[0], hn[1], vh & 1u);
         }
@@ -1367,7 +1369,7 @@ __global__ void __launch_bounds__(MK_THREADS, 1) decode_mk_kernel(const __grid_c
           hn[h] = h_own[rr + h] + sacc;
           h_own[rr + h] = hn[h];
           ss = fmaf(hn[h], hn[h], ss);
-          if (p == nphase - 1) P.h[g.r0 + rr + h] = hn[h];  // stage output
+          if (p == nphase - 1 || (PL && pe < nphase)) P.h[g.r0 + rr + h] = hn[h];  // stage output
         }
         sk_put_pair<QT, BS>(P.xs_h, xstride, pos, g.r0 + rr, hn[0], hn[1], vh & 1u);
       }
@@ -1395,7 +1397,7 @@ __global__ void __launch_bounds__(MK_THREADS, 1) decode_mk_kernel(const __grid_c
   }
   // every CTA read the epoch before writing its first image (which CTA 0's last
   // phase has consumed), so the next launch may see the new one
-  if (stack && cta == 0 && ct == 0) st_relaxed_u32(P.epoch, ep + 1u);
+  if (stack && cta == 0 && ct == 0 && pe == nphase) st_relaxed_u32(P.epoch, ep + 1u);  // (per token)
 }
 
 // ---------------------------------------------------------------------------
@@ -1491,9 +1493,18 @@ if_status mk_launch(MkParams& P, cudaStream_t st) {
   P.xstride = mk_xstride(nbp_max);
   void (*kern)(MkParams);
   if (!q3h) {  // k-bit schemes: runtime stride; TP merges stay on the per-layer path
-    if (P.mode == MK_MODE_STACK && P.tp > 1) return IF_ERR_UNSUPPORTED;
+    if (P.mode == MK_MODE_STACK && (P.tp > 1 || P.part)) return IF_ERR_UNSUPPORTED;
     kern = gk_select(qt, bs, P.seg_nb != 0);
     if (!kern) return IF_ERR_UNSUPPORTED;
+  } else if (P.mode == MK_MODE_STACK && P.part) {  // partial launches around the KV attention
+    if (P.seg_nb || P.tp > 1) return IF_ERR_UNSUPPORTED;
+    switch (P.xstride) {
+      case 73: kern = decode_mk_kernel<73, false, false, 35, 64, true>; break;
+      case 137: kern = decode_mk_kernel<137, false, false, 35, 64, true>; break;
+      case 201: kern = decode_mk_kernel<201, false, false, 35, 64, true>; break;
+      case 233: kern = decode_mk_kernel<233, false, false, 35, 64, true>; break;
+      default: kern = decode_mk_kernel<0, false, false, 35, 64, true>; break;
+    }
   } else if (P.mode == MK_MODE_STACK && P.tp > 1) {  // in-engine TP merges (whole-K phases)
     if (P.seg_nb || P.tp > 8 || !P.tp_box[P.tp_me]) return IF_ERR_UNSUPPORTED;
     switch (P.xstride) {

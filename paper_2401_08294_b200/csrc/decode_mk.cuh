@@ -44,6 +44,13 @@ struct MkParams {
   float* tp_box[8];  // exchange regions of the group members (group-rank order; [me] = own)
   int grid;          // CTAs per launch (0 = one per SM); ranks sharing one GPU split the SMs
   int qt, bs;        // scheme (if_qtype, block): 35/64 = the 3.5-bit engine; k-bit schemes too
+  // partial launches (KV attention between the qkv and o phases, stack.cu): phases
+  // [p_begin, p_end) of the stack; the first one stages its input from x_first (or h),
+  // a final qkv phase writes its rows to qkv_out, o/down always write h, and only the
+  // launch that ends the stack advances the epoch.  part = 0: the whole stack.
+  int part, p_begin, p_end;
+  const float* x_first;
+  float* qkv_out;
   int seg_nb;  // K-segment length in 64-blocks (multiple of 32); 0 = whole rows
   unsigned long long* dbg;  // nullable: per-CTA %globaltimer stamps [G][nphase][8] (instrumentation)
   const uint8_t* w[MK_MAXL][4];  // qkv, o, gu (gate/up rows interleaved), down per layer

@@ -385,8 +385,11 @@ static if_status run_stack(const if_stack_shape* shape, const if_plan* plan, int
   // the engine per token); the k-bit schemes up to B = 6 (their batched path is tcgen05)
   static const char* tenv = getenv("IFB_MK_TMAX");  // experiments only
   const int mk_tmax = tenv ? atoi(tenv) : (sc.type == IF_Q3H && sc.block == 64 ? 2 : 6);
+  // with a KV cache (NEXT-1) the 3.5-bit engine runs in partial launches per token:
+  // [qkv_0] attn_0 [o_0 gu_0 down_0 qkv_1] attn_1 ... [o_L-1 gu down] (one rank)
+  const bool mk_kv = kvr && T <= 2 && sc.type == IF_Q3H && sc.block == 64 && groups == 1 && !getenv("IFB_NO_MK_KV");
   const bool mk = mode == IF_DECODE && T <= mk_tmax && !(sc.type == IF_Q3H && sc.block == 32) && tp_ok &&
-                  nlayers <= MK_MAXL && nlayers > 0 && !kvr;
+                  nlayers <= MK_MAXL && nlayers > 0 && (!kvr || mk_kv);
   if (mk) {
     static thread_local MkParams P;
     P.mode = MK_MODE_STACK;
@@ -431,11 +434,36 @@ static if_status run_stack(const if_stack_shape* shape, const if_plan* plan, int
       P.w[l][2] = Wl.wgu;
       P.w[l][3] = Wl.wdown;
     }
-    for (int64_t t = 0; t < T; t++) {
+    P.part = 0;
+    P.x_first = nullptr;
+    P.qkv_out = nullptr;
+    for (int64_t t = 0; t < T && !st; t++) {
       P.h = h_out + t * L.d;
       P.last_qkv = last_qkv ? last_qkv + t * L.nqkv : nullptr;
-      st = mk_launch(P, cs);
-      if (st) break;
+      if (!kvr) {
+        st = mk_launch(P, cs);
+        continue;
+      }
+      // KV attention between each layer's qkv and o phases (attn.cu on this token)
+      P.part = 1;
+      P.last_qkv = nullptr;  // q, k are returned after RoPE: copied after the last attention
+      P.x_first = w.ctx;
+      P.qkv_out = w.qkv;
+      for (int k = 0; k <= nlayers && !st; k++) {
+        P.p_begin = k == 0 ? 0 : 4 * (k - 1) + 1;
+        P.p_end = k == nlayers ? 4 * nlayers : 4 * k + 1;
+        st = mk_launch(P, cs);
+        if (st || k == nlayers) break;
+        KvRun one = *kvr;
+        one.slot_ids = kvr->slot_ids + t;
+        one.positions = kvr->positions + t;
+        AttnArgs aa = attn_args(L, &one, w, 1, nlayers, k);
+        aa.ctx = w.ctx;
+        st = attn_run(aa, cs);
+        if (!st && k == nlayers - 1 && last_qkv &&
+            cudaMemcpyAsync(last_qkv + t * L.nqkv, w.qkv, (size_t)L.nqkv * 4, cudaMemcpyDeviceToDevice, cs) != cudaSuccess)
+          st = check_launch("if_run_stack: last_qkv");
+      }
     }
     if (st != IF_ERR_UNSUPPORTED) {
       if (st) return st;
