@@ -9,7 +9,8 @@
 
 namespace ifb {
 
-constexpr int ATT_MAXSPLIT = 16;  // position splits per (token, kv group)
+constexpr int ATT_MAXSPLIT = 32;  // position splits per (token, kv group)
+constexpr int ATT_MAXT = 64;      // split merging (and the fp16 split) up to this many tokens
 
 struct AttnArgs {
   float* qkv;  // [T, (lh + 2 lkv) hd] this rank's projections; q/k rotated in place
@@ -21,7 +22,8 @@ struct AttnArgs {
   float* v;
   int slots, max_ctx, layer;
   int32_t* status;          // nullable device status (IF_ERR_ARG on an out-of-range slot/position)
-  float* part;              // workspace [T][lh][ATT_MAXSPLIT][hd + 2]
+  float* part;              // workspace [min(T, ATT_MAXT)][lh][ATT_MAXSPLIT][hd + 2]
+  uint32_t* cnt;            // workspace, zero between calls: attn_cnt_words(lkv) counters
   float* ctx;               // nullable fp32 [T, lh hd]
   __nv_bfloat16* ctx16;     // nullable bf16 [T, lh hd] (prefill)
   __half* x2;               // nullable fp16 hi/lo split [2 bp, lh hd] (batched decode)
@@ -32,5 +34,6 @@ struct AttnArgs {
 
 if_status attn_run(const AttnArgs& a, cudaStream_t st);
 int attn_nsplit(int64_t T, int lkv, int max_ctx);
+size_t attn_cnt_words(int lkv);
 
 }  // namespace ifb

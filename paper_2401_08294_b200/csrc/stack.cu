@@ -277,7 +277,8 @@ struct WS {
   float* gu;
   float* act;
   float* part;
-  float* attn;  // KV-cache attention partials [T][lh][ATT_MAXSPLIT][hd + 2]
+  float* attn;  // KV-cache attention partials [min(T, ATT_MAXT)][lh][ATT_MAXSPLIT][hd + 2]
+  uint32_t* acnt;  // attention merge counters (self-resetting; fixed offset)
   int* done;  // decode engine: phase counters [4 * MK_MAXL] + epoch
   float* xsimg;  // 3 transformed-input images + sum-h^2 partials (decode engine)
   void* x2;      // batched decode: fp16 hi/lo split of a qGEMV input (2 x 64 x maxK halves)
@@ -307,13 +308,14 @@ static WS carve(void* base, const Local& L, int64_t T) {
   const size_t maxK = (size_t)std::max(std::max(L.d, L.nq), L.lf);
   w.x2 = take(64 * maxK + X2_SC_BYTES / 4);  // [64 per-token scales][2 x 64 x maxK fp16]
   w.x2_bytes = 64 * maxK * 4 + X2_SC_BYTES;
+  w.acnt = reinterpret_cast<uint32_t*>(take(attn_cnt_words(L.lkv)));
   w.a = take((size_t)T * L.d);
   w.qkv = take((size_t)T * L.nqkv);
   w.ctx = take((size_t)T * L.nq);
   w.gu = take((size_t)T * 2 * L.lf);
   w.act = take((size_t)T * L.lf);
   w.part = take((size_t)T * L.d);
-  w.attn = take((size_t)T * L.lh * ATT_MAXSPLIT * (L.hd + 2));
+  w.attn = take((size_t)std::min<int64_t>(T, ATT_MAXT) * L.lh * ATT_MAXSPLIT * (L.hd + 2));
   w.bytes = off;
   return w;
 }
@@ -612,6 +614,7 @@ static AttnArgs attn_args(const Local& L, const KvRun* kvr, const WS& w, int64_t
   a.layer = l;
   a.status = kvr->kv->status;
   a.part = w.attn;
+  a.cnt = w.acnt;
   return a;
 }
 
