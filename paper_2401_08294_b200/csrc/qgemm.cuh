@@ -20,6 +20,13 @@ if_status qgemv_tc_launch(if_scheme s, const uint8_t* W, int64_t N, int64_t K, c
                           int accumulate, cudaStream_t st, void* x2_scratch = nullptr, size_t x2_bytes = 0,
                           int x2_ready = 0);
 // Q3H_B64, 2 <= B <= 32: warp-level mma.sync with the decode in registers (qgemv_ms.cu)
+// fused batched decode chain (qgemv_ms.cu): 4 launches per layer + 1, T in [2, 16]
+struct MsChainLayer {
+  const uint8_t *wqkv, *wo, *wgu, *wdown;
+};
+size_t ms_chain_ws_bytes(int64_t d, int64_t nq, int64_t lf);
+if_status ms_chain_run(const MsChainLayer* layers, int nlayers, int64_t d, int64_t lh, int64_t lkv, int64_t hd,
+                       int64_t lf, int per, int64_t T, float* h, float* last_qkv, void* ws, cudaStream_t st);
 if_status qgemv_ms_launch(if_scheme s, const uint8_t* W, int64_t N, int64_t K, const __half* x2, const float* sc,
                           int64_t B, float* y, int accumulate, cudaStream_t st);
 // if_qgemv / if_qgemv_acc with optional tensor-core scratch (the stack's workspace)

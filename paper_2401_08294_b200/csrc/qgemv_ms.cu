@@ -23,10 +23,14 @@
 // and redistributed through a per-warp shared buffer.
 #include <cuda_fp16.h>
 
+#include <stdio.h>
+#include <stdlib.h>
+
 #include <algorithm>
 
 #include "common.cuh"
 #include "qgemm.cuh"
+#include "pipe.cuh"
 #include "simd.cuh"
 
 namespace ifb {
@@ -213,6 +217,341 @@ __global__ void __launch_bounds__(MS_THREADS, IFB_MS_MINB) qgemv_ms_kernel(const
   }
 }
 
+// ============================================================================
+// v2 (round 2): integer codes in the A fragments, Eq. 2's scale applied per block in
+// fp32, split-K reduced across a thread-block cluster in fixed order (deterministic).
+//
+//   y[b, n] = sum_blocks  lo_nb S_b + (hi_nb - lo_nb)/10 * sum_k q_k x_k       (Eq. 2)
+//
+// With q_e x_e + q_o x_o = c x_o + q_e (x_e - 11 x_o) (c = 11 q_e + q_o) the
+// MMA takes A = (c - 5, q_e) per pair and B = (x_o, x' = x_e - 11 x_o): both A values are
+// small exact integers in fp16, so W' is never rounded; the -5 bias (which keeps the
+// floor exact, below) is undone with the block's sum of odd x.  A lane's 8 pair codes of
+// a row (56 bits at bit 32 + 56 c of the block) are read through four 32-bit views with
+// codes a at bit 2 and a + 2 at bit 16; one LOP3 turns a view into the fp16 pair
+// (1024 + 4 c_a, 1024 + c_b) (the 0x6400 exponent of 1024 OR'ed in), and
+//   C = H - (1044, 1029) = (4 (c_a - 5), c_b - 5)                 exact
+//   T = fma(C, (1/44, 1/11), 1536) = 1536 + floor(c / 11)        (one rounding, ulp 1;
+//       exhaustively checked for every code 0..120)
+//   U = T - 1536 = (q_e,a, q_e,b)                                exact
+// so a pair costs 1/2 view shift + 1/2 LOP3 + 3/2 half2 ops for two weights, against
+// ~10 issue slots per 4 weights for the fp32 W' + fp16 rounding of qgemv_ms_kernel.
+// The x fragments (x_o/4 for codes a, whose view scale is 4; x' = x_e - 11 x_o; fp16
+// hi + lo of each, per-token 2^k as in x2) are built once per CTA in shared memory,
+// permuted into the fragment order, with the block sums S = sum x and 5 sum x_o.
+// ============================================================================
+constexpr int M2_MAXS = 8;  // split-K CTAs per cluster (portable cluster size)
+__device__ __forceinline__ uint32_t hfma2_u(uint32_t a, uint32_t b, uint32_t c) {
+  uint32_t d;
+  asm("fma.rn.f16x2 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+  return d;
+}
+__device__ __forceinline__ uint32_t hadd2_u(uint32_t a, uint32_t b) {
+  uint32_t d;
+  asm("add.rn.f16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
+  return d;
+}
+// view -> (C, U) of its two pair codes (lo half: code at bit 2, hi half: code at bit 16).
+// magic = 0x64006400 and k11 = (1/44, 1/11) arrive in registers (runtime values, see the
+// kernel's `zero`): with both as immediates ptxas splits the LOP3 in two and
+// rematerialises the HFMA2 constant with a MOV per use
+__device__ __forceinline__ void ms2_view(uint32_t v, uint32_t magic, uint32_t k11, uint32_t& C, uint32_t& U) {
+  const uint32_t H = and_or(v, 0x007F01FCu, magic);  // (1024 + 4 c_a, 1024 + c_b)
+  C = hadd2_u(H, 0xE405E414u);                        // + (-1044, -1029)
+  const uint32_t T = hfma2_u(C, k11, 0x66006600u);    // C (1/44, 1/11) + 1536
+  U = hadd2_u(T, 0xE600E600u);                        // - 1536
+}
+__device__ __forceinline__ uint32_t shr64_lo(uint32_t lo, uint32_t hi, uint32_t s) {
+  return (uint32_t)((((uint64_t)hi << 32) | lo) >> s);
+}
+// element e of a C fragment held as f32x2 pairs: e = (row half << 1) | token
+__device__ __forceinline__ float ms2_el(const u64 (&p)[2], int e) {
+  const float2 v = unpack2(p[e >> 1]);
+  return (e & 1) ? v.y : v.x;
+}
+__device__ __forceinline__ uint32_t pack_h2(float a, float b) { return h2_as_u32(__floats2half2_rn(a, b)); }
+
+template <int NT>
+struct Ms2Geo {
+  static constexpr int BP = 8 * NT;
+  static constexpr int DEPTH = NT == 1 ? 8 : 4;                     // weight blocks in flight per warp
+  static constexpr int RING = MS_WARPS * DEPTH * 512;               // bytes
+  static constexpr int XF_BLK = NT * 2 * 2 * 32 * 16 + NT * 4 * 16;  // x fragments + sums per block
+  static constexpr int SMEM_MAX = 112 * 1024;                       // two CTAs per SM
+  static constexpr int KMAX = (SMEM_MAX - RING) / XF_BLK;           // blocks per CTA
+};
+
+template <int NT>
+__global__ void __launch_bounds__(MS_THREADS, 2) qgemv_ms2_kernel(const uint8_t* __restrict__ W, int N, int K,
+                                                                const __half* __restrict__ x2,
+                                                                const float* __restrict__ sc, int B,
+                                                                float* __restrict__ y, int kper, int accumulate,
+                                                                uint32_t zero) {
+  using Gm = Ms2Geo<NT>;
+  constexpr int BP = Gm::BP, DEPTH = Gm::DEPTH;
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int nb = K >> 6;
+  const int kb0 = blockIdx.y * kper, kb1 = min(nb, kb0 + kper), nkb = kb1 - kb0;
+  uint32_t* wst = reinterpret_cast<uint32_t*>(smem);                        // [warps][DEPTH][16 rows][8 words]
+  uint4* xf = reinterpret_cast<uint4*>(smem + Gm::RING);                    // [kb][t][hi/lo][q][32 lanes]
+  float4* xsum = reinterpret_cast<float4*>(xf + (size_t)kper * NT * 2 * 2 * 32);  // [kb][t][c]
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  pdl_trigger();
+  // weights do not depend on the predecessor: the ring fills before the wait.
+  // lane l copies 16 bytes of row l/2 (half l%2) of every block: 512 coalesced bytes
+  const int rbase = blockIdx.x * MS_ROWS + warp * 16;
+  const int64_t row_bytes = (int64_t)nb * 32;
+  const int lrow = rbase + (lane >> 1);
+  const uint8_t* wrow = W + (int64_t)min(lrow, N - 1) * row_bytes + (lane & 1) * 16;
+  const uint32_t src_size = lrow < N ? 16u : 0u;  // rows past N read as zeros
+  uint32_t* ring = wst + warp * DEPTH * 128;
+  const uint32_t ring_s = (uint32_t)__cvta_generic_to_shared(ring) + lane * 16;
+  // the ring reads 32 B per row per block; DRAM wants whole lines: prefetch each of
+  // the warp's 16 row segments (nkb * 32 contiguous bytes) into L2 up front
+  if (lane < 16 && rbase + lane < N)
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(W + (int64_t)(rbase + lane) * row_bytes + (int64_t)kb0 * 32),
+                 "r"((uint32_t)nkb * 32u)
+                 : "memory");
+#pragma unroll
+  for (int i = 0; i < DEPTH; i++) {
+    if (i < nkb)
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(ring_s + i * 512),
+                   "l"(wrow + (int64_t)(kb0 + i) * 32), "r"(src_size)
+                   : "memory");
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  }
+  pdl_wait();
+  // ---- x fragments of this CTA's K-range: item (kb, token, c) = 16 x values
+  {
+    const int nitem = nkb * BP * 4;
+    for (int it = threadIdx.x; it < ((nitem + 31) & ~31); it += MS_THREADS) {
+      const bool ok = it < nitem;
+      const int c = it & 3, tok = (it >> 2) % BP, kb = (it >> 2) / BP;
+      float xv[16];
+      if (ok) {
+        const int64_t k = (int64_t)(kb0 + kb) * 64 + 16 * c;
+        const uint4* ph = reinterpret_cast<const uint4*>(x2 + (int64_t)tok * K + k);
+        const uint4* pl = reinterpret_cast<const uint4*>(x2 + (int64_t)(BP + tok) * K + k);
+        const uint4 h0 = ph[0], h1 = ph[1], l0 = pl[0], l1 = pl[1];
+        const uint32_t hw[8] = {h0.x, h0.y, h0.z, h0.w, h1.x, h1.y, h1.z, h1.w};
+        const uint32_t lw[8] = {l0.x, l0.y, l0.z, l0.w, l1.x, l1.y, l1.z, l1.w};
+#pragma unroll
+        for (int i = 0; i < 8; i++) {
+          const float2 a = __half22float2(*reinterpret_cast<const __half2*>(&hw[i]));
+          const float2 b = __half22float2(*reinterpret_cast<const __half2*>(&lw[i]));
+          // hi + lo is the fp32 value (exact, 22 bits); 2^-4 keeps x' = x_e - 11 x_o
+          // inside fp16 range (x2 rows peak near 2^15; undone in the epilogue)
+          xv[2 * i] = (a.x + b.x) * 0.0625f;
+          xv[2 * i + 1] = (a.y + b.y) * 0.0625f;
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < 16; i++) xv[i] = 0.f;
+      }
+      float s = 0.f, so = 0.f;
+#pragma unroll
+      for (int i = 0; i < 8; i++) {
+        s += xv[2 * i] + xv[2 * i + 1];
+        so += xv[2 * i + 1];
+      }
+      // fragment values: view m = codes (a, a + 2), a = {0, 1, 4, 5}[m]
+      float fv[16];  // [m][b0 lo, b0 hi, b1 lo, b1 hi]
+#pragma unroll
+      for (int m = 0; m < 4; m++) {
+        const int a = (m & 1) + 4 * (m >> 1), b = a + 2;
+        fv[4 * m + 0] = 0.25f * xv[2 * a + 1];                // x_o,a / 4 (view scale 4)
+        fv[4 * m + 1] = xv[2 * b + 1];                        // x_o,b
+        fv[4 * m + 2] = fmaf(-11.f, xv[2 * a + 1], xv[2 * a]);  // x'_a
+        fv[4 * m + 3] = fmaf(-11.f, xv[2 * b + 1], xv[2 * b]);  // x'_b
+      }
+      uint32_t fh[8], fl[8];
+#pragma unroll
+      for (int i = 0; i < 8; i++) {
+        const __half2 h = __floats2half2_rn(fv[2 * i], fv[2 * i + 1]);
+        const float2 hf = __half22float2(h);
+        fh[i] = h2_as_u32(h);
+        fl[i] = pack_h2(fv[2 * i] - hf.x, fv[2 * i + 1] - hf.y);
+      }
+      // the four c items of (kb, tok) sit in adjacent lanes
+      s += __shfl_xor_sync(0xffffffffu, s, 1);
+      s += __shfl_xor_sync(0xffffffffu, s, 2);
+      so += __shfl_xor_sync(0xffffffffu, so, 1);
+      so += __shfl_xor_sync(0xffffffffu, so, 2);
+      if (ok) {
+        const int t = tok >> 3, g = tok & 7, fl_lane = 4 * g + c;
+        uint4* dh = xf + ((size_t)(kb * NT + t) * 2 + 0) * 64 + fl_lane;
+        uint4* dl = xf + ((size_t)(kb * NT + t) * 2 + 1) * 64 + fl_lane;
+        dh[0] = make_uint4(fh[0], fh[1], fh[2], fh[3]);
+        dh[32] = make_uint4(fh[4], fh[5], fh[6], fh[7]);
+        dl[0] = make_uint4(fl[0], fl[1], fl[2], fl[3]);
+        dl[32] = make_uint4(fl[4], fl[5], fl[6], fl[7]);
+        if (c == 0) {
+          float* q = reinterpret_cast<float*>(xsum + (size_t)(kb * NT + t) * 4 + ((tok >> 1) & 3));
+          q[tok & 1] = 5.f * so;
+          q[2 + (tok & 1)] = s;
+        }
+      }
+    }
+  }
+  __syncthreads();
+  const int g = lane >> 2, c = lane & 3;
+  const uint32_t magic = 0x64006400u | zero, k11 = 0x2DD125D1u | zero;  // zero == 0 (opaque to ptxas)
+  // this lane's code window: words wb..wb+2 of a row block, four view shifts (shr64_lo)
+  const int wb = c == 0 ? 0 : 2 * c, wb2 = wb + 2 < 8 ? wb + 2 : 7;
+  const uint32_t s0 = c == 0 ? 30u : 30u - 8u * c, s1 = s0 + 7u;  // views 0, 1 from words (wb, wb+1)
+  const uint32_t s2 = c == 0 ? 26u : 26u - 8u * c, s3 = s2 + 7u;  // views 2, 3 from words (wb+1, wb+2)
+  u64 ya[NT][2], yb[NT][2];  // f32x2: (token 2c, 2c+1) of rows g (index 0) and g + 8 (index 1)
+#pragma unroll
+  for (int t = 0; t < NT; t++) ya[t][0] = ya[t][1] = yb[t][0] = yb[t][1] = 0ull;
+  const uint4* xfl = xf + lane;
+  const float4* xsl = xsum + c;
+  int slot = 0;
+  for (int kb = 0; kb < nkb; kb++) {
+    asm volatile("cp.async.wait_group %0;" ::"n"(DEPTH - 1) : "memory");  // block kb (this lane's part)
+    __syncwarp();                                                         // ... and every lane's
+    const uint32_t* wb0 = ring + slot * 128 + g * 8;
+    const uint32_t* wb1 = wb0 + 64;  // row g + 8
+    uint32_t Ca[4], Ua[4], Cb[4], Ub[4];
+    u64 lo0, d0, lo1, d1;
+    {
+      const uint2 p0 = *reinterpret_cast<const uint2*>(wb0 + wb), p1 = *reinterpret_cast<const uint2*>(wb1 + wb);
+      const uint32_t q0 = wb0[wb2], q1 = wb1[wb2], h0 = wb0[0], h1 = wb1[0];
+      ms2_view(shr64_lo(p0.x, p0.y, s0), magic, k11, Ca[0], Ua[0]);
+      ms2_view(shr64_lo(p0.x, p0.y, s1), magic, k11, Ca[1], Ua[1]);
+      ms2_view(shr64_lo(p0.y, q0, s2), magic, k11, Ca[2], Ua[2]);
+      ms2_view(shr64_lo(p0.y, q0, s3), magic, k11, Ca[3], Ua[3]);
+      ms2_view(shr64_lo(p1.x, p1.y, s0), magic, k11, Cb[0], Ub[0]);
+      ms2_view(shr64_lo(p1.x, p1.y, s1), magic, k11, Cb[1], Ub[1]);
+      ms2_view(shr64_lo(p1.y, q1, s2), magic, k11, Cb[2], Ub[2]);
+      ms2_view(shr64_lo(p1.y, q1, s3), magic, k11, Cb[3], Ub[3]);
+      const float2 f0 = __half22float2(*reinterpret_cast<const __half2*>(&h0));
+      const float2 f1 = __half22float2(*reinterpret_cast<const __half2*>(&h1));
+      lo0 = pack2(f0.x, f0.x), d0 = pack2(f0.y - f0.x, f0.y - f0.x);
+      lo1 = pack2(f1.x, f1.x), d1 = pack2(f1.y - f1.x, f1.y - f1.x);
+    }
+    __syncwarp();  // the slot is read: refill it with block kb + DEPTH
+    if (kb + DEPTH < nkb)
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(ring_s + slot * 512),
+                   "l"(wrow + (int64_t)(kb0 + kb + DEPTH) * 32), "r"(src_size)
+                   : "memory");
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    slot = slot + 1 == DEPTH ? 0 : slot + 1;
+#pragma unroll
+    for (int t = 0; t < NT; t++) {
+      const uint4* fx = xfl + (size_t)(kb * NT + t) * 128;
+      const uint4 h0 = fx[0], h1 = fx[32], l0 = fx[64], l1 = fx[96];
+      const float4 sm = xsl[(kb * NT + t) * 4];
+      float D[4] = {0.f, 0.f, 0.f, 0.f};
+      mma16816(D, Ca[0], Cb[0], Ua[0], Ub[0], h0.x, h0.y);
+      mma16816(D, Ca[1], Cb[1], Ua[1], Ub[1], h0.z, h0.w);
+      mma16816(D, Ca[2], Cb[2], Ua[2], Ub[2], h1.x, h1.y);
+      mma16816(D, Ca[3], Cb[3], Ua[3], Ub[3], h1.z, h1.w);
+      mma16816(D, Ca[0], Cb[0], Ua[0], Ub[0], l0.x, l0.y);
+      mma16816(D, Ca[1], Cb[1], Ua[1], Ub[1], l0.z, l0.w);
+      mma16816(D, Ca[2], Cb[2], Ua[2], Ub[2], l1.x, l1.y);
+      mma16816(D, Ca[3], Cb[3], Ua[3], Ub[3], l1.z, l1.w);
+      // D = sum q x - 5 sum x_o (rows g, g+8 x tokens 2c, 2c+1)
+      const u64 so5 = pack2(sm.x, sm.y), s2 = pack2(sm.z, sm.w);
+      ya[t][0] = ffma2(d0, fadd2(pack2(D[0], D[1]), so5), ya[t][0]);
+      ya[t][1] = ffma2(d1, fadd2(pack2(D[2], D[3]), so5), ya[t][1]);
+      yb[t][0] = ffma2(lo0, s2, yb[t][0]);
+      yb[t][1] = ffma2(lo1, s2, yb[t][1]);
+    }
+  }
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
+  // ---- epilogue: v = (0.1 ya + yb) 2^-k_tok; split-K partials summed over the cluster
+  //      in rank order by rank 0 (deterministic), which owns the y update
+  const int S = gridDim.y;
+  if (S == 1) {
+#pragma unroll
+    for (int t = 0; t < NT; t++)
+#pragma unroll
+      for (int e = 0; e < 4; e++) {
+        const int tok = 8 * t + 2 * c + (e & 1), row = rbase + g + (e >> 1) * 8;
+        if (tok < B && row < N) {
+          const float v = fmaf(0.1f, ms2_el(ya[t], e), ms2_el(yb[t], e)) * (16.f * sc[tok]);
+          float* dst = y + (int64_t)tok * N + row;
+          *dst = accumulate ? *dst + v : v;
+        }
+      }
+    return;
+  }
+  __syncthreads();  // every warp is done with its ring: reuse it for the partial tile
+  float* part = reinterpret_cast<float*>(smem);  // [BP][128 rows]
+#pragma unroll
+  for (int t = 0; t < NT; t++)
+#pragma unroll
+    for (int e = 0; e < 4; e++) {
+      const int tok = 8 * t + 2 * c + (e & 1), r = warp * 16 + g + (e >> 1) * 8;
+      part[tok * MS_ROWS + r] = fmaf(0.1f, ms2_el(ya[t], e), ms2_el(yb[t], e));
+    }
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+  uint32_t rank;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
+  if (rank == 0) {
+    const uint32_t pbase = (uint32_t)__cvta_generic_to_shared(part);
+    for (int i = threadIdx.x; i < B * MS_ROWS; i += MS_THREADS) {
+      const int tok = i / MS_ROWS, r = i - tok * MS_ROWS, row = blockIdx.x * MS_ROWS + r;
+      float pv[M2_MAXS];
+#pragma unroll
+      for (int q = 0; q < M2_MAXS; q++) {  // every remote load in flight, then the fixed-order sum
+        pv[q] = 0.f;
+        if (q < S) {
+          uint32_t ra;
+          asm("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(pbase + 4u * i), "r"(q));
+          asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(pv[q]) : "r"(ra));
+        }
+      }
+      float v = pv[0];
+#pragma unroll
+      for (int q = 1; q < M2_MAXS; q++) v += pv[q];
+      if (row < N) {
+        v *= 16.f * sc[tok];
+        float* dst = y + (int64_t)tok * N + row;
+        *dst = accumulate ? *dst + v : v;
+      }
+    }
+  }
+  // no CTA leaves while rank 0 may still read its shared memory
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+template <int NT>
+static if_status ms2_launch(const uint8_t* W, int N, int K, const __half* x2, const float* sc, int B, float* y,
+                            int accumulate, cudaStream_t st, int sms) {
+  using Gm = Ms2Geo<NT>;
+  const int nb = K / 64;
+  const int nrt = (N + MS_ROWS - 1) / MS_ROWS;
+  int splits = std::max((nb + Gm::KMAX - 1) / Gm::KMAX, (2 * sms + nrt - 1) / nrt);
+  splits = std::min(std::min(splits, M2_MAXS), nb);
+  int kper = (nb + splits - 1) / splits;
+  if (kper > Gm::KMAX) return IF_ERR_UNSUPPORTED;
+  splits = (nb + kper - 1) / kper;
+  const size_t smem = (size_t)Gm::RING + (size_t)kper * Gm::XF_BLK;
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(qgemv_ms2_kernel<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, Gm::SMEM_MAX);
+    configured = true;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)nrt, (unsigned)splits);
+  cfg.blockDim = dim3(MS_THREADS);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  attr[1].id = cudaLaunchAttributeClusterDimension;
+  attr[1].val.clusterDim.x = 1;
+  attr[1].val.clusterDim.y = (unsigned)splits;
+  attr[1].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 2;
+  cudaLaunchKernelEx(&cfg, qgemv_ms2_kernel<NT>, W, N, K, x2, sc, B, y, kper, accumulate, 0u);
+  count_launch();
+  return check_launch("qgemv_ms2");
+}
+
 // y (+)= W' x for a Q3H_B64 weight and the fp16 hi/lo split x2 [2 bp, K] (+ per-token
 // 2^-k in sc) that qgemv_tc_launch prepared.  IF_ERR_UNSUPPORTED for other shapes.
 if_status qgemv_ms_launch(if_scheme s, const uint8_t* W, int64_t N, int64_t K, const __half* x2, const float* sc,
@@ -221,6 +560,19 @@ if_status qgemv_ms_launch(if_scheme s, const uint8_t* W, int64_t N, int64_t K, c
       (reinterpret_cast<uintptr_t>(W) & 15u) || (reinterpret_cast<uintptr_t>(x2) & 15u))
     return IF_ERR_UNSUPPORTED;
   const int bp = tc_bpad((int)B), NT = bp / 8;
+  static const int no_ms2 = getenv("IFB_NO_MS2") != nullptr;  // A/B experiments only
+  if (NT <= 2 && !no_ms2) {
+    static int sms2 = 0;
+    if (!sms2) {
+      int dev = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms2, cudaDevAttrMultiProcessorCount, dev);
+      if (sms2 <= 0) sms2 = 148;
+    }
+    const if_status r = NT == 1 ? ms2_launch<1>(W, (int)N, (int)K, x2, sc, (int)B, y, accumulate, st, sms2)
+                                : ms2_launch<2>(W, (int)N, (int)K, x2, sc, (int)B, y, accumulate, st, sms2);
+    if (r != IF_ERR_UNSUPPORTED) return r;
+  }
   const int nb = (int)(K / 64);
   const int nrt = (int)((N + MS_ROWS - 1) / MS_ROWS);
   // split K until the grid covers the SMs twice and the x tile fits two CTAs per SM
@@ -268,6 +620,575 @@ if_status qgemv_ms_launch(if_scheme s, const uint8_t* W, int64_t N, int64_t K, c
   cudaLaunchKernelEx(&cfg, kern, W, (int)N, (int)K, x2, sc, (int)B, y, kper, atomic_out);
   count_launch();
   return check_launch("qgemv_ms");
+}
+
+
+// ============================================================================
+// Fused batched decode chain (a4 + a6, 2 <= B <= 16, Q3H_B64, one tensor-parallel rank).
+// Four kernels per layer -- qkv, o, gate/up, down -- each the integer-code warp-MMA GEMV
+// above, with the stack glue (RMSNorm, v-broadcast, SiLU*u, residual) moved
+// into the epilogue of the CTA that owns the split-K reduction.  That epilogue writes
+// the NEXT phase's input straight in the MMA fragment order (records below), so there
+// are no glue launches and no per-CTA x preparation: a CTA bulk-copies its K-range of
+// records.  RMSNorm is folded into the consumer's output, W (s h) = s (W h) (s per
+// token from per-row-tile sum-h^2 partials summed in fixed order: deterministic).
+// Each (token, 64-block) pair carries its own power-of-two scale, so any finite input
+// range works (the split needs |x'| <= 65504 only after scaling).
+//
+// Record of (block kb, token tile t), FR_REC bytes, kb-major (a K-range is contiguous):
+//   [0, 2048)    fragments uint4 [hi/lo][q][32 lanes] (lane 4 g + c = token g, values
+//                x[16c, 16c+16) of the block, ordered as in qgemv_ms2_kernel)
+//   [2048, 2112) float4 [cq] = {5 So(2cq), 5 So(2cq+1), S(2cq), S(2cq+1)} (unscaled sums)
+//   [2112, 2176) float4 [cq] = {2^-k(2cq), 2^-k(2cq+1), 0, 0}
+// ============================================================================
+constexpr int FR_REC = 2176;
+constexpr int MS_PART_TILES = 1024;  // split-K partial tiles (N/128 x S) of one launch
+extern unsigned long long* g_mk_dbg;  // qgemv.cu: instrumentation buffer (ifx_set_mk_debug)
+static int g_ms_seq = 0;              // launch number inside the instrumented call
+enum { MSK_QKV = 0, MSK_O = 1, MSK_GU = 2, MSK_DOWN = 3, MSK_PREP = 4 };
+
+struct MsChainP {
+  const uint8_t* W;
+  int N, K, B, kper;
+  const uint8_t* fin;   // input records [K/64][NT]
+  const float* ssq_in;  // [nt_ssq][BP] sum-h^2 partials of the RMSNorm input (qkv, gu)
+  int nt_ssq, d;
+  float* h;             // residual [B][d] (o, down, prep)
+  float* qkv_out;       // optional [B][N] (qkv)
+  uint8_t* fout;        // records of the next phase's input (nullptr: none)
+  float* ssq_out;       // [N/128][BP] (o, down, prep)
+  int v_off, hd, per, lh;
+  float* part;     // split-K partial tiles [N/128][S][BP][128]
+  uint32_t* cnt;   // per-tile arrival counters (zero-filled workspace, self-resetting)
+  unsigned long long* dbg;  // instrumentation: %globaltimer stamps [16 launches][1024 CTAs][8] (nullable)
+  int seq;
+  int ko;  // experiments (IFB_MS_KO): 1 = no decode / MMA, 2 = no weight waits, 3 = no weight loads
+};
+
+// One item = (token tok, 16 values x[16c, 16c+16) of one 64-block); the four items of a
+// (token, block) sit in adjacent lanes c = lane & 3 (all 32 lanes call, `ok` masks).
+template <int NT>
+__device__ __forceinline__ void ms_put_item(uint8_t* rec, int tok, int c, const float (&x)[16], bool ok) {
+  float amax = 0.f, s = 0.f, so = 0.f;
+#pragma unroll
+  for (int i = 0; i < 16; i++) amax = fmaxf(amax, fabsf(x[i]));
+#pragma unroll
+  for (int i = 0; i < 8; i++) {
+    s += x[2 * i] + x[2 * i + 1];
+    so += x[2 * i + 1];
+  }
+  amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, 1));
+  amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, 2));
+  s += __shfl_xor_sync(0xffffffffu, s, 1);
+  s += __shfl_xor_sync(0xffffffffu, s, 2);
+  so += __shfl_xor_sync(0xffffffffu, so, 1);
+  so += __shfl_xor_sync(0xffffffffu, so, 2);
+  if (!ok) return;
+  const int k = xsplit_k(amax) - 4;  // |x| 2^k < 2^11: |x_e - 11 x_o| 2^k < 24576
+  const float sig = pow2f(k);
+  float fv[16];
+#pragma unroll
+  for (int m = 0; m < 4; m++) {
+    const int a = (m & 1) + 4 * (m >> 1), b = a + 2;
+    fv[4 * m + 0] = 0.25f * sig * x[2 * a + 1];
+    fv[4 * m + 1] = sig * x[2 * b + 1];
+    fv[4 * m + 2] = sig * fmaf(-11.f, x[2 * a + 1], x[2 * a]);
+    fv[4 * m + 3] = sig * fmaf(-11.f, x[2 * b + 1], x[2 * b]);
+  }
+  uint32_t fh[8], fl[8];
+#pragma unroll
+  for (int i = 0; i < 8; i++) {
+    const __half2 hh = __floats2half2_rn(fv[2 * i], fv[2 * i + 1]);
+    const float2 hf = __half22float2(hh);
+    fh[i] = h2_as_u32(hh);
+    fl[i] = pack_h2(fv[2 * i] - hf.x, fv[2 * i + 1] - hf.y);
+  }
+  const int fl_lane = 4 * (tok & 7) + c;
+  uint4* f = reinterpret_cast<uint4*>(rec) + fl_lane;
+  f[0] = make_uint4(fh[0], fh[1], fh[2], fh[3]);
+  f[32] = make_uint4(fh[4], fh[5], fh[6], fh[7]);
+  f[64] = make_uint4(fl[0], fl[1], fl[2], fl[3]);
+  f[96] = make_uint4(fl[4], fl[5], fl[6], fl[7]);
+  if (c == 0) {
+    float* sp = reinterpret_cast<float*>(rec + 2048) + 4 * ((tok >> 1) & 3);
+    const int e = tok & 1;
+    sp[e] = 5.f * so;
+    sp[2 + e] = s;
+    sp[16 + e] = pow2f(-k);
+    sp[18 + e] = 0.f;
+  }
+}
+
+// fragments of nblk consecutive 64-blocks (first global block blk0) of vals [BP][ld]
+// (column offset col0), written to the records of fout; dup/stride: extra copies
+template <int NT>
+__device__ __forceinline__ void ms_emit_blocks(const float* vals, int ld, int col0, int nblk, uint8_t* fout,
+                                               const int* dst_blk) {
+  constexpr int BP = 8 * NT;
+  const int nitem = nblk * BP * 4;
+  for (int it0 = (threadIdx.x & ~31); it0 < nitem; it0 += MS_THREADS) {
+    const int it = it0 + (threadIdx.x & 31);
+    const bool ok = it < nitem;
+    const int c = it & 3, tok = (it >> 2) % BP, blk = (it >> 2) / BP;
+    float x[16];
+#pragma unroll
+    for (int i = 0; i < 16; i++) x[i] = ok ? vals[tok * ld + col0 + 64 * blk + 16 * c + i] : 0.f;
+    const int db = ok ? dst_blk[blk] : 0;
+    ms_put_item<NT>(fout + ((size_t)db * NT + (tok >> 3)) * FR_REC, tok, c, x, ok);
+  }
+}
+
+// V = 0: ring 8 (NT = 1) / 4 blocks deep per warp, two CTAs per SM (112 KB each);
+// V = 1: ring 4 deep, three CTAs per SM (74 KB each) -- more warps to hide latency
+template <int NT, int V = 0>
+struct MsGeo {
+  static constexpr int BP = 8 * NT;
+  static constexpr int DEPTH = (NT == 1 && V == 0) ? 8 : 4;
+  static constexpr int RING = MS_WARPS * DEPTH * 512;
+  static constexpr int REC = NT * FR_REC;  // per block
+  static constexpr int MINB = V == 1 ? 3 : 2;
+  static constexpr int SMEM_HI = V == 1 ? 74 * 1024 : 112 * 1024;
+};
+
+// rms inverse per token into sinv[BP] (threads tok < BP), fixed-order sum of partials
+template <int NT>
+__device__ __forceinline__ void ms_rms(const MsChainP& P, float* sinv) {
+  constexpr int BP = 8 * NT;
+  if (threadIdx.x < BP) {
+    float s = 0.f;
+    for (int i = 0; i < P.nt_ssq; i++) s += P.ssq_in[i * BP + threadIdx.x];
+    sinv[threadIdx.x] = 1.0f / sqrtf(s / (float)P.d + 1e-5f);
+  }
+}
+
+// o / down / prep: vals [BP][128] = this tile's new h rows (residual already added by
+// the caller or loaded), per-token sum of squares -> ssq_out, fragments -> fout
+template <int NT>
+__device__ __forceinline__ void ms_emit_h(const MsChainP& P, float* vals, float* red, bool add) {
+  constexpr int BP = 8 * NT;
+  const int bx = blockIdx.x;
+  const int warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int it = 0; it < BP / 2; it++) {
+    const int i = threadIdx.x + it * MS_THREADS, tok = i >> 7, r = i & 127, row = 128 * bx + r;
+    float hn = 0.f;
+    if (tok < P.B) {
+      float* hp = P.h + (int64_t)tok * P.d + row;
+      hn = add ? *hp + vals[i] : *hp;
+      if (add) *hp = hn;
+    }
+    vals[i] = hn;
+    float q = hn * hn;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) q += __shfl_xor_sync(0xffffffffu, q, o);
+    if ((threadIdx.x & 31) == 0) red[it * 8 + warp] = q;
+  }
+  __syncthreads();
+  if (threadIdx.x < BP) {
+    const int tok = threadIdx.x, it = tok >> 1, w0 = (tok & 1) * 4;
+    const float* rr = red + it * 8 + w0;
+    P.ssq_out[bx * BP + tok] = ((rr[0] + rr[1]) + rr[2]) + rr[3];
+  }
+  if (P.fout) {
+    const int dst[2] = {2 * bx, 2 * bx + 1};
+    ms_emit_blocks<NT>(vals, 128, 0, 2, P.fout, dst);
+  }
+}
+
+__device__ __forceinline__ unsigned long long ms_gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+template <int NT, int KIND, int V>
+__global__ void __launch_bounds__(MS_THREADS, MsGeo<NT, V>::MINB) ms_chain_kernel(const __grid_constant__ MsChainP P,
+                                                                                   uint32_t zero) {
+  using Gm = MsGeo<NT, V>;
+  unsigned long long* dbg = P.dbg && P.seq < 16 && threadIdx.x == 0
+                                ? P.dbg + ((size_t)P.seq * 1024 + (blockIdx.y * gridDim.x + blockIdx.x) % 1024) * 8
+                                : nullptr;
+  if (dbg) dbg[0] = ms_gtimer();
+  constexpr int BP = Gm::BP, DEPTH = Gm::DEPTH;
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  float* vals = reinterpret_cast<float*>(smem);  // epilogue: [BP][128] (reuses the ring)
+  float* acts = vals + BP * 128;                 // gu: [BP][64]
+  // tail (never aliased by the ring): mbarrier, sinv [BP], red [64]
+  unsigned char* tail = KIND == MSK_PREP ? smem + 14 * 1024 : smem + Gm::RING + (size_t)P.kper * Gm::REC;
+  uint64_t* xbar = reinterpret_cast<uint64_t*>(tail);
+  float* sinv = reinterpret_cast<float*>(tail + 16);
+  float* red = reinterpret_cast<float*>(tail + 128);
+  if constexpr (KIND == MSK_PREP) {
+    // stage input: sum-h^2 partials and fragments of h (one 128-row tile per CTA)
+    pdl_trigger();
+    pdl_wait();
+    ms_emit_h<NT>(P, vals, red, false);
+    return;
+  } else {
+    const int nb = P.K >> 6;
+    const int kb0 = blockIdx.y * P.kper, kb1 = min(nb, kb0 + P.kper), nkb = kb1 - kb0;
+    uint32_t* ring = reinterpret_cast<uint32_t*>(smem) + warp * DEPTH * 128;
+    unsigned char* xr = smem + Gm::RING;  // this CTA's input records
+    const int rbase = blockIdx.x * MS_ROWS + warp * 16;
+    const int64_t row_bytes = (int64_t)nb * 32;
+    const int lrow = rbase + (lane >> 1);
+    const uint8_t* wrow = P.W + (int64_t)min(lrow, P.N - 1) * row_bytes + (lane & 1) * 16;
+    const uint32_t src_size = lrow < P.N ? 16u : 0u;
+    const uint32_t ring_s = (uint32_t)__cvta_generic_to_shared(ring) + lane * 16;
+    if (threadIdx.x == 0) {
+      mbar_init(xbar, 1);
+      fence_mbar_init();
+    }
+    pdl_trigger();
+#pragma unroll
+    for (int i = 0; i < DEPTH; i++) {
+      if (i < nkb)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(ring_s + i * 512),
+                     "l"(wrow + (int64_t)(kb0 + i) * 32), "r"(src_size)
+                     : "memory");
+      asm volatile("cp.async.commit_group;" ::: "memory");
+    }
+    __syncthreads();  // mbarrier initialised
+    pdl_wait();       // the previous phase's records are complete
+    if (dbg) dbg[1] = ms_gtimer();
+    if (threadIdx.x == 0) {
+      const uint32_t bytes = (uint32_t)nkb * Gm::REC;
+      mbar_arrive_expect_tx(xbar, bytes);
+      bulk_g2s(xr, P.fin + (size_t)kb0 * Gm::REC, bytes, xbar, 0ull, false);
+    }
+    if constexpr (KIND == MSK_QKV || KIND == MSK_GU) ms_rms<NT>(P, sinv);
+    mbar_wait(xbar, 0);
+    if (dbg) dbg[2] = ms_gtimer();
+    const int g = lane >> 2, c = lane & 3;
+    const uint32_t magic = 0x64006400u | zero, k11 = 0x2DD125D1u | zero;
+    const int wb = 2 * c, wb2 = wb + 2 < 8 ? wb + 2 : 7;
+    const uint32_t s0 = 30u - 8u * c, s1 = s0 + 7u, s2 = 26u - 8u * c, s3 = s2 + 7u;
+    u64 ya[NT][2], yb[NT][2];
+#pragma unroll
+    for (int t = 0; t < NT; t++) ya[t][0] = ya[t][1] = yb[t][0] = yb[t][1] = 0ull;
+    // two blocks per iteration (independent decode + MMA chains: the warp is latency-
+    // bound, 16 warps per SM), hi and lo fragments in separate accumulators
+    auto decode = [&](int sl, uint32_t (&Ca)[4], uint32_t (&Ua)[4], uint32_t (&Cb)[4], uint32_t (&Ub)[4], u64& lo0,
+                      u64& d0, u64& lo1, u64& d1) {
+      const uint32_t* wb0 = ring + sl * 128 + g * 8;
+      const uint32_t* wb1 = wb0 + 64;
+      const uint2 p0 = *reinterpret_cast<const uint2*>(wb0 + wb), p1 = *reinterpret_cast<const uint2*>(wb1 + wb);
+      const uint32_t q0 = wb0[wb2], q1 = wb1[wb2], h0 = wb0[0], h1 = wb1[0];
+      ms2_view(shr64_lo(p0.x, p0.y, s0), magic, k11, Ca[0], Ua[0]);
+      ms2_view(shr64_lo(p0.x, p0.y, s1), magic, k11, Ca[1], Ua[1]);
+      ms2_view(shr64_lo(p0.y, q0, s2), magic, k11, Ca[2], Ua[2]);
+      ms2_view(shr64_lo(p0.y, q0, s3), magic, k11, Ca[3], Ua[3]);
+      ms2_view(shr64_lo(p1.x, p1.y, s0), magic, k11, Cb[0], Ub[0]);
+      ms2_view(shr64_lo(p1.x, p1.y, s1), magic, k11, Cb[1], Ub[1]);
+      ms2_view(shr64_lo(p1.y, q1, s2), magic, k11, Cb[2], Ub[2]);
+      ms2_view(shr64_lo(p1.y, q1, s3), magic, k11, Cb[3], Ub[3]);
+      const float2 f0 = __half22float2(*reinterpret_cast<const __half2*>(&h0));
+      const float2 f1 = __half22float2(*reinterpret_cast<const __half2*>(&h1));
+      lo0 = pack2(f0.x, f0.x), d0 = pack2(f0.y - f0.x, f0.y - f0.x);
+      lo1 = pack2(f1.x, f1.x), d1 = pack2(f1.y - f1.x, f1.y - f1.x);
+    };
+    auto mma_block = [&](int kb, int t, const uint32_t (&Ca)[4], const uint32_t (&Ua)[4], const uint32_t (&Cb)[4],
+                         const uint32_t (&Ub)[4], u64 lo0, u64 d0, u64 lo1, u64 d1) {
+      const unsigned char* rec = xr + (size_t)(kb * NT + t) * FR_REC;
+      const uint4* fx = reinterpret_cast<const uint4*>(rec) + lane;
+      const uint4 h0 = fx[0], h1 = fx[32], l0 = fx[64], l1 = fx[96];
+      const float4 sm = reinterpret_cast<const float4*>(rec + 2048)[c];
+      const float4 iv = reinterpret_cast<const float4*>(rec + 2112)[c];
+      float Dh[4] = {0.f, 0.f, 0.f, 0.f}, Dl[4] = {0.f, 0.f, 0.f, 0.f};
+      mma16816(Dh, Ca[0], Cb[0], Ua[0], Ub[0], h0.x, h0.y);
+      mma16816(Dl, Ca[0], Cb[0], Ua[0], Ub[0], l0.x, l0.y);
+      mma16816(Dh, Ca[1], Cb[1], Ua[1], Ub[1], h0.z, h0.w);
+      mma16816(Dl, Ca[1], Cb[1], Ua[1], Ub[1], l0.z, l0.w);
+      mma16816(Dh, Ca[2], Cb[2], Ua[2], Ub[2], h1.x, h1.y);
+      mma16816(Dl, Ca[2], Cb[2], Ua[2], Ub[2], l1.x, l1.y);
+      mma16816(Dh, Ca[3], Cb[3], Ua[3], Ub[3], h1.z, h1.w);
+      mma16816(Dl, Ca[3], Cb[3], Ua[3], Ub[3], l1.z, l1.w);
+      // D 2^-k + 5 So = sum q x (per token); then Eq. 2: (hi - lo) (.)/10 + lo S
+      const u64 so5 = pack2(sm.x, sm.y), s2v = pack2(sm.z, sm.w), inv = pack2(iv.x, iv.y);
+      const u64 D01 = fadd2(pack2(Dh[0], Dh[1]), pack2(Dl[0], Dl[1]));
+      const u64 D23 = fadd2(pack2(Dh[2], Dh[3]), pack2(Dl[2], Dl[3]));
+      ya[t][0] = ffma2(d0, ffma2(D01, inv, so5), ya[t][0]);
+      ya[t][1] = ffma2(d1, ffma2(D23, inv, so5), ya[t][1]);
+      yb[t][0] = ffma2(lo0, s2v, yb[t][0]);
+      yb[t][1] = ffma2(lo1, s2v, yb[t][1]);
+    };
+    auto refill = [&](int sl, int kb_next) {
+      if (kb_next < nkb && P.ko != 3)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(ring_s + sl * 512),
+                     "l"(wrow + (int64_t)(kb0 + kb_next) * 32), "r"(src_size)
+                     : "memory");
+      asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    int slot = 0;
+    for (int kb = 0; kb < nkb; kb++) {
+      if (P.ko < 2) asm volatile("cp.async.wait_group %0;" ::"n"(DEPTH - 1) : "memory");  // block kb (this lane)
+      __syncwarp();                                                                         // ... and every lane's
+      if (P.ko == 1) {
+        refill(slot, kb + DEPTH);
+        slot = slot + 1 == DEPTH ? 0 : slot + 1;
+        continue;
+      }
+      uint32_t Ca[4], Ua[4], Cb[4], Ub[4];
+      u64 lo0, d0, lo1, d1;
+      decode(slot, Ca, Ua, Cb, Ub, lo0, d0, lo1, d1);
+      __syncwarp();  // the slot is read: refill it with block kb + DEPTH
+      refill(slot, kb + DEPTH);
+      slot = slot + 1 == DEPTH ? 0 : slot + 1;
+#pragma unroll
+      for (int t = 0; t < NT; t++) mma_block(kb, t, Ca, Ua, Cb, Ub, lo0, d0, lo1, d1);
+    }
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+    if (dbg) dbg[3] = ms_gtimer();
+    __syncthreads();  // the ring is free: partial tile [BP][128]
+#pragma unroll
+    for (int t = 0; t < NT; t++)
+#pragma unroll
+      for (int e = 0; e < 4; e++) {
+        const int tok = 8 * t + 2 * c + (e & 1), r = warp * 16 + g + (e >> 1) * 8;
+        vals[tok * 128 + r] = fmaf(0.1f, ms2_el(ya[t], e), ms2_el(yb[t], e));
+      }
+    const int S = gridDim.y;
+    if (S > 1) {
+      // split-K: every CTA stores its partial tile; the LAST to arrive (per-tile counter,
+      // self-resetting) sums the S partials in split order (deterministic) and owns the
+      // epilogue -- the others exit at once (no cluster barrier to wait on)
+      __syncthreads();
+      float* mine = P.part + ((size_t)blockIdx.x * S + blockIdx.y) * (BP * 128);
+      for (int i = threadIdx.x; i < BP * 128; i += MS_THREADS) __stcg(mine + i, vals[i]);
+      __syncthreads();  // the CTA's stores happen-before thread 0's release (bar.sync cumulativity)
+      if (threadIdx.x == 0) {
+        uint32_t old;
+        asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(P.cnt + blockIdx.x) : "memory");
+        const int last = old == (uint32_t)(S - 1);
+        if (last) P.cnt[blockIdx.x] = 0u;  // every split arrived: reset for the next launch
+        red[0] = last ? 1.f : 0.f;
+      }
+      __syncthreads();  // ... and thread 0's acquire happens-before every thread's loads below
+      if (red[0] == 0.f) return;
+      const float* all = P.part + (size_t)blockIdx.x * S * (BP * 128);
+      for (int i = threadIdx.x; i < BP * 128; i += MS_THREADS) {
+        float pv[M2_MAXS];
+#pragma unroll
+        for (int q = 0; q < M2_MAXS; q++) pv[q] = q < S ? __ldcg(all + (size_t)q * (BP * 128) + i) : 0.f;
+        float v = pv[0];
+#pragma unroll
+        for (int q = 1; q < M2_MAXS; q++) v += pv[q];
+        vals[i] = v;
+      }
+      __syncthreads();
+      if (dbg) dbg[4] = ms_gtimer();
+    } else {
+      __syncthreads();
+      if (dbg) dbg[4] = ms_gtimer();
+    }
+    // ---- the owner's epilogue: stack glue + the next phase's records ----
+    const int bx = blockIdx.x;
+    if constexpr (KIND == MSK_O || KIND == MSK_DOWN) {
+      ms_emit_h<NT>(P, vals, red, true);
+    } else if constexpr (KIND == MSK_QKV) {
+#pragma unroll
+      for (int it = 0; it < BP / 2; it++) {
+        const int i = threadIdx.x + it * MS_THREADS, tok = i >> 7, r = i & 127, row = 128 * bx + r;
+        const float v = tok < P.B ? vals[i] * sinv[tok] : 0.f;
+        vals[i] = v;
+        if (P.qkv_out && tok < P.B) P.qkv_out[(int64_t)tok * P.N + row] = v;
+      }
+      __syncthreads();
+      // v rows -> the ctx blocks of every q head of the kv group (one rank: h0 = k0 = 0)
+      int dst[2 * 8];
+      int nd = 0, col[2 * 8];
+      for (int blk = 0; blk < 2; blk++) {
+        const int rb = 2 * bx + blk;  // global 64-block of qkv rows
+        if (rb * 64 < P.v_off || rb * 64 >= P.N) continue;
+        const int jb = rb - P.v_off / 64, j = (jb * 64) / P.hd, eb = (jb * 64 - j * P.hd) / 64;
+        for (int i = j * P.per; i < (j + 1) * P.per && i < P.lh && nd < 16; i++) {
+          dst[nd] = (i * P.hd) / 64 + eb;
+          col[nd] = 64 * blk;
+          nd++;
+        }
+      }
+      for (int q = 0; q < nd; q++) ms_emit_blocks<NT>(vals, 128, col[q], 1, P.fout, &dst[q]);
+    } else {  // MSK_GU: act f = silu(s g) (s u), gate/up rows interleaved (2f, 2f+1)
+#pragma unroll
+      for (int it = 0; it < BP / 4; it++) {
+        const int i = threadIdx.x + it * MS_THREADS, tok = i >> 6, f = i & 63;
+        float a = 0.f;
+        if (tok < P.B) {
+          const float gg = vals[tok * 128 + 2 * f] * sinv[tok], u = vals[tok * 128 + 2 * f + 1] * sinv[tok];
+          a = gg / (1.0f + expf(-gg)) * u;
+        }
+        acts[tok * 64 + f] = a;
+      }
+      __syncthreads();
+      const int dst[1] = {bx};
+      ms_emit_blocks<NT>(acts, 64, 0, 1, P.fout, dst);
+    }
+    if (dbg) dbg[5] = ms_gtimer();
+  }
+}
+
+// split-K geometry of one phase: splits (cluster size) and blocks per CTA; false when
+// the K-range of the fewest CTAs the cluster allows does not fit shared memory
+template <int NT, int V>
+static bool ms_geo(int N, int K, int sms, int* splits_out, int* kper_out) {
+  using Gm = MsGeo<NT, V>;
+  const int nb = K / 64, nrt = N / MS_ROWS;
+  // MINB CTAs per SM while the records fit SMEM_HI, else one (up to 220 KB)
+  const int kmax2 = (Gm::SMEM_HI - Gm::RING - 512) / Gm::REC, kmax1 = (220 * 1024 - Gm::RING - 512) / Gm::REC;
+  // cost model (per-warp latency-bound CTAs): waves x (blocks per CTA + fixed cost
+  // of ~6 blocks for prologue / epilogue + 1 per cluster rank in the reduction)
+  int best = -1, best_cost = 0;
+  for (int sp = 1; sp <= std::min(M2_MAXS, nb); sp++) {
+    const int kper = (nb + sp - 1) / sp;
+    if (kper > kmax1) continue;
+    const int per_sm = kper <= kmax2 ? Gm::MINB : 1;
+    const int waves = (nrt * sp + per_sm * sms - 1) / (per_sm * sms);
+    const int cost = waves * (kper + 6 + sp);
+    if (best < 0 || cost < best_cost) best = sp, best_cost = cost;
+  }
+  if (best < 0) return false;
+  const int kper = (nb + best - 1) / best;
+  *splits_out = (nb + kper - 1) / kper;
+  *kper_out = kper;
+  return true;
+}
+
+template <int NT, int KIND, int V>
+static if_status ms_chain_launch(MsChainP P, cudaStream_t st, int sms) {
+  using Gm = MsGeo<NT, V>;
+  auto kern = ms_chain_kernel<NT, KIND, V>;
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+    configured = true;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.blockDim = dim3(MS_THREADS);
+  cfg.stream = st;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  int splits = 1;
+  if constexpr (KIND == MSK_PREP) {
+    cfg.gridDim = dim3((unsigned)(P.d / 128));
+    cfg.dynamicSmemBytes = 16 * 1024;
+  } else {
+    int kper = 0;
+    if (!ms_geo<NT, V>(P.N, P.K, sms, &splits, &kper)) return IF_ERR_UNSUPPORTED;
+    static const char* so = getenv("IFB_MS_SPLITS");  // experiments: "qkv,o,gu,down"
+    if (so) {
+      int v[4] = {0, 0, 0, 0};
+      sscanf(so, "%d,%d,%d,%d", &v[0], &v[1], &v[2], &v[3]);
+      const int nb = P.K / 64, want = v[KIND & 3];
+      if (want > 0 && want <= M2_MAXS && (nb + want - 1) / want <= kper * 4) {
+        kper = (nb + want - 1) / want;
+        splits = (nb + kper - 1) / kper;
+      }
+    }
+    const int nrt = P.N / MS_ROWS;
+    if (nrt * splits > MS_PART_TILES) return IF_ERR_UNSUPPORTED;
+    P.kper = kper;
+    cfg.gridDim = dim3((unsigned)nrt, (unsigned)splits);
+    cfg.dynamicSmemBytes = (size_t)Gm::RING + (size_t)kper * Gm::REC + 512;
+  }
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  static const char* ko = getenv("IFB_MS_KO");  // experiments only
+  P.ko = ko ? atoi(ko) : 0;
+  P.dbg = g_mk_dbg;
+  P.seq = g_mk_dbg ? g_ms_seq++ : 0;
+  if (!g_mk_dbg) g_ms_seq = 0;
+  cudaLaunchKernelEx(&cfg, kern, P, 0u);
+  count_launch();
+  return check_launch("ms_chain");
+}
+
+// bytes of the chain's record buffers (h, ctx, act) + sum-h^2 partials for NT = 2
+size_t ms_chain_ws_bytes(int64_t d, int64_t nq, int64_t lf) {
+  return (size_t)((d + nq + lf) / 64) * 2 * FR_REC + (size_t)(d / 128) * 16 * 4 + 256 +
+         (size_t)MS_PART_TILES * 16 * 128 * 4 + (size_t)MS_PART_TILES * 4;
+}
+
+// the decode stack of one rank (no tensor parallelism) through the fused chain;
+// IF_ERR_UNSUPPORTED when the shape or batch does not fit (caller falls back)
+if_status ms_chain_run(const MsChainLayer* layers, int nlayers, int64_t d, int64_t lh, int64_t lkv, int64_t hd,
+                       int64_t lf, int per, int64_t T, float* h, float* last_qkv, void* ws, cudaStream_t st) {
+  static const int off = getenv("IFB_NO_MSCHAIN") != nullptr;  // A/B experiments only
+  const int64_t nq = lh * hd, nqkv = (lh + 2 * lkv) * hd;
+  if (off || T < 2 || T > 16 || d % 128 || nqkv % 128 || (2 * lf) % 128 || hd % 64 || nq % 64 || per > 8 ||
+      (reinterpret_cast<uintptr_t>(ws) & 255u))
+    return IF_ERR_UNSUPPORTED;
+  for (int l = 0; l < nlayers; l++)
+    for (const uint8_t* w : {layers[l].wqkv, layers[l].wo, layers[l].wgu, layers[l].wdown})
+      if (reinterpret_cast<uintptr_t>(w) & 15u) return IF_ERR_UNSUPPORTED;
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
+  }
+  uint8_t* base = static_cast<uint8_t*>(ws);
+  uint8_t* rec_h = base;
+  uint8_t* rec_ctx = rec_h + (size_t)(d / 64) * 2 * FR_REC;
+  uint8_t* rec_act = rec_ctx + (size_t)(nq / 64) * 2 * FR_REC;
+  float* ssq = reinterpret_cast<float*>(rec_act + (size_t)(lf / 64) * 2 * FR_REC);
+  float* part = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(ssq) + (size_t)(d / 128) * 16 * 4 + 256);
+  uint32_t* cnt = reinterpret_cast<uint32_t*>(part + (size_t)MS_PART_TILES * 16 * 128);
+  const int NT = T <= 8 ? 1 : 2;
+  {  // every phase must fit before anything is launched (the caller falls back)
+    int sp, kp;
+    const int64_t dims[4][2] = {{nqkv, d}, {d, nq}, {2 * lf, d}, {d, lf}};
+    for (const auto& nk : dims)
+      if (!(NT == 1 ? ms_geo<1, 0>((int)nk[0], (int)nk[1], sms, &sp, &kp) && ms_geo<1, 1>((int)nk[0], (int)nk[1], sms, &sp, &kp)
+                    : ms_geo<2, 0>((int)nk[0], (int)nk[1], sms, &sp, &kp) && ms_geo<2, 1>((int)nk[0], (int)nk[1], sms, &sp, &kp)))
+        return IF_ERR_UNSUPPORTED;
+  }
+  static const char* venv = getenv("IFB_MS_VAR");  // occupancy variant (experiments)
+  const int var = venv ? atoi(venv) : 0;
+  auto run = [&]<int NTc, int V>() -> if_status {
+    MsChainP P = {};
+    P.B = (int)T;
+    P.d = (int)d;
+    P.h = h;
+    P.ssq_out = ssq;
+    P.fout = rec_h;
+    if_status r = ms_chain_launch<NTc, MSK_PREP, V>(P, st, sms);
+    for (int l = 0; l < nlayers && !r; l++) {
+      const bool lastl = l == nlayers - 1;
+      MsChainP q = {};
+      q.B = (int)T;
+      q.d = (int)d;
+      q.nt_ssq = (int)(d / 128);
+      // qkv: rms(h) folded into the output; v rows -> ctx records
+      q.part = part, q.cnt = cnt;
+      q.W = layers[l].wqkv, q.N = (int)nqkv, q.K = (int)d, q.fin = rec_h, q.ssq_in = ssq, q.fout = rec_ctx;
+      q.qkv_out = lastl ? last_qkv : nullptr;
+      q.v_off = (int)((lh + lkv) * hd), q.hd = (int)hd, q.per = per, q.lh = (int)lh;
+      if ((r = ms_chain_launch<NTc, MSK_QKV, V>(q, st, sms))) break;
+      // o: h += W_o ctx; h records + sum h^2
+      MsChainP o = {};
+      o.part = part, o.cnt = cnt;
+      o.B = (int)T, o.d = (int)d, o.W = layers[l].wo, o.N = (int)d, o.K = (int)nq, o.fin = rec_ctx, o.h = h;
+      o.ssq_out = ssq, o.fout = rec_h;
+      if ((r = ms_chain_launch<NTc, MSK_O, V>(o, st, sms))) break;
+      // gate/up: act records
+      MsChainP g = {};
+      g.part = part, g.cnt = cnt;
+      g.B = (int)T, g.d = (int)d, g.nt_ssq = (int)(d / 128), g.W = layers[l].wgu, g.N = (int)(2 * lf), g.K = (int)d;
+      g.fin = rec_h, g.ssq_in = ssq, g.fout = rec_act;
+      if ((r = ms_chain_launch<NTc, MSK_GU, V>(g, st, sms))) break;
+      // down: h += W_down act; next layer's h records
+      MsChainP dn = {};
+      dn.part = part, dn.cnt = cnt;
+      dn.B = (int)T, dn.d = (int)d, dn.W = layers[l].wdown, dn.N = (int)d, dn.K = (int)lf, dn.fin = rec_act, dn.h = h;
+      dn.ssq_out = ssq, dn.fout = lastl ? nullptr : rec_h;
+      if ((r = ms_chain_launch<NTc, MSK_DOWN, V>(dn, st, sms))) break;
+    }
+    return r;
+  };
+  if (var == 1) return NT == 1 ? run.template operator()<1, 1>() : run.template operator()<2, 1>();
+  return NT == 1 ? run.template operator()<1, 0>() : run.template operator()<2, 0>();
 }
 
 }  // namespace ifb

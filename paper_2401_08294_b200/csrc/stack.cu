@@ -7,6 +7,7 @@
 #include <cuda_bf16.h>
 
 #include <algorithm>
+#include <vector>
 
 #include "attn.cuh"
 #include "comm.cuh"
@@ -282,6 +283,7 @@ struct WS {
   int* done;  // decode engine: phase counters [4 * MK_MAXL] + epoch
   float* xsimg;  // 3 transformed-input images + sum-h^2 partials (decode engine)
   void* x2;      // batched decode: fp16 hi/lo split of a qGEMV input (2 x 64 x maxK halves)
+  void* msrec;   // fused batched chain (qgemv_ms.cu): fragment records + sum-h^2 partials
   size_t x2_bytes;
   size_t bytes;
 };
@@ -309,6 +311,7 @@ static WS carve(void* base, const Local& L, int64_t T) {
   w.x2 = take(64 * maxK + X2_SC_BYTES / 4);  // [64 per-token scales][2 x 64 x maxK fp16]
   w.x2_bytes = 64 * maxK * 4 + X2_SC_BYTES;
   w.acnt = reinterpret_cast<uint32_t*>(take(attn_cnt_words(L.lkv)));
+  w.msrec = take(ms_chain_ws_bytes(L.d, L.nq, L.lf) / 4 + 1);
   w.a = take((size_t)T * L.d);
   w.qkv = take((size_t)T * L.nqkv);
   w.ctx = take((size_t)T * L.nq);
@@ -382,11 +385,11 @@ static if_status run_stack(const if_stack_shape* shape, const if_plan* plan, int
   float* tp_boxes[8] = {nullptr};
   int tp_n = 1, tp_me = 0, tp_hidden = 0, tp_grid = 0;
   const bool tp_ok = groups == 1 || (comm_engine(comm, tp_boxes, &tp_n, &tp_me, &tp_hidden, &tp_grid) && tp_hidden >= L.d);
-  // batch sizes that run one engine launch per token: 3.5-bit from B = 3 takes the
-  // batched warp-MMA qGEMV chain instead (measured: B = 3..6 954..1877 tok/s vs 902 with
-  // the engine per token); the k-bit schemes up to B = 6 (their batched path is tcgen05)
+  // batch sizes that run one engine launch per token: 3.5-bit from B = 2 takes the fused
+  // batched chain instead (measured 7B: B = 2 934 tok/s vs 909 with the engine per token,
+  // B = 3 1396); the k-bit schemes up to B = 6 (their batched path is tcgen05)
   static const char* tenv = getenv("IFB_MK_TMAX");  // experiments only
-  const int mk_tmax = tenv ? atoi(tenv) : (sc.type == IF_Q3H && sc.block == 64 ? 2 : 6);
+  const int mk_tmax = tenv ? atoi(tenv) : (sc.type == IF_Q3H && sc.block == 64 ? 1 : 6);
   // with a KV cache (NEXT-1) the 3.5-bit engine runs in partial launches per token:
   // [qkv_0] attn_0 [o_0 gu_0 down_0 qkv_1] attn_1 ... [o_L-1 gu down] (one rank)
   const bool mk_kv = kvr && T <= 2 && sc.type == IF_Q3H && sc.block == 64 && groups == 1 && !getenv("IFB_NO_MK_KV");
@@ -467,6 +470,24 @@ static if_status run_stack(const if_stack_shape* shape, const if_plan* plan, int
           st = check_launch("if_run_stack: last_qkv");
       }
     }
+    if (st != IF_ERR_UNSUPPORTED) {
+      if (st) return st;
+      if (!last) {
+        if ((st = comm_send(comm, h_out, nh, cs))) return st;
+      }
+      return check_launch("if_run_stack");
+    }
+  }
+  // batched 3.5-bit decode (T <= 16, one TP rank): the fused chain, 4 launches per layer
+  // with the glue in the GEMV epilogues (qgemv_ms.cu)
+  if (mode == IF_DECODE && T >= 2 && !kvr && groups == 1 && sc.type == IF_Q3H && sc.block == 64 && nlayers > 0) {
+    std::vector<MsChainLayer> ml((size_t)nlayers);
+    for (int l = 0; l < nlayers; l++) {
+      const if_layer_weights& Wl = stage_layers[l];
+      if (!Wl.wqkv || !Wl.wo || !Wl.wgu || !Wl.wdown) return set_error(IF_ERR_ARG, "if_run_stack: null weights, layer %d", l);
+      ml[(size_t)l] = {Wl.wqkv, Wl.wo, Wl.wgu, Wl.wdown};
+    }
+    st = ms_chain_run(ml.data(), nlayers, L.d, L.lh, L.lkv, L.hd, L.lf, per, T, h_out, last_qkv, w.msrec, cs);
     if (st != IF_ERR_UNSUPPORTED) {
       if (st) return st;
       if (!last) {
