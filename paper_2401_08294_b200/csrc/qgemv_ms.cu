@@ -643,6 +643,7 @@ if_status qgemv_ms_launch(if_scheme s, const uint8_t* W, int64_t N, int64_t K, c
 // ============================================================================
 constexpr int FR_REC = 2176;
 constexpr int MS_PART_TILES = 1024;  // split-K partial tiles (N/128 x S) of one launch
+constexpr int MS_BPMAX = 32;         // tokens (4 tiles of 8)
 extern unsigned long long* g_mk_dbg;  // qgemv.cu: instrumentation buffer (ifx_set_mk_debug)
 static int g_ms_seq = 0;              // launch number inside the instrumented call
 enum { MSK_QKV = 0, MSK_O = 1, MSK_GU = 2, MSK_DOWN = 3, MSK_PREP = 4 };
@@ -813,11 +814,11 @@ __global__ void __launch_bounds__(MS_THREADS, MsGeo<NT, V>::MINB) ms_chain_kerne
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   float* vals = reinterpret_cast<float*>(smem);  // epilogue: [BP][128] (reuses the ring)
   float* acts = vals + BP * 128;                 // gu: [BP][64]
-  // tail (never aliased by the ring): mbarrier, sinv [BP], red [64]
-  unsigned char* tail = KIND == MSK_PREP ? smem + 14 * 1024 : smem + Gm::RING + (size_t)P.kper * Gm::REC;
+  // tail (never aliased by the ring, the records or vals/acts): mbarrier, sinv [BP], red [128]
+  unsigned char* tail = KIND == MSK_PREP ? smem + 24 * 1024 : smem + Gm::RING + (size_t)P.kper * Gm::REC;
   uint64_t* xbar = reinterpret_cast<uint64_t*>(tail);
-  float* sinv = reinterpret_cast<float*>(tail + 16);
-  float* red = reinterpret_cast<float*>(tail + 128);
+  float* sinv = reinterpret_cast<float*>(tail + 64);
+  float* red = reinterpret_cast<float*>(tail + 256);
   if constexpr (KIND == MSK_PREP) {
     // stage input: sum-h^2 partials and fragments of h (one 128-row tile per CTA)
     pdl_trigger();
@@ -1034,13 +1035,13 @@ static bool ms_geo(int N, int K, int sms, int* splits_out, int* kper_out) {
   using Gm = MsGeo<NT, V>;
   const int nb = K / 64, nrt = N / MS_ROWS;
   // MINB CTAs per SM while the records fit SMEM_HI, else one (up to 220 KB)
-  const int kmax2 = (Gm::SMEM_HI - Gm::RING - 512) / Gm::REC, kmax1 = (220 * 1024 - Gm::RING - 512) / Gm::REC;
+  const int kmax2 = (Gm::SMEM_HI - Gm::RING - 1024) / Gm::REC, kmax1 = (220 * 1024 - Gm::RING - 1024) / Gm::REC;
   // cost model (per-warp latency-bound CTAs): waves x (blocks per CTA + fixed cost
   // of ~6 blocks for prologue / epilogue + 1 per cluster rank in the reduction)
   int best = -1, best_cost = 0;
   for (int sp = 1; sp <= std::min(M2_MAXS, nb); sp++) {
     const int kper = (nb + sp - 1) / sp;
-    if (kper > kmax1) continue;
+    if (kper > kmax1 || Gm::BP * 192 * 4 > Gm::RING + kper * Gm::REC || nrt * sp > MS_PART_TILES) continue;
     const int per_sm = kper <= kmax2 ? Gm::MINB : 1;
     const int waves = (nrt * sp + per_sm * sms - 1) / (per_sm * sms);
     const int cost = waves * (kper + 6 + sp);
@@ -1071,7 +1072,7 @@ static if_status ms_chain_launch(MsChainP P, cudaStream_t st, int sms) {
   int splits = 1;
   if constexpr (KIND == MSK_PREP) {
     cfg.gridDim = dim3((unsigned)(P.d / 128));
-    cfg.dynamicSmemBytes = 16 * 1024;
+    cfg.dynamicSmemBytes = 25 * 1024;
   } else {
     int kper = 0;
     if (!ms_geo<NT, V>(P.N, P.K, sms, &splits, &kper)) return IF_ERR_UNSUPPORTED;
@@ -1089,7 +1090,7 @@ static if_status ms_chain_launch(MsChainP P, cudaStream_t st, int sms) {
     if (nrt * splits > MS_PART_TILES) return IF_ERR_UNSUPPORTED;
     P.kper = kper;
     cfg.gridDim = dim3((unsigned)nrt, (unsigned)splits);
-    cfg.dynamicSmemBytes = (size_t)Gm::RING + (size_t)kper * Gm::REC + 512;
+    cfg.dynamicSmemBytes = (size_t)Gm::RING + (size_t)kper * Gm::REC + 1024;
   }
   cfg.attrs = attr;
   cfg.numAttrs = 1;
@@ -1105,8 +1106,8 @@ static if_status ms_chain_launch(MsChainP P, cudaStream_t st, int sms) {
 
 // bytes of the chain's record buffers (h, ctx, act) + sum-h^2 partials for NT = 2
 size_t ms_chain_ws_bytes(int64_t d, int64_t nq, int64_t lf) {
-  return (size_t)((d + nq + lf) / 64) * 2 * FR_REC + (size_t)(d / 128) * 16 * 4 + 256 +
-         (size_t)MS_PART_TILES * 16 * 128 * 4 + (size_t)MS_PART_TILES * 4;
+  return (size_t)((d + nq + lf) / 64) * 4 * FR_REC + (size_t)(d / 128) * MS_BPMAX * 4 + 256 +
+         (size_t)MS_PART_TILES * MS_BPMAX * 128 * 4 + (size_t)MS_PART_TILES * 4;
 }
 
 // the decode stack of one rank (no tensor parallelism) through the fused chain;
@@ -1130,22 +1131,21 @@ if_status ms_chain_run(const MsChainLayer* layers, int nlayers, int64_t d, int64
   }
   uint8_t* base = static_cast<uint8_t*>(ws);
   uint8_t* rec_h = base;
-  uint8_t* rec_ctx = rec_h + (size_t)(d / 64) * 2 * FR_REC;
-  uint8_t* rec_act = rec_ctx + (size_t)(nq / 64) * 2 * FR_REC;
-  float* ssq = reinterpret_cast<float*>(rec_act + (size_t)(lf / 64) * 2 * FR_REC);
-  float* part = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(ssq) + (size_t)(d / 128) * 16 * 4 + 256);
-  uint32_t* cnt = reinterpret_cast<uint32_t*>(part + (size_t)MS_PART_TILES * 16 * 128);
-  const int NT = T <= 8 ? 1 : 2;
+  uint8_t* rec_ctx = rec_h + (size_t)(d / 64) * 4 * FR_REC;
+  uint8_t* rec_act = rec_ctx + (size_t)(nq / 64) * 4 * FR_REC;
+  float* ssq = reinterpret_cast<float*>(rec_act + (size_t)(lf / 64) * 4 * FR_REC);
+  float* part = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(ssq) + (size_t)(d / 128) * MS_BPMAX * 4 + 256);
+  uint32_t* cnt = reinterpret_cast<uint32_t*>(part + (size_t)MS_PART_TILES * MS_BPMAX * 128);
+  const int NT = T <= 8 ? 1 : T <= 16 ? 2 : 4;
   {  // every phase must fit before anything is launched (the caller falls back)
     int sp, kp;
     const int64_t dims[4][2] = {{nqkv, d}, {d, nq}, {2 * lf, d}, {d, lf}};
     for (const auto& nk : dims)
-      if (!(NT == 1 ? ms_geo<1, 0>((int)nk[0], (int)nk[1], sms, &sp, &kp) && ms_geo<1, 1>((int)nk[0], (int)nk[1], sms, &sp, &kp)
-                    : ms_geo<2, 0>((int)nk[0], (int)nk[1], sms, &sp, &kp) && ms_geo<2, 1>((int)nk[0], (int)nk[1], sms, &sp, &kp)))
+      if (!(NT == 1   ? ms_geo<1, 0>((int)nk[0], (int)nk[1], sms, &sp, &kp)
+            : NT == 2 ? ms_geo<2, 0>((int)nk[0], (int)nk[1], sms, &sp, &kp)
+                      : ms_geo<4, 0>((int)nk[0], (int)nk[1], sms, &sp, &kp)))
         return IF_ERR_UNSUPPORTED;
   }
-  static const char* venv = getenv("IFB_MS_VAR");  // occupancy variant (experiments)
-  const int var = venv ? atoi(venv) : 0;
   auto run = [&]<int NTc, int V>() -> if_status {
     MsChainP P = {};
     P.B = (int)T;
@@ -1187,8 +1187,7 @@ if_status ms_chain_run(const MsChainLayer* layers, int nlayers, int64_t d, int64
     }
     return r;
   };
-  if (var == 1) return NT == 1 ? run.template operator()<1, 1>() : run.template operator()<2, 1>();
-  return NT == 1 ? run.template operator()<1, 0>() : run.template operator()<2, 0>();
+  return NT == 1 ? run.template operator()<1, 0>() : NT == 2 ? run.template operator()<2, 0>() : run.template operator()<4, 0>();
 }
 
 }  // namespace ifb

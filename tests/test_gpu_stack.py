@@ -47,8 +47,9 @@ def _oracle(cfg, qtype, bs, stk, h):
 @pytest.mark.parametrize("qtype,bs", [(35, 64), (4, 32), (3, 32), (8, 64), (2, 64)])
 @pytest.mark.parametrize("T", [1, 4, 7, 16])
 def test_stack_decode_small(qtype, bs, T):
-    """T <= 6 (Q3H_B64): the persistent engine once per token; T >= 7: the tensor-core
-    batched qGEMV (fp16 W', fp16 hi/lo x, Q23) -- both held to 1e-3."""
+    """Q3H_B64: T = 1 the persistent engine, T >= 2 the fused batched chain (integer codes
+    in mma.sync fragments); k-bit schemes: the engine once per token up to T = 6, then the
+    tensor-core batched qGEMV (fp16 W', fp16 hi/lo x, Q23) -- all held to 1e-3."""
     stk, h, out, qkv = _run(SMALL, qtype, bs, T)
     ho, qo = _oracle(SMALL, qtype, bs, stk, h)
     assert normwise(out, ho) <= 1e-3
@@ -190,3 +191,35 @@ def test_stack_decode_large_activations(T):
     o = out.cpu().numpy()
     assert np.all(np.isfinite(o))
     assert normwise(o, ho) <= 1e-3
+
+
+@pytest.mark.parametrize("T", [2, 8, 12, 16])
+def test_stack_chain_parity_deterministic(T):
+    """The fused batched chain (qgemv_ms.cu: 3.5-bit, 2 <= T <= 16, one rank): 1e-3 vs the
+    oracle, exactly 1 + 4 L launches, and bit-identical across runs (the split-K partials
+    are summed in split order by the last CTA to arrive, whatever the arrival order)."""
+    d = dev()
+    cfg = SMALL
+    s = F.scheme(35, 64)
+    shape = F.stack_shape(*[cfg[k] for k in ("layers", "hidden", "heads", "kv_heads", "head_dim", "ffn")], s)
+    plan = F.if_plan_partition(F.IF_BY_LAYER, shape, 1)
+    stk = Stack(cfg, s, plan, 0, d)
+    h = synth.activations(T, cfg["hidden"], tid=11)
+    hd = torch.from_numpy(h).to(d)
+    nqkv = (cfg["heads"] + 2 * cfg["kv_heads"]) * cfg["head_dim"]
+    ws = torch.zeros(F.if_stack_workspace_bytes(shape, plan, 0, T, F.IF_DECODE), dtype=torch.uint8, device=d)
+    outs, qkvs = [], []
+    for rep in range(3):
+        out = torch.empty_like(hd)
+        qkv = torch.empty(T, nqkv, device=d)
+        F.if_launch_count(True)
+        F.if_run_stack(shape, plan, 0, None, stk.arr, hd, T, F.IF_DECODE, out, qkv, ws)
+        torch.cuda.synchronize()
+        assert F.if_launch_count() == 1 + 4 * cfg["layers"]
+        outs.append(out.cpu().numpy())
+        qkvs.append(qkv.cpu().numpy())
+    assert np.array_equal(outs[0], outs[1]) and np.array_equal(outs[0], outs[2])
+    assert np.array_equal(qkvs[0], qkvs[1])
+    ho, qo = _oracle(cfg, 35, 64, stk, h)
+    assert normwise(outs[0], ho) <= 1e-3
+    assert normwise(qkvs[0], qo) <= 1e-3
