@@ -27,6 +27,7 @@
 #include <cuda_bf16.h>
 
 #include "attn.cuh"
+#include "ms_rec.cuh"
 #include "common.cuh"
 
 namespace ifb {
@@ -128,7 +129,7 @@ __global__ void __launch_bounds__(128) attn_kernel(const float* __restrict__ qkv
                                                    const float* __restrict__ vc, int slots, int max_ctx, int nsplit,
                                                    float* part, uint32_t* gcnt, uint32_t* tcnt, float* ctx,
                                                    __nv_bfloat16* __restrict__ ctx16, __half* __restrict__ x2, int bp,
-                                                   float* __restrict__ x2sc) {
+                                                   float* __restrict__ x2sc, uint8_t* __restrict__ rec, int rec_nt) {
   pdl_trigger();
   pdl_wait();
   constexpr int NW = ATT_NW, U = ATT_U, hd = 32 * EPL;
@@ -272,6 +273,21 @@ __global__ void __launch_bounds__(128) attn_kernel(const float* __restrict__ qkv
       if (ctx16) ctx16[o] = __float2bfloat16(v);
     }
   }
+  if (rec) {
+    // this CTA wrote the final ctx of (t, group jl): per * hd values = nblk 64-blocks,
+    // re-read (same CTA, after the barrier) into the chain's fragment records
+    __syncthreads();
+    const int nblk = per * hd / 64, gb0 = jl * per * hd / 64, nit = nblk * 4;
+    for (int it0 = threadIdx.x & ~31; it0 < ((nit + 31) & ~31); it0 += blockDim.x) {
+      const int it = it0 + lane, blk = it >> 2, c = it & 3;
+      const bool ok = it < nit;
+      float x[16];
+      const float* src = ctx + (int64_t)t * nq + (int64_t)(gb0 + blk) * 64 + 16 * c;
+#pragma unroll
+      for (int i = 0; i < 16; i++) x[i] = ok ? src[i] : 0.f;
+      ms_put_item(rec + ((size_t)(gb0 + (ok ? blk : 0)) * rec_nt + (t >> 3)) * FR_REC, t, c, x, ok);
+    }
+  }
   if (!x2) return;
   // the last group of token t to arrive writes the row's fp16 hi/lo split (common.cuh)
   __threadfence();
@@ -341,7 +357,7 @@ static void attn_launch(const AttnArgs& a, float* kc, float* vc, int ns, cudaStr
   const dim3 gb((unsigned)(a.T * a.lkv), (unsigned)ns);
   launch_attn(attn_kernel<EPL>, gb, 128, 0, st, a.pdl, (const float*)a.qkv, (int)a.T, a.lh, a.lkv, a.slot_ids,
               a.positions, (const float*)kc, (const float*)vc, a.slots, a.max_ctx, ns, a.part, a.cnt,
-              a.cnt ? a.cnt + (size_t)ATT_MAXT * a.lkv : nullptr, a.ctx, a.ctx16, a.x2, a.bp, a.x2sc);
+              a.cnt ? a.cnt + (size_t)ATT_MAXT * a.lkv : nullptr, a.ctx, a.ctx16, a.x2, a.bp, a.x2sc, a.rec, a.rec_nt);
 }
 
 if_status attn_run(const AttnArgs& a, cudaStream_t st) {
@@ -352,6 +368,7 @@ if_status attn_run(const AttnArgs& a, cudaStream_t st) {
   if ((ns > 1 || a.x2) && (!a.cnt || a.T > ATT_MAXT || !a.part))
     return set_error(IF_ERR_ARG, "attention: split merge needs the counter / partial workspace (T=%lld)", (long long)a.T);
   if (a.x2 && (!a.ctx || a.bp < a.T)) return set_error(IF_ERR_ARG, "attention: fp16 split needs the fp32 context");
+  if (a.rec && (!a.ctx || a.hd % 64 || a.rec_nt * 8 < a.T)) return set_error(IF_ERR_ARG, "attention: records need the fp32 context");
   const size_t layer_elems = (size_t)a.slots * a.max_ctx * a.lkv * a.hd;
   float* kc = a.k + (size_t)a.layer * layer_elems;
   float* vc = a.v + (size_t)a.layer * layer_elems;

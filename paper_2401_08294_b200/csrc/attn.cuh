@@ -29,6 +29,8 @@ struct AttnArgs {
   __half* x2;               // nullable fp16 hi/lo split [2 bp, lh hd] (batched decode)
   int bp;
   float* x2sc;              // per-token 2^-k of the split
+  uint8_t* rec;             // nullable: fragment records of ctx for the fused batched chain (ms_rec.cuh)
+  int rec_nt;               // token tiles of 8 per record block (1 or 2)
   bool pdl;
 };
 

@@ -25,8 +25,11 @@ struct MsChainLayer {
   const uint8_t *wqkv, *wo, *wgu, *wdown;
 };
 size_t ms_chain_ws_bytes(int64_t d, int64_t nq, int64_t lf);
+// attention step of a KV-cache chain: layer l, ctx record buffer, token tiles per block
+typedef if_status (*MsAttnFn)(void* ctx, int layer, uint8_t* rec_ctx, int nt);
 if_status ms_chain_run(const MsChainLayer* layers, int nlayers, int64_t d, int64_t lh, int64_t lkv, int64_t hd,
-                       int64_t lf, int per, int64_t T, float* h, float* last_qkv, void* ws, cudaStream_t st);
+                       int64_t lf, int per, int64_t T, float* h, float* last_qkv, void* ws, cudaStream_t st,
+                       MsAttnFn attn = nullptr, void* actx = nullptr, float* qkv_buf = nullptr);
 if_status qgemv_ms_launch(if_scheme s, const uint8_t* W, int64_t N, int64_t K, const __half* x2, const float* sc,
                           int64_t B, float* y, int accumulate, cudaStream_t st);
 // if_qgemv / if_qgemv_acc with optional tensor-core scratch (the stack's workspace)

@@ -30,6 +30,7 @@
 
 #include "common.cuh"
 #include "qgemm.cuh"
+#include "ms_rec.cuh"
 #include "pipe.cuh"
 #include "simd.cuh"
 
@@ -635,13 +636,7 @@ if_status qgemv_ms_launch(if_scheme s, const uint8_t* W, int64_t N, int64_t K, c
 // Each (token, 64-block) pair carries its own power-of-two scale, so any finite input
 // range works (the split needs |x'| <= 65504 only after scaling).
 //
-// Record of (block kb, token tile t), FR_REC bytes, kb-major (a K-range is contiguous):
-//   [0, 2048)    fragments uint4 [hi/lo][q][32 lanes] (lane 4 g + c = token g, values
-//                x[16c, 16c+16) of the block, ordered as in qgemv_ms2_kernel)
-//   [2048, 2112) float4 [cq] = {5 So(2cq), 5 So(2cq+1), S(2cq), S(2cq+1)} (unscaled sums)
-//   [2112, 2176) float4 [cq] = {2^-k(2cq), 2^-k(2cq+1), 0, 0}
-// ============================================================================
-constexpr int FR_REC = 2176;
+// Record layout: ms_rec.cuh (FR_REC bytes per (64-block, 8-token tile), kb-major).
 constexpr int MS_PART_TILES = 1024;  // split-K partial tiles (N/128 x S) of one launch
 constexpr int MS_BPMAX = 32;         // tokens (4 tiles of 8)
 extern unsigned long long* g_mk_dbg;  // qgemv.cu: instrumentation buffer (ifx_set_mk_debug)
@@ -659,66 +654,13 @@ struct MsChainP {
   uint8_t* fout;        // records of the next phase's input (nullptr: none)
   float* ssq_out;       // [N/128][BP] (o, down, prep)
   int v_off, hd, per, lh;
+  int kv;          // qkv: attention over a KV cache follows (no v-broadcast records)
   float* part;     // split-K partial tiles [N/128][S][BP][128]
   uint32_t* cnt;   // per-tile arrival counters (zero-filled workspace, self-resetting)
   unsigned long long* dbg;  // instrumentation: %globaltimer stamps [16 launches][1024 CTAs][8] (nullable)
   int seq;
   int ko;  // experiments (IFB_MS_KO): 1 = no decode / MMA, 2 = no weight waits, 3 = no weight loads
 };
-
-// One item = (token tok, 16 values x[16c, 16c+16) of one 64-block); the four items of a
-// (token, block) sit in adjacent lanes c = lane & 3 (all 32 lanes call, `ok` masks).
-template <int NT>
-__device__ __forceinline__ void ms_put_item(uint8_t* rec, int tok, int c, const float (&x)[16], bool ok) {
-  float amax = 0.f, s = 0.f, so = 0.f;
-#pragma unroll
-  for (int i = 0; i < 16; i++) amax = fmaxf(amax, fabsf(x[i]));
-#pragma unroll
-  for (int i = 0; i < 8; i++) {
-    s += x[2 * i] + x[2 * i + 1];
-    so += x[2 * i + 1];
-  }
-  amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, 1));
-  amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, 2));
-  s += __shfl_xor_sync(0xffffffffu, s, 1);
-  s += __shfl_xor_sync(0xffffffffu, s, 2);
-  so += __shfl_xor_sync(0xffffffffu, so, 1);
-  so += __shfl_xor_sync(0xffffffffu, so, 2);
-  if (!ok) return;
-  const int k = xsplit_k(amax) - 4;  // |x| 2^k < 2^11: |x_e - 11 x_o| 2^k < 24576
-  const float sig = pow2f(k);
-  float fv[16];
-#pragma unroll
-  for (int m = 0; m < 4; m++) {
-    const int a = (m & 1) + 4 * (m >> 1), b = a + 2;
-    fv[4 * m + 0] = 0.25f * sig * x[2 * a + 1];
-    fv[4 * m + 1] = sig * x[2 * b + 1];
-    fv[4 * m + 2] = sig * fmaf(-11.f, x[2 * a + 1], x[2 * a]);
-    fv[4 * m + 3] = sig * fmaf(-11.f, x[2 * b + 1], x[2 * b]);
-  }
-  uint32_t fh[8], fl[8];
-#pragma unroll
-  for (int i = 0; i < 8; i++) {
-    const __half2 hh = __floats2half2_rn(fv[2 * i], fv[2 * i + 1]);
-    const float2 hf = __half22float2(hh);
-    fh[i] = h2_as_u32(hh);
-    fl[i] = pack_h2(fv[2 * i] - hf.x, fv[2 * i + 1] - hf.y);
-  }
-  const int fl_lane = 4 * (tok & 7) + c;
-  uint4* f = reinterpret_cast<uint4*>(rec) + fl_lane;
-  f[0] = make_uint4(fh[0], fh[1], fh[2], fh[3]);
-  f[32] = make_uint4(fh[4], fh[5], fh[6], fh[7]);
-  f[64] = make_uint4(fl[0], fl[1], fl[2], fl[3]);
-  f[96] = make_uint4(fl[4], fl[5], fl[6], fl[7]);
-  if (c == 0) {
-    float* sp = reinterpret_cast<float*>(rec + 2048) + 4 * ((tok >> 1) & 3);
-    const int e = tok & 1;
-    sp[e] = 5.f * so;
-    sp[2 + e] = s;
-    sp[16 + e] = pow2f(-k);
-    sp[18 + e] = 0.f;
-  }
-}
 
 // fragments of nblk consecutive 64-blocks (first global block blk0) of vals [BP][ld]
 // (column offset col0), written to the records of fout; dup/stride: extra copies
@@ -735,7 +677,7 @@ __device__ __forceinline__ void ms_emit_blocks(const float* vals, int ld, int co
 #pragma unroll
     for (int i = 0; i < 16; i++) x[i] = ok ? vals[tok * ld + col0 + 64 * blk + 16 * c + i] : 0.f;
     const int db = ok ? dst_blk[blk] : 0;
-    ms_put_item<NT>(fout + ((size_t)db * NT + (tok >> 3)) * FR_REC, tok, c, x, ok);
+    ms_put_item(fout + ((size_t)db * NT + (tok >> 3)) * FR_REC, tok, c, x, ok);
   }
 }
 
@@ -998,7 +940,7 @@ __global__ void __launch_bounds__(MS_THREADS, MsGeo<NT, V>::MINB) ms_chain_kerne
       // v rows -> the ctx blocks of every q head of the kv group (one rank: h0 = k0 = 0)
       int dst[2 * 8];
       int nd = 0, col[2 * 8];
-      for (int blk = 0; blk < 2; blk++) {
+      for (int blk = 0; blk < 2 && !P.kv; blk++) {
         const int rb = 2 * bx + blk;  // global 64-block of qkv rows
         if (rb * 64 < P.v_off || rb * 64 >= P.N) continue;
         const int jb = rb - P.v_off / 64, j = (jb * 64) / P.hd, eb = (jb * 64 - j * P.hd) / 64;
@@ -1113,7 +1055,8 @@ size_t ms_chain_ws_bytes(int64_t d, int64_t nq, int64_t lf) {
 // the decode stack of one rank (no tensor parallelism) through the fused chain;
 // IF_ERR_UNSUPPORTED when the shape or batch does not fit (caller falls back)
 if_status ms_chain_run(const MsChainLayer* layers, int nlayers, int64_t d, int64_t lh, int64_t lkv, int64_t hd,
-                       int64_t lf, int per, int64_t T, float* h, float* last_qkv, void* ws, cudaStream_t st) {
+                       int64_t lf, int per, int64_t T, float* h, float* last_qkv, void* ws, cudaStream_t st,
+                       MsAttnFn attn, void* actx, float* qkv_buf) {
   static const int off = getenv("IFB_NO_MSCHAIN") != nullptr;  // A/B experiments only
   const int64_t nq = lh * hd, nqkv = (lh + 2 * lkv) * hd;
   if (off || T < 2 || T > 16 || d % 128 || nqkv % 128 || (2 * lf) % 128 || hd % 64 || nq % 64 || per > 8 ||
@@ -1163,9 +1106,13 @@ if_status ms_chain_run(const MsChainLayer* layers, int nlayers, int64_t d, int64
       // qkv: rms(h) folded into the output; v rows -> ctx records
       q.part = part, q.cnt = cnt;
       q.W = layers[l].wqkv, q.N = (int)nqkv, q.K = (int)d, q.fin = rec_h, q.ssq_in = ssq, q.fout = rec_ctx;
-      q.qkv_out = lastl ? last_qkv : nullptr;
+      q.qkv_out = attn ? qkv_buf : (lastl ? last_qkv : nullptr);
+      q.kv = attn ? 1 : 0;
       q.v_off = (int)((lh + lkv) * hd), q.hd = (int)hd, q.per = per, q.lh = (int)lh;
       if ((r = ms_chain_launch<NTc, MSK_QKV, V>(q, st, sms))) break;
+      // KV decode (NEXT-1): RoPE + append + attention over the cache, whose merge writes
+      // the ctx records (attn.cu)
+      if (attn && (r = attn(actx, l, rec_ctx, NTc))) break;
       // o: h += W_o ctx; h records + sum h^2
       MsChainP o = {};
       o.part = part, o.cnt = cnt;

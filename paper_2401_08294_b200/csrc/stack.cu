@@ -392,7 +392,7 @@ static if_status run_stack(const if_stack_shape* shape, const if_plan* plan, int
   const int mk_tmax = tenv ? atoi(tenv) : (sc.type == IF_Q3H && sc.block == 64 ? 1 : 6);
   // with a KV cache (NEXT-1) the 3.5-bit engine runs in partial launches per token:
   // [qkv_0] attn_0 [o_0 gu_0 down_0 qkv_1] attn_1 ... [o_L-1 gu down] (one rank)
-  const bool mk_kv = kvr && T <= 2 && sc.type == IF_Q3H && sc.block == 64 && groups == 1 && !getenv("IFB_NO_MK_KV");
+  const bool mk_kv = kvr && T <= (getenv("IFB_NO_MSCHAIN_KV") ? 2 : 1) && sc.type == IF_Q3H && sc.block == 64 && groups == 1 && !getenv("IFB_NO_MK_KV");
   const bool mk = mode == IF_DECODE && T <= mk_tmax && !(sc.type == IF_Q3H && sc.block == 32) && tp_ok &&
                   nlayers <= MK_MAXL && nlayers > 0 && (!kvr || mk_kv);
   if (mk) {
@@ -480,14 +480,41 @@ static if_status run_stack(const if_stack_shape* shape, const if_plan* plan, int
   }
   // batched 3.5-bit decode (T <= 16, one TP rank): the fused chain, 4 launches per layer
   // with the glue in the GEMV epilogues (qgemv_ms.cu)
-  if (mode == IF_DECODE && T >= 2 && !kvr && groups == 1 && sc.type == IF_Q3H && sc.block == 64 && nlayers > 0) {
+  if (mode == IF_DECODE && T >= 2 && groups == 1 && sc.type == IF_Q3H && sc.block == 64 && nlayers > 0 &&
+      (!kvr || !getenv("IFB_NO_MSCHAIN_KV"))) {
     std::vector<MsChainLayer> ml((size_t)nlayers);
     for (int l = 0; l < nlayers; l++) {
       const if_layer_weights& Wl = stage_layers[l];
       if (!Wl.wqkv || !Wl.wo || !Wl.wgu || !Wl.wdown) return set_error(IF_ERR_ARG, "if_run_stack: null weights, layer %d", l);
       ml[(size_t)l] = {Wl.wqkv, Wl.wo, Wl.wgu, Wl.wdown};
     }
-    st = ms_chain_run(ml.data(), nlayers, L.d, L.lh, L.lkv, L.hd, L.lf, per, T, h_out, last_qkv, w.msrec, cs);
+    // with a KV cache: attention between each layer's qkv and o kernels; its merge
+    // writes the ctx records; q, k are returned after RoPE (copied after the last layer)
+    struct KvChain {
+      const Local* L;
+      const KvRun* kvr;
+      const WS* w;
+      int64_t T;
+      int nlayers;
+      float* last_qkv;
+      cudaStream_t cs;
+    } kc = {&L, kvr, &w, T, nlayers, last_qkv, cs};
+    MsAttnFn fn = nullptr;
+    if (kvr)
+      fn = [](void* p, int l, uint8_t* rec, int nt) -> if_status {
+        const KvChain& k = *static_cast<const KvChain*>(p);
+        AttnArgs aa = attn_args(*k.L, k.kvr, *k.w, k.T, k.nlayers, l);
+        aa.ctx = k.w->ctx;
+        aa.rec = rec;
+        aa.rec_nt = nt;
+        aa.pdl = true;
+        if_status r = attn_run(aa, k.cs);
+        if (!r && l == k.nlayers - 1 && k.last_qkv &&
+            cudaMemcpyAsync(k.last_qkv, k.w->qkv, (size_t)k.T * k.L->nqkv * 4, cudaMemcpyDeviceToDevice, k.cs) != cudaSuccess)
+          r = check_launch("if_run_stack: last_qkv");
+        return r;
+      };
+    st = ms_chain_run(ml.data(), nlayers, L.d, L.lh, L.lkv, L.hd, L.lf, per, T, h_out, last_qkv, w.msrec, cs, fn, &kc, w.qkv);
     if (st != IF_ERR_UNSUPPORTED) {
       if (st) return st;
       if (!last) {
