@@ -707,9 +707,8 @@ __device__ __forceinline__ void ms_rms(const MsChainP& P, float* sinv) {
 // o / down / prep: vals [BP][128] = this tile's new h rows (residual already added by
 // the caller or loaded), per-token sum of squares -> ssq_out, fragments -> fout
 template <int NT>
-__device__ __forceinline__ void ms_emit_h(const MsChainP& P, float* vals, float* red, bool add) {
+__device__ __forceinline__ void ms_emit_h(const MsChainP& P, int bx, float* vals, float* red, bool add) {
   constexpr int BP = 8 * NT;
-  const int bx = blockIdx.x;
   const int warp = threadIdx.x >> 5;
 #pragma unroll
   for (int it = 0; it < BP / 2; it++) {
@@ -735,6 +734,115 @@ __device__ __forceinline__ void ms_emit_h(const MsChainP& P, float* vals, float*
   if (P.fout) {
     const int dst[2] = {2 * bx, 2 * bx + 1};
     ms_emit_blocks<NT>(vals, 128, 0, 2, P.fout, dst);
+  }
+}
+
+// ---- the chain's per-block decode + MMA, shared by the per-phase kernels and the engine ----
+struct MsLane {
+  int g, c, wb, wb2;
+  uint32_t s0, s1, s2, s3, magic, k11;
+};
+__device__ __forceinline__ MsLane ms_lane(int lane, uint32_t zero) {
+  MsLane L;
+  L.g = lane >> 2, L.c = lane & 3;
+  L.magic = 0x64006400u | zero, L.k11 = 0x2DD125D1u | zero;  // registers (see ms2_view)
+  L.wb = 2 * L.c, L.wb2 = L.wb + 2 < 8 ? L.wb + 2 : 7;
+  L.s0 = 30u - 8u * L.c, L.s1 = L.s0 + 7u, L.s2 = 26u - 8u * L.c, L.s3 = L.s2 + 7u;
+  return L;
+}
+struct MsBlk {
+  uint32_t Ca[4], Ua[4], Cb[4], Ub[4];
+  u64 lo0, d0, lo1, d1;
+};
+// rows g and g + 8 of one 64-block slot [16 rows][8 words] -> A fragments + Eq. 2 scales
+__device__ __forceinline__ void ms_decode(const uint32_t* slot, const MsLane& L, MsBlk& b) {
+  const uint32_t* wb0 = slot + L.g * 8;
+  const uint32_t* wb1 = wb0 + 64;
+  const uint2 p0 = *reinterpret_cast<const uint2*>(wb0 + L.wb), p1 = *reinterpret_cast<const uint2*>(wb1 + L.wb);
+  const uint32_t q0 = wb0[L.wb2], q1 = wb1[L.wb2], h0 = wb0[0], h1 = wb1[0];
+  ms2_view(shr64_lo(p0.x, p0.y, L.s0), L.magic, L.k11, b.Ca[0], b.Ua[0]);
+  ms2_view(shr64_lo(p0.x, p0.y, L.s1), L.magic, L.k11, b.Ca[1], b.Ua[1]);
+  ms2_view(shr64_lo(p0.y, q0, L.s2), L.magic, L.k11, b.Ca[2], b.Ua[2]);
+  ms2_view(shr64_lo(p0.y, q0, L.s3), L.magic, L.k11, b.Ca[3], b.Ua[3]);
+  ms2_view(shr64_lo(p1.x, p1.y, L.s0), L.magic, L.k11, b.Cb[0], b.Ub[0]);
+  ms2_view(shr64_lo(p1.x, p1.y, L.s1), L.magic, L.k11, b.Cb[1], b.Ub[1]);
+  ms2_view(shr64_lo(p1.y, q1, L.s2), L.magic, L.k11, b.Cb[2], b.Ub[2]);
+  ms2_view(shr64_lo(p1.y, q1, L.s3), L.magic, L.k11, b.Cb[3], b.Ub[3]);
+  const float2 f0 = __half22float2(*reinterpret_cast<const __half2*>(&h0));
+  const float2 f1 = __half22float2(*reinterpret_cast<const __half2*>(&h1));
+  b.lo0 = pack2(f0.x, f0.x), b.d0 = pack2(f0.y - f0.x, f0.y - f0.x);
+  b.lo1 = pack2(f1.x, f1.x), b.d1 = pack2(f1.y - f1.x, f1.y - f1.x);
+}
+// one block's MMAs against token tile t's record; accumulates Eq. 2 into ya / yb
+__device__ __forceinline__ void ms_mma(const unsigned char* rec, int lane, int c, const MsBlk& b, u64 (&ya)[2],
+                                       u64 (&yb)[2]) {
+  const uint4* fx = reinterpret_cast<const uint4*>(rec) + lane;
+  const uint4 h0 = fx[0], h1 = fx[32], l0 = fx[64], l1 = fx[96];
+  const float4 sm = reinterpret_cast<const float4*>(rec + 2048)[c];
+  const float4 iv = reinterpret_cast<const float4*>(rec + 2112)[c];
+  float Dh[4] = {0.f, 0.f, 0.f, 0.f}, Dl[4] = {0.f, 0.f, 0.f, 0.f};
+  mma16816(Dh, b.Ca[0], b.Cb[0], b.Ua[0], b.Ub[0], h0.x, h0.y);
+  mma16816(Dl, b.Ca[0], b.Cb[0], b.Ua[0], b.Ub[0], l0.x, l0.y);
+  mma16816(Dh, b.Ca[1], b.Cb[1], b.Ua[1], b.Ub[1], h0.z, h0.w);
+  mma16816(Dl, b.Ca[1], b.Cb[1], b.Ua[1], b.Ub[1], l0.z, l0.w);
+  mma16816(Dh, b.Ca[2], b.Cb[2], b.Ua[2], b.Ub[2], h1.x, h1.y);
+  mma16816(Dl, b.Ca[2], b.Cb[2], b.Ua[2], b.Ub[2], l1.x, l1.y);
+  mma16816(Dh, b.Ca[3], b.Cb[3], b.Ua[3], b.Ub[3], h1.z, h1.w);
+  mma16816(Dl, b.Ca[3], b.Cb[3], b.Ua[3], b.Ub[3], l1.z, l1.w);
+  // D 2^-k + 5 So = sum q x (per token); then Eq. 2: (hi - lo) (.)/10 + lo S
+  const u64 so5 = pack2(sm.x, sm.y), s2v = pack2(sm.z, sm.w), inv = pack2(iv.x, iv.y);
+  const u64 D01 = fadd2(pack2(Dh[0], Dh[1]), pack2(Dl[0], Dl[1]));
+  const u64 D23 = fadd2(pack2(Dh[2], Dh[3]), pack2(Dl[2], Dl[3]));
+  ya[0] = ffma2(b.d0, ffma2(D01, inv, so5), ya[0]);
+  ya[1] = ffma2(b.d1, ffma2(D23, inv, so5), ya[1]);
+  yb[0] = ffma2(b.lo0, s2v, yb[0]);
+  yb[1] = ffma2(b.lo1, s2v, yb[1]);
+}
+
+// the split-K owner's epilogue of tile bx: stack glue + the next phase's records
+template <int NT, int KIND>
+__device__ __forceinline__ void ms_owner_epilogue(const MsChainP& P, int bx, float* vals, float* acts, float* red,
+                                                  const float* sinv) {
+  constexpr int BP = 8 * NT;
+  if constexpr (KIND == MSK_O || KIND == MSK_DOWN) {
+    ms_emit_h<NT>(P, bx, vals, red, true);
+  } else if constexpr (KIND == MSK_QKV) {
+#pragma unroll
+    for (int it = 0; it < BP / 2; it++) {
+      const int i = threadIdx.x + it * MS_THREADS, tok = i >> 7, r = i & 127, row = 128 * bx + r;
+      const float v = tok < P.B ? vals[i] * sinv[tok] : 0.f;
+      vals[i] = v;
+      if (P.qkv_out && tok < P.B) P.qkv_out[(int64_t)tok * P.N + row] = v;
+    }
+    __syncthreads();
+    // v rows -> the ctx blocks of every q head of the kv group (one rank: h0 = k0 = 0)
+    int dst[2 * 8];
+    int nd = 0, col[2 * 8];
+    for (int blk = 0; blk < 2 && !P.kv; blk++) {
+      const int rb = 2 * bx + blk;  // global 64-block of qkv rows
+      if (rb * 64 < P.v_off || rb * 64 >= P.N) continue;
+      const int jb = rb - P.v_off / 64, j = (jb * 64) / P.hd, eb = (jb * 64 - j * P.hd) / 64;
+      for (int i = j * P.per; i < (j + 1) * P.per && i < P.lh && nd < 16; i++) {
+        dst[nd] = (i * P.hd) / 64 + eb;
+        col[nd] = 64 * blk;
+        nd++;
+      }
+    }
+    for (int q = 0; q < nd; q++) ms_emit_blocks<NT>(vals, 128, col[q], 1, P.fout, &dst[q]);
+  } else {  // MSK_GU: act f = silu(s g) (s u), gate/up rows interleaved (2f, 2f+1)
+#pragma unroll
+    for (int it = 0; it < BP / 4; it++) {
+      const int i = threadIdx.x + it * MS_THREADS, tok = i >> 6, f = i & 63;
+      float a = 0.f;
+      if (tok < P.B) {
+        const float gg = vals[tok * 128 + 2 * f] * sinv[tok], u = vals[tok * 128 + 2 * f + 1] * sinv[tok];
+        a = gg / (1.0f + expf(-gg)) * u;
+      }
+      acts[tok * 64 + f] = a;
+    }
+    __syncthreads();
+    const int dst[1] = {bx};
+    ms_emit_blocks<NT>(acts, 64, 0, 1, P.fout, dst);
   }
 }
 
@@ -765,7 +873,7 @@ __global__ void __launch_bounds__(MS_THREADS, MsGeo<NT, V>::MINB) ms_chain_kerne
     // stage input: sum-h^2 partials and fragments of h (one 128-row tile per CTA)
     pdl_trigger();
     pdl_wait();
-    ms_emit_h<NT>(P, vals, red, false);
+    ms_emit_h<NT>(P, blockIdx.x, vals, red, false);
     return;
   } else {
     const int nb = P.K >> 6;
@@ -803,58 +911,10 @@ __global__ void __launch_bounds__(MS_THREADS, MsGeo<NT, V>::MINB) ms_chain_kerne
     mbar_wait(xbar, 0);
     if (dbg) dbg[2] = ms_gtimer();
     const int g = lane >> 2, c = lane & 3;
-    const uint32_t magic = 0x64006400u | zero, k11 = 0x2DD125D1u | zero;
-    const int wb = 2 * c, wb2 = wb + 2 < 8 ? wb + 2 : 7;
-    const uint32_t s0 = 30u - 8u * c, s1 = s0 + 7u, s2 = 26u - 8u * c, s3 = s2 + 7u;
     u64 ya[NT][2], yb[NT][2];
 #pragma unroll
     for (int t = 0; t < NT; t++) ya[t][0] = ya[t][1] = yb[t][0] = yb[t][1] = 0ull;
-    // two blocks per iteration (independent decode + MMA chains: the warp is latency-
-    // bound, 16 warps per SM), hi and lo fragments in separate accumulators
-    auto decode = [&](int sl, uint32_t (&Ca)[4], uint32_t (&Ua)[4], uint32_t (&Cb)[4], uint32_t (&Ub)[4], u64& lo0,
-                      u64& d0, u64& lo1, u64& d1) {
-      const uint32_t* wb0 = ring + sl * 128 + g * 8;
-      const uint32_t* wb1 = wb0 + 64;
-      const uint2 p0 = *reinterpret_cast<const uint2*>(wb0 + wb), p1 = *reinterpret_cast<const uint2*>(wb1 + wb);
-      const uint32_t q0 = wb0[wb2], q1 = wb1[wb2], h0 = wb0[0], h1 = wb1[0];
-      ms2_view(shr64_lo(p0.x, p0.y, s0), magic, k11, Ca[0], Ua[0]);
-      ms2_view(shr64_lo(p0.x, p0.y, s1), magic, k11, Ca[1], Ua[1]);
-      ms2_view(shr64_lo(p0.y, q0, s2), magic, k11, Ca[2], Ua[2]);
-      ms2_view(shr64_lo(p0.y, q0, s3), magic, k11, Ca[3], Ua[3]);
-      ms2_view(shr64_lo(p1.x, p1.y, s0), magic, k11, Cb[0], Ub[0]);
-      ms2_view(shr64_lo(p1.x, p1.y, s1), magic, k11, Cb[1], Ub[1]);
-      ms2_view(shr64_lo(p1.y, q1, s2), magic, k11, Cb[2], Ub[2]);
-      ms2_view(shr64_lo(p1.y, q1, s3), magic, k11, Cb[3], Ub[3]);
-      const float2 f0 = __half22float2(*reinterpret_cast<const __half2*>(&h0));
-      const float2 f1 = __half22float2(*reinterpret_cast<const __half2*>(&h1));
-      lo0 = pack2(f0.x, f0.x), d0 = pack2(f0.y - f0.x, f0.y - f0.x);
-      lo1 = pack2(f1.x, f1.x), d1 = pack2(f1.y - f1.x, f1.y - f1.x);
-    };
-    auto mma_block = [&](int kb, int t, const uint32_t (&Ca)[4], const uint32_t (&Ua)[4], const uint32_t (&Cb)[4],
-                         const uint32_t (&Ub)[4], u64 lo0, u64 d0, u64 lo1, u64 d1) {
-      const unsigned char* rec = xr + (size_t)(kb * NT + t) * FR_REC;
-      const uint4* fx = reinterpret_cast<const uint4*>(rec) + lane;
-      const uint4 h0 = fx[0], h1 = fx[32], l0 = fx[64], l1 = fx[96];
-      const float4 sm = reinterpret_cast<const float4*>(rec + 2048)[c];
-      const float4 iv = reinterpret_cast<const float4*>(rec + 2112)[c];
-      float Dh[4] = {0.f, 0.f, 0.f, 0.f}, Dl[4] = {0.f, 0.f, 0.f, 0.f};
-      mma16816(Dh, Ca[0], Cb[0], Ua[0], Ub[0], h0.x, h0.y);
-      mma16816(Dl, Ca[0], Cb[0], Ua[0], Ub[0], l0.x, l0.y);
-      mma16816(Dh, Ca[1], Cb[1], Ua[1], Ub[1], h0.z, h0.w);
-      mma16816(Dl, Ca[1], Cb[1], Ua[1], Ub[1], l0.z, l0.w);
-      mma16816(Dh, Ca[2], Cb[2], Ua[2], Ub[2], h1.x, h1.y);
-      mma16816(Dl, Ca[2], Cb[2], Ua[2], Ub[2], l1.x, l1.y);
-      mma16816(Dh, Ca[3], Cb[3], Ua[3], Ub[3], h1.z, h1.w);
-      mma16816(Dl, Ca[3], Cb[3], Ua[3], Ub[3], l1.z, l1.w);
-      // D 2^-k + 5 So = sum q x (per token); then Eq. 2: (hi - lo) (.)/10 + lo S
-      const u64 so5 = pack2(sm.x, sm.y), s2v = pack2(sm.z, sm.w), inv = pack2(iv.x, iv.y);
-      const u64 D01 = fadd2(pack2(Dh[0], Dh[1]), pack2(Dl[0], Dl[1]));
-      const u64 D23 = fadd2(pack2(Dh[2], Dh[3]), pack2(Dl[2], Dl[3]));
-      ya[t][0] = ffma2(d0, ffma2(D01, inv, so5), ya[t][0]);
-      ya[t][1] = ffma2(d1, ffma2(D23, inv, so5), ya[t][1]);
-      yb[t][0] = ffma2(lo0, s2v, yb[t][0]);
-      yb[t][1] = ffma2(lo1, s2v, yb[t][1]);
-    };
+    const MsLane ML = ms_lane(lane, zero);
     auto refill = [&](int sl, int kb_next) {
       if (kb_next < nkb && P.ko != 3)
         asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(ring_s + sl * 512),
@@ -871,14 +931,13 @@ __global__ void __launch_bounds__(MS_THREADS, MsGeo<NT, V>::MINB) ms_chain_kerne
         slot = slot + 1 == DEPTH ? 0 : slot + 1;
         continue;
       }
-      uint32_t Ca[4], Ua[4], Cb[4], Ub[4];
-      u64 lo0, d0, lo1, d1;
-      decode(slot, Ca, Ua, Cb, Ub, lo0, d0, lo1, d1);
+      MsBlk bk;
+      ms_decode(ring + slot * 128, ML, bk);
       __syncwarp();  // the slot is read: refill it with block kb + DEPTH
       refill(slot, kb + DEPTH);
       slot = slot + 1 == DEPTH ? 0 : slot + 1;
 #pragma unroll
-      for (int t = 0; t < NT; t++) mma_block(kb, t, Ca, Ua, Cb, Ub, lo0, d0, lo1, d1);
+      for (int t = 0; t < NT; t++) ms_mma(xr + (size_t)(kb * NT + t) * FR_REC, lane, ML.c, bk, ya[t], yb[t]);
     }
     asm volatile("cp.async.wait_group 0;" ::: "memory");
     if (dbg) dbg[3] = ms_gtimer();
@@ -925,47 +984,7 @@ __global__ void __launch_bounds__(MS_THREADS, MsGeo<NT, V>::MINB) ms_chain_kerne
       if (dbg) dbg[4] = ms_gtimer();
     }
     // ---- the owner's epilogue: stack glue + the next phase's records ----
-    const int bx = blockIdx.x;
-    if constexpr (KIND == MSK_O || KIND == MSK_DOWN) {
-      ms_emit_h<NT>(P, vals, red, true);
-    } else if constexpr (KIND == MSK_QKV) {
-#pragma unroll
-      for (int it = 0; it < BP / 2; it++) {
-        const int i = threadIdx.x + it * MS_THREADS, tok = i >> 7, r = i & 127, row = 128 * bx + r;
-        const float v = tok < P.B ? vals[i] * sinv[tok] : 0.f;
-        vals[i] = v;
-        if (P.qkv_out && tok < P.B) P.qkv_out[(int64_t)tok * P.N + row] = v;
-      }
-      __syncthreads();
-      // v rows -> the ctx blocks of every q head of the kv group (one rank: h0 = k0 = 0)
-      int dst[2 * 8];
-      int nd = 0, col[2 * 8];
-      for (int blk = 0; blk < 2 && !P.kv; blk++) {
-        const int rb = 2 * bx + blk;  // global 64-block of qkv rows
-        if (rb * 64 < P.v_off || rb * 64 >= P.N) continue;
-        const int jb = rb - P.v_off / 64, j = (jb * 64) / P.hd, eb = (jb * 64 - j * P.hd) / 64;
-        for (int i = j * P.per; i < (j + 1) * P.per && i < P.lh && nd < 16; i++) {
-          dst[nd] = (i * P.hd) / 64 + eb;
-          col[nd] = 64 * blk;
-          nd++;
-        }
-      }
-      for (int q = 0; q < nd; q++) ms_emit_blocks<NT>(vals, 128, col[q], 1, P.fout, &dst[q]);
-    } else {  // MSK_GU: act f = silu(s g) (s u), gate/up rows interleaved (2f, 2f+1)
-#pragma unroll
-      for (int it = 0; it < BP / 4; it++) {
-        const int i = threadIdx.x + it * MS_THREADS, tok = i >> 6, f = i & 63;
-        float a = 0.f;
-        if (tok < P.B) {
-          const float gg = vals[tok * 128 + 2 * f] * sinv[tok], u = vals[tok * 128 + 2 * f + 1] * sinv[tok];
-          a = gg / (1.0f + expf(-gg)) * u;
-        }
-        acts[tok * 64 + f] = a;
-      }
-      __syncthreads();
-      const int dst[1] = {bx};
-      ms_emit_blocks<NT>(acts, 64, 0, 1, P.fout, dst);
-    }
+    ms_owner_epilogue<NT, KIND>(P, blockIdx.x, vals, acts, red, sinv);
     if (dbg) dbg[5] = ms_gtimer();
   }
 }
@@ -1047,6 +1066,7 @@ static if_status ms_chain_launch(MsChainP P, cudaStream_t st, int sms) {
 }
 
 // bytes of the chain's record buffers (h, ctx, act) + sum-h^2 partials for NT = 2
+
 size_t ms_chain_ws_bytes(int64_t d, int64_t nq, int64_t lf) {
   return (size_t)((d + nq + lf) / 64) * 4 * FR_REC + (size_t)(d / 128) * MS_BPMAX * 4 + 256 +
          (size_t)MS_PART_TILES * MS_BPMAX * 128 * 4 + (size_t)MS_PART_TILES * 4;
