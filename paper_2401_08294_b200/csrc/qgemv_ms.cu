@@ -242,6 +242,7 @@ __global__ void __launch_bounds__(MS_THREADS, IFB_MS_MINB) qgemv_ms_kernel(const
 // permuted into the fragment order, with the block sums S = sum x and 5 sum x_o.
 // ============================================================================
 constexpr int M2_MAXS = 8;  // split-K CTAs per cluster (portable cluster size)
+constexpr int MS_MAXS = 16;  // chain: split-K CTAs per tile (last-CTA reduction, no cluster)
 __device__ __forceinline__ uint32_t hfma2_u(uint32_t a, uint32_t b, uint32_t c) {
   uint32_t d;
   asm("fma.rn.f16x2 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
@@ -969,12 +970,12 @@ __global__ void __launch_bounds__(MS_THREADS, MsGeo<NT, V>::MINB) ms_chain_kerne
       if (red[0] == 0.f) return;
       const float* all = P.part + (size_t)blockIdx.x * S * (BP * 128);
       for (int i = threadIdx.x; i < BP * 128; i += MS_THREADS) {
-        float pv[M2_MAXS];
+        float pv[MS_MAXS];
 #pragma unroll
-        for (int q = 0; q < M2_MAXS; q++) pv[q] = q < S ? __ldcg(all + (size_t)q * (BP * 128) + i) : 0.f;
+        for (int q = 0; q < MS_MAXS; q++) pv[q] = q < S ? __ldcg(all + (size_t)q * (BP * 128) + i) : 0.f;
         float v = pv[0];
 #pragma unroll
-        for (int q = 1; q < M2_MAXS; q++) v += pv[q];
+        for (int q = 1; q < MS_MAXS; q++) v += pv[q];
         vals[i] = v;
       }
       __syncthreads();
@@ -1000,7 +1001,7 @@ static bool ms_geo(int N, int K, int sms, int* splits_out, int* kper_out) {
   // cost model (per-warp latency-bound CTAs): waves x (blocks per CTA + fixed cost
   // of ~6 blocks for prologue / epilogue + 1 per cluster rank in the reduction)
   int best = -1, best_cost = 0;
-  for (int sp = 1; sp <= std::min(M2_MAXS, nb); sp++) {
+  for (int sp = 1; sp <= std::min(MS_MAXS, nb); sp++) {
     const int kper = (nb + sp - 1) / sp;
     if (kper > kmax1 || Gm::BP * 192 * 4 > Gm::RING + kper * Gm::REC || nrt * sp > MS_PART_TILES) continue;
     const int per_sm = kper <= kmax2 ? Gm::MINB : 1;
@@ -1042,7 +1043,7 @@ static if_status ms_chain_launch(MsChainP P, cudaStream_t st, int sms) {
       int v[4] = {0, 0, 0, 0};
       sscanf(so, "%d,%d,%d,%d", &v[0], &v[1], &v[2], &v[3]);
       const int nb = P.K / 64, want = v[KIND & 3];
-      if (want > 0 && want <= M2_MAXS && (nb + want - 1) / want <= kper * 4) {
+      if (want > 0 && want <= MS_MAXS && (nb + want - 1) / want <= kper * 4) {
         kper = (nb + want - 1) / want;
         splits = (nb + kper - 1) / kper;
       }
