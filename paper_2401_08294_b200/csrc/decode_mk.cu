@@ -609,6 +609,7 @@ __global__ void __launch_bounds__(MK_THREADS, 1) decode_mk_kernel(const __grid_c
     }(std::make_integer_sequence<int, BS>{});
   }
   __syncthreads();
+  if constexpr (PL) pdl_trigger();
   const bool stack = P.mode == MK_MODE_STACK;
   const int nphase = stack ? 4 * P.layers : 1;
   const int pb = PL ? P.p_begin : 0, pe = PL ? P.p_end : nphase;  // this launch's phases
@@ -660,6 +661,7 @@ __global__ void __launch_bounds__(MK_THREADS, 1) decode_mk_kernel(const __grid_c
   }
 
   // ============================ consumers ============================
+  if constexpr (PL) pdl_wait();  // the predecessor (attention) wrote this launch's inputs
   const int ct = threadIdx.x - 32;
   const int cw = warp - 1;
   const Q3HConst kc = q3h_const();
@@ -1539,12 +1541,30 @@ if_status mk_launch(MkParams& P, cudaStream_t st) {
   cfg.blockDim = dim3(MK_THREADS);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeCooperative;  // grid-wide phase dependencies need co-residency
-  attr[0].val.cooperative = 1;
+  cudaLaunchAttribute attr[2];
+  int na = 0;
+  if (!(P.mode == MK_MODE_GEMV || getenv("IFB_MK_NOCOOP"))) {
+    attr[na].id = cudaLaunchAttributeCooperative;  // grid-wide phase dependencies need co-residency
+    attr[na].val.cooperative = 1;
+    na++;
+  }
+  // partial launches (KV decode) follow an attention kernel: programmatic dependent
+  // launch lets the producer warp start the weight stream before that kernel completes
+  // (consumers wait with griddepcontrol.wait before their first activation read)
+  static const int no_pdl = getenv("IFB_MK_NOPDL") != nullptr;  // A/B experiments only
+  if (P.part && !no_pdl) {
+    attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[na].val.programmaticStreamSerializationAllowed = 1;
+    na++;
+  }
   cfg.attrs = attr;
-  cfg.numAttrs = (P.mode == MK_MODE_GEMV || getenv("IFB_MK_NOCOOP")) ? 0 : 1;
+  cfg.numAttrs = na;
   cudaError_t e = cudaLaunchKernelEx(&cfg, kern, P);
+  if (e != cudaSuccess && P.part && !no_pdl) {  // a driver that refuses cooperative + PDL: plain launch
+    (void)cudaGetLastError();
+    cfg.numAttrs = na - 1;
+    e = cudaLaunchKernelEx(&cfg, kern, P);
+  }
   count_launch();
   if (e != cudaSuccess) return set_error(IF_ERR_CUDA, "decode_mk: %s", cudaGetErrorString(e));
   return check_launch("decode_mk");
