@@ -711,7 +711,7 @@ __global__ void __launch_bounds__(MK_THREADS, 1) decode_mk_kernel(const __grid_c
 #ifndef IFB_MK_POLL
       if (ct == 0) {
         SpinGuard sg;
-        const uint32_t target = (ep + 1u) * (uint32_t)G;
+        const uint32_t target = (ep + 1u) * (uint32_t)G - (uint32_t)P.early;
         // wrap-safe: the difference is taken in uint32_t (defined modulo 2^32), then read as signed
         while ((int32_t)(ld_relaxed_u32(reinterpret_cast<const uint32_t*>(P.done + p - 1)) - target) < 0) {
           __nanosleep(20);
@@ -1049,7 +1049,7 @@ __global__ void __launch_bounds__(MK_THREADS, 1) decode_mk_kernel(const __grid_c
 #ifndef IFB_MK_POLL
       if (ct == 0) {
         SpinGuard sg;
-        const uint32_t target = (ep + 1u) * (uint32_t)G;
+        const uint32_t target = (ep + 1u) * (uint32_t)G - (uint32_t)P.early;
         // wrap-safe: the difference is taken in uint32_t (defined modulo 2^32), then read as signed
         while ((int32_t)(ld_relaxed_u32(reinterpret_cast<const uint32_t*>(P.done + p - 1)) - target) < 0) {
           __nanosleep(20);
@@ -1552,6 +1552,10 @@ if_status mk_launch(MkParams& P, cudaStream_t st) {
   // launch lets the producer warp start the weight stream before that kernel completes
   // (consumers wait with griddepcontrol.wait before their first activation read)
   static const int no_pdl = getenv("IFB_MK_NOPDL") != nullptr;  // A/B experiments only
+  // measured (7B B = 1, 200 steps): all CTAs 897 tok/s, all but 4 905, 8 908, 16 911, 24 911,
+  // 48 832 (the late words' re-reads congest L2)
+  static const char* early_env = getenv("IFB_MK_EARLY");  // A/B experiments only
+  P.early = std::max(0, std::min(early_env ? atoi(early_env) : 16, (int)G / 8));
   if (P.part && !no_pdl) {
     attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[na].val.programmaticStreamSerializationAllowed = 1;

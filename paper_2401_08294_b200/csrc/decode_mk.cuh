@@ -52,6 +52,10 @@ struct MkParams {
   const float* x_first;
   float* qkv_out;
   int seg_nb;  // K-segment length in 64-blocks (multiple of 32); 0 = whole rows
+  // readers start staging a phase input once all but `early` CTAs signalled the previous
+  // phase (the parity tags catch the late words; no writer can be a version ahead, see
+  // decode_mk.cu); 0 = wait for every CTA
+  int early;
   unsigned long long* dbg;  // nullable: per-CTA %globaltimer stamps [G][nphase][8] (instrumentation)
   const uint8_t* w[MK_MAXL][4];  // qkv, o, gu (gate/up rows interleaved), down per layer
 };

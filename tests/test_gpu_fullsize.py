@@ -103,8 +103,11 @@ def _host_layer_rows_check(cfg, stk, rows_per=3):
 
 @pytest.mark.slow
 @pytest.mark.parametrize("model", ["13b", "70b"])
-@pytest.mark.parametrize("T", [1, 16])
+@pytest.mark.parametrize("T", [1, 8, 16])
 def test_stack_full_width_two_layers(model, T):
+    """13B/70B widths: T = 1 the persistent engine; T = 8 the fused batched chain (70B's
+    down projection, K = 28672, in 16 split-K CTAs per tile); T = 16 the chain (13B) or
+    the per-layer path (70B: its records do not fit)."""
     d = dev()
     cfg = dict(synth.LLAMA[model], layers=2)
     s = F.scheme(35, 64)
