@@ -711,14 +711,21 @@ template <int NT>
 __device__ __forceinline__ void ms_emit_h(const MsChainP& P, int bx, float* vals, float* red, bool add) {
   constexpr int BP = 8 * NT;
   const int warp = threadIdx.x >> 5;
+  // every h load in flight before the first store (the stores would otherwise order
+  // each following load behind them: one L2 latency per token pair)
+  float hold[BP / 2];
+#pragma unroll
+  for (int it = 0; it < BP / 2; it++) {
+    const int i = threadIdx.x + it * MS_THREADS, tok = i >> 7, r = i & 127;
+    hold[it] = tok < P.B ? __ldcg(P.h + (int64_t)tok * P.d + 128 * bx + r) : 0.f;
+  }
 #pragma unroll
   for (int it = 0; it < BP / 2; it++) {
     const int i = threadIdx.x + it * MS_THREADS, tok = i >> 7, r = i & 127, row = 128 * bx + r;
     float hn = 0.f;
     if (tok < P.B) {
-      float* hp = P.h + (int64_t)tok * P.d + row;
-      hn = add ? *hp + vals[i] : *hp;
-      if (add) *hp = hn;
+      hn = add ? hold[it] + vals[i] : hold[it];
+      if (add) P.h[(int64_t)tok * P.d + row] = hn;
     }
     vals[i] = hn;
     float q = hn * hn;
