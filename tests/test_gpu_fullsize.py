@@ -130,3 +130,35 @@ def test_stack_full_width_two_layers(model, T):
                                     [deinterleave_rows(l[2], 2 * cfg["ffn"]) for l in host], [l[3] for l in host], h)
     assert normwise(out.cpu().numpy(), ho) <= 1e-3
     assert normwise(qkv.cpu().numpy(), qo) <= 1e-3
+
+
+@pytest.mark.slow
+def test_stack_7b_width_chain_four_layers():
+    """The fused batched chain at 7B width (T = 8, 4 layers): one fp16 per x element with a
+    power-of-two scale per (token, 64-block) (DESIGN.md Q30) compounds over the layers;
+    still within the 1e-3 decode gate against the fp64 oracle."""
+    d = dev()
+    cfg = dict(synth.LLAMA["7b"], layers=4)
+    s = F.scheme(35, 64)
+    shape = F.stack_shape(*[cfg[k] for k in ("layers", "hidden", "heads", "kv_heads", "head_dim", "ffn")], s)
+    plan = F.if_plan_partition(F.IF_BY_LAYER, shape, 1)
+    stk = Stack(cfg, s, plan, 0, d)
+    T = 8
+    h = synth.activations(T, cfg["hidden"], tid=5)
+    hd_ = torch.from_numpy(h).to(d)
+    out = torch.empty_like(hd_)
+    nqkv = (cfg["heads"] + 2 * cfg["kv_heads"]) * cfg["head_dim"]
+    qkv = torch.empty(T, nqkv, device=d)
+    ws = torch.zeros(F.if_stack_workspace_bytes(shape, plan, 0, T, F.IF_DECODE), dtype=torch.uint8, device=d)
+    F.if_launch_count(True)
+    F.if_run_stack(shape, plan, 0, None, stk.arr, hd_, T, F.IF_DECODE, out, qkv, ws)
+    torch.cuda.synchronize()
+    assert F.if_launch_count() == 1 + 4 * cfg["layers"]
+    host = [[t.cpu().numpy() for t in layer] for layer in stk.layers]
+    del stk
+    ho, qo = oracle_stack_per_token(dict(cfg, qtype=35, block=64), [l[0] for l in host], [l[1] for l in host],
+                                    [deinterleave_rows(l[2], 2 * cfg["ffn"]) for l in host], [l[3] for l in host], h)
+    err = normwise(out.cpu().numpy(), ho)
+    print("7B chain 4 layers T=8 normwise", err)
+    assert err <= 1e-3
+    assert normwise(qkv.cpu().numpy(), qo) <= 1e-3
