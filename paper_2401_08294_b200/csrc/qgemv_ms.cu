@@ -638,8 +638,8 @@ if_status qgemv_ms_launch(if_scheme s, const uint8_t* W, int64_t N, int64_t K, c
 // range works (the split needs |x'| <= 65504 only after scaling).
 //
 // Record layout: ms_rec.cuh (FR_REC bytes per (64-block, 8-token tile), kb-major).
-constexpr int MS_PART_TILES = 1024;  // split-K partial tiles (N/128 x S) of one launch
-constexpr int MS_BPMAX = 32;         // tokens (4 tiles of 8)
+constexpr int MS_PART_TILES = 2048;  // split-K partial tiles (N/128 x S) of one launch (70B gate/up: 448 x 3)
+constexpr int MS_BPMAX = 16;         // tokens (2 tiles of 8)
 extern unsigned long long* g_mk_dbg;  // qgemv.cu: instrumentation buffer (ifx_set_mk_debug)
 static int g_ms_seq = 0;              // launch number inside the instrumented call
 enum { MSK_QKV = 0, MSK_O = 1, MSK_GU = 2, MSK_DOWN = 3, MSK_PREP = 4 };
@@ -1076,7 +1076,7 @@ static if_status ms_chain_launch(MsChainP P, cudaStream_t st, int sms) {
 // bytes of the chain's record buffers (h, ctx, act) + sum-h^2 partials for NT = 2
 
 size_t ms_chain_ws_bytes(int64_t d, int64_t nq, int64_t lf) {
-  return (size_t)((d + nq + lf) / 64) * 4 * FR_REC + (size_t)(d / 128) * MS_BPMAX * 4 + 256 +
+  return (size_t)((d + nq + lf) / 64) * (MS_BPMAX / 8) * FR_REC + (size_t)(d / 128) * MS_BPMAX * 4 + 256 +
          (size_t)MS_PART_TILES * MS_BPMAX * 128 * 4 + (size_t)MS_PART_TILES * 4;
 }
 
@@ -1102,19 +1102,18 @@ if_status ms_chain_run(const MsChainLayer* layers, int nlayers, int64_t d, int64
   }
   uint8_t* base = static_cast<uint8_t*>(ws);
   uint8_t* rec_h = base;
-  uint8_t* rec_ctx = rec_h + (size_t)(d / 64) * 4 * FR_REC;
-  uint8_t* rec_act = rec_ctx + (size_t)(nq / 64) * 4 * FR_REC;
-  float* ssq = reinterpret_cast<float*>(rec_act + (size_t)(lf / 64) * 4 * FR_REC);
+  uint8_t* rec_ctx = rec_h + (size_t)(d / 64) * (MS_BPMAX / 8) * FR_REC;
+  uint8_t* rec_act = rec_ctx + (size_t)(nq / 64) * (MS_BPMAX / 8) * FR_REC;
+  float* ssq = reinterpret_cast<float*>(rec_act + (size_t)(lf / 64) * (MS_BPMAX / 8) * FR_REC);
   float* part = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(ssq) + (size_t)(d / 128) * MS_BPMAX * 4 + 256);
   uint32_t* cnt = reinterpret_cast<uint32_t*>(part + (size_t)MS_PART_TILES * MS_BPMAX * 128);
-  const int NT = T <= 8 ? 1 : T <= 16 ? 2 : 4;
+  const int NT = T <= 8 ? 1 : 2;
   {  // every phase must fit before anything is launched (the caller falls back)
     int sp, kp;
     const int64_t dims[4][2] = {{nqkv, d}, {d, nq}, {2 * lf, d}, {d, lf}};
     for (const auto& nk : dims)
-      if (!(NT == 1   ? ms_geo<1, 0>((int)nk[0], (int)nk[1], sms, &sp, &kp)
-            : NT == 2 ? ms_geo<2, 0>((int)nk[0], (int)nk[1], sms, &sp, &kp)
-                      : ms_geo<4, 0>((int)nk[0], (int)nk[1], sms, &sp, &kp)))
+      if (!(NT == 1 ? ms_geo<1, 0>((int)nk[0], (int)nk[1], sms, &sp, &kp)
+                    : ms_geo<2, 0>((int)nk[0], (int)nk[1], sms, &sp, &kp)))
         return IF_ERR_UNSUPPORTED;
   }
   auto run = [&]<int NTc, int V>() -> if_status {
@@ -1162,7 +1161,7 @@ if_status ms_chain_run(const MsChainLayer* layers, int nlayers, int64_t d, int64
     }
     return r;
   };
-  return NT == 1 ? run.template operator()<1, 0>() : NT == 2 ? run.template operator()<2, 0>() : run.template operator()<4, 0>();
+  return NT == 1 ? run.template operator()<1, 0>() : run.template operator()<2, 0>();
 }
 
 }  // namespace ifb
