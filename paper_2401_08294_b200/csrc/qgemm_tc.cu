@@ -26,6 +26,7 @@
 #include "common.cuh"
 #include "pipe.cuh"
 #include "qgemm.cuh"
+#include "simd.cuh"
 
 namespace ifb {
 
@@ -371,14 +372,22 @@ __device__ __forceinline__ void dequant_q3h64_half_f32(const unsigned char* raw,
     const float lo = half_bits_to_float(hdr & 0xFFFFu), hi = half_bits_to_float(hdr >> 16);
     const float step = __fdiv_rn(__fsub_rn(hi, lo), 10.0f);
     const float M23 = 8388608.0f, r11 = 0.0909090936183929443359375f;  // 2^23, roundup(1/11)
+    // two pairs per f32x2 instruction (each lane the same IEEE operation as the scalar
+    // form: identical bits, half the FMA-class issue slots)
+    const u64 nM2 = pack2(-M23, -M23), M2 = pack2(M23, M23), r2 = pack2(r11, r11), m2 = pack2(-11.0f, -11.0f);
+    const u64 st2 = pack2(step, step), lo2 = pack2(lo, lo);
 #pragma unroll
-    for (int jr = 0; jr < 16; jr++) {
-      const int p = 7 * jr;
-      const uint32_t t = (p & 31) ? __funnelshift_r(c[p >> 5], c[(p >> 5) + 1], p & 31) : c[p >> 5];
-      const float cf = __uint_as_float((t & 0x7Fu) | 0x4B000000u) - M23;      // c, exact
-      const float qe = __fmaf_rd(cf, r11, M23) - M23;                            // floor(c / 11)
-      const float qo = __fmaf_rn(qe, -11.0f, cf);                                // c mod 11
-      outw[jr] = pack16x2<!BF16>(__fmaf_rn(qe, step, lo), __fmaf_rn(qo, step, lo));
+    for (int jr = 0; jr < 16; jr += 2) {
+      const int p0 = 7 * jr, p1 = p0 + 7;
+      const uint32_t t0 = (p0 & 31) ? __funnelshift_r(c[p0 >> 5], c[(p0 >> 5) + 1], p0 & 31) : c[p0 >> 5];
+      const uint32_t t1 = (p1 & 31) ? __funnelshift_r(c[p1 >> 5], c[(p1 >> 5) + 1], p1 & 31) : c[p1 >> 5];
+      const u64 cf = fadd2(pack2(__uint_as_float((t0 & 0x7Fu) | 0x4B000000u), __uint_as_float((t1 & 0x7Fu) | 0x4B000000u)),
+                           nM2);                                   // c, exact
+      const u64 qe = fadd2(ffma2_rm(cf, r2, M2), nM2);             // floor(c / 11)
+      const u64 qo = ffma2(qe, m2, cf);                            // c mod 11
+      const float2 we = unpack2(ffma2(qe, st2, lo2)), wo = unpack2(ffma2(qo, st2, lo2));
+      outw[jr] = pack16x2<!BF16>(we.x, wo.x);
+      outw[jr + 1] = pack16x2<!BF16>(we.y, wo.y);
     }
   } else {
 #pragma unroll
