@@ -1,6 +1,6 @@
 """One small invocation of each hot kernel, for compute-sanitizer (memcheck / racecheck /
-synccheck): the persistent decode engine on a 2-layer SMALL stack (B = 1), the batched
-tensor-core qGEMV (B = 8), the prefill qGEMM (M = 70), the KV-cache attention stack,
+synccheck): the persistent decode engine on a 2-layer SMALL stack (B = 1), the fused
+batched chain (B = 8 and 16; with the KV cache at B = 2), the batched tensor-core qGEMV (B = 8), the prefill qGEMM (M = 70), the KV-cache attention stack,
 quantize / dequantize, the LM head and the speculative verification."""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -13,7 +13,7 @@ cfg = dict(layers=2, hidden=512, heads=8, kv_heads=2, head_dim=64, ffn=1408)
 shape = F.stack_shape(*[cfg[k] for k in ("layers", "hidden", "heads", "kv_heads", "head_dim", "ffn")], s)
 plan = F.if_plan_partition(F.IF_BY_LAYER, shape, 1)
 stk = Stack(cfg, s, plan, 0, dev)
-for T in (1, 8):
+for T in (1, 8, 16):
     h = torch.from_numpy(synth.activations(T, 512)).to(dev)
     out = torch.empty_like(h)
     ws = torch.zeros(F.if_stack_workspace_bytes(shape, plan, 0, T, F.IF_DECODE), dtype=torch.uint8, device=dev)
