@@ -459,8 +459,14 @@ def run_ours(args):
     #      device copy and a 512 B memset around it).  Algorithmic bytes per
     #      launch = the packed weights of the rank's layers (0.5 B/weight).
     launches_mk = launches_per_step
-    roof = {"kernel": "decode_mk (persistent whole-stack decode, 1 launch/step)" if launches_mk == 1 else
-            "qgemv (per-layer kernels)", "bound": "hbm", "achieved": stack_gbs_rank,
+    if launches_mk == 1:
+        kname = "decode_mk (persistent whole-stack decode, 1 launch/step)"
+    elif args.scheme == "Q3H_B64" and 2 <= B <= 16 and ws == 1:
+        kname = ("ms_chain_kernel (fused batched chain, 4 launches/layer + 1" +
+                 (" + 2 attention kernels/layer" if args.kv_pos else "") + "; step-level bytes / step time)")
+    else:
+        kname = "per-layer batched qGEMV + glue kernels (step-level bytes / step time)"
+    roof = {"kernel": kname, "bound": "hbm", "achieved": stack_gbs_rank,
             "peak": hbm_peak, "unit": "GB/s", "frac": stack_gbs_rank / hbm_peak,
             "peak_kind": f"{peak_kind} copy bandwidth (MEASURED_PEAKS.json hbm_gbs)",
             "traffic": None, "avg_launch_us": ms_per_step * 1e3 / max(1, launches_mk),
