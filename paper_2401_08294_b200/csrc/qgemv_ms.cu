@@ -660,7 +660,6 @@ struct MsChainP {
   uint32_t* cnt;   // per-tile arrival counters (zero-filled workspace, self-resetting)
   unsigned long long* dbg;  // instrumentation: %globaltimer stamps [16 launches][1024 CTAs][8] (nullable)
   int seq;
-  int ko;  // experiments (IFB_MS_KO): 1 = no decode / MMA, 2 = no weight waits, 3 = no weight loads
 };
 
 // fragments of nblk consecutive 64-blocks (first global block blk0) of vals [BP][ld]
@@ -924,7 +923,7 @@ __global__ void __launch_bounds__(MS_THREADS, MsGeo<NT, V>::MINB) ms_chain_kerne
     for (int t = 0; t < NT; t++) ya[t][0] = ya[t][1] = yb[t][0] = yb[t][1] = 0ull;
     const MsLane ML = ms_lane(lane, zero);
     auto refill = [&](int sl, int kb_next) {
-      if (kb_next < nkb && P.ko != 3)
+      if (kb_next < nkb)
         asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(ring_s + sl * 512),
                      "l"(wrow + (int64_t)(kb0 + kb_next) * 32), "r"(src_size)
                      : "memory");
@@ -932,13 +931,8 @@ __global__ void __launch_bounds__(MS_THREADS, MsGeo<NT, V>::MINB) ms_chain_kerne
     };
     int slot = 0;
     for (int kb = 0; kb < nkb; kb++) {
-      if (P.ko < 2) asm volatile("cp.async.wait_group %0;" ::"n"(DEPTH - 1) : "memory");  // block kb (this lane)
+      asm volatile("cp.async.wait_group %0;" ::"n"(DEPTH - 1) : "memory");  // block kb (this lane)
       __syncwarp();                                                                         // ... and every lane's
-      if (P.ko == 1) {
-        refill(slot, kb + DEPTH);
-        slot = slot + 1 == DEPTH ? 0 : slot + 1;
-        continue;
-      }
       MsBlk bk;
       ms_decode(ring + slot * 128, ML, bk);
       __syncwarp();  // the slot is read: refill it with block kb + DEPTH
@@ -1063,8 +1057,6 @@ static if_status ms_chain_launch(MsChainP P, cudaStream_t st, int sms) {
   }
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  static const char* ko = getenv("IFB_MS_KO");  // experiments only
-  P.ko = ko ? atoi(ko) : 0;
   P.dbg = g_mk_dbg;
   P.seq = g_mk_dbg ? g_ms_seq++ : 0;
   if (!g_mk_dbg) g_ms_seq = 0;
