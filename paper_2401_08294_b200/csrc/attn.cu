@@ -24,6 +24,8 @@
 // The cache is the caller's device memory, fp32 [layers][slots][max_ctx][lkv][hd]
 // (rank-local kv heads); K/V bytes join the decode roofline (2 * 4 * lkv * hd per position
 // per layer read).
+#include <stdlib.h>
+
 #include <cuda_bf16.h>
 
 #include "attn.cuh"
@@ -119,6 +121,24 @@ __global__ void __launch_bounds__(128) rope_append_kernel(float* __restrict__ qk
   }
 }
 
+// RoPE of one lane's EPL values (pairs (2m, 2m+1), m = lane EPL/2 + j) at position p:
+// the rope_append_kernel formula (angles in fp64)
+template <int EPL>
+__device__ __forceinline__ void rope_pairs(float (&v)[EPL], int p, int lane) {
+  constexpr int hd = 32 * EPL;
+#pragma unroll
+  for (int j = 0; j < EPL / 2; j++) {
+    const int m = lane * (EPL / 2) + j;
+    const double theta = exp(-2.0 * (double)m / (double)hd * 9.210340371976184);  // 10000^(-2m/hd), ln 10000
+    double sn, c;
+    sincos((double)p * theta, &sn, &c);
+    const float cf = (float)c, sf = (float)sn;
+    const float x = v[2 * j], y = v[2 * j + 1];
+    v[2 * j] = x * cf - y * sf;
+    v[2 * j + 1] = x * sf + y * cf;
+  }
+}
+
 // partial record per (token, local head, split): [m, l, acc[hd]] (hd + 2 floats)
 // grid (T * lkv, nsplit), 128 threads.  gcnt[t * lkv + jl] / tcnt[t]: zero between calls
 // (the last arriver resets its counter).
@@ -129,7 +149,8 @@ __global__ void __launch_bounds__(128) attn_kernel(const float* __restrict__ qkv
                                                    const float* __restrict__ vc, int slots, int max_ctx, int nsplit,
                                                    float* part, uint32_t* gcnt, uint32_t* tcnt, float* ctx,
                                                    __nv_bfloat16* __restrict__ ctx16, __half* __restrict__ x2, int bp,
-                                                   float* __restrict__ x2sc, uint8_t* __restrict__ rec, int rec_nt) {
+                                                   float* __restrict__ x2sc, uint8_t* __restrict__ rec, int rec_nt,
+                                                   int fused, float* __restrict__ rot_out, int32_t* __restrict__ status) {
   pdl_trigger();
   pdl_wait();
   constexpr int NW = ATT_NW, U = ATT_U, hd = 32 * EPL;
@@ -156,6 +177,10 @@ __global__ void __launch_bounds__(128) attn_kernel(const float* __restrict__ qkv
     for (int e = 0; e < EPL; e++) acc[h][e] = 0.f;
     if (h < per) {
       ld_vec<EPL>(qkv + (int64_t)t * nqkv + (jl * per + h) * hd + lane * EPL, q[h]);
+      if (fused && ok) {
+        rope_pairs<EPL>(q[h], p, lane);  // q after RoPE (the rope kernel's turn, in registers)
+        if (rot_out && sp == 0) st_vec<EPL>(rot_out + (int64_t)t * nqkv + (jl * per + h) * hd + lane * EPL, q[h]);
+      }
 #pragma unroll
       for (int e = 0; e < EPL; e++) q[h][e] *= scale;
     } else {
@@ -164,13 +189,37 @@ __global__ void __launch_bounds__(128) attn_kernel(const float* __restrict__ qkv
     }
   }
   const int64_t base = (int64_t)s * max_ctx * lkv * hd + (int64_t)jl * hd + lane * EPL;
+  // fused RoPE/append (T = 1): k_p, v_p of this group from the projections, k rotated;
+  // position p is read from registers (the append below is for later steps), and the
+  // split holding p appends them
+  float kp[EPL], vp[EPL];
+  if (fused && ok) {
+    ld_vec<EPL>(qkv + (int64_t)t * nqkv + (lh + jl) * hd + lane * EPL, kp);
+    ld_vec<EPL>(qkv + (int64_t)t * nqkv + (lh + lkv + jl) * hd + lane * EPL, vp);
+    rope_pairs<EPL>(kp, p, lane);
+    if (warp == 0 && p >= tau0 && p < tau1) {
+      st_vec<EPL>(const_cast<float*>(kc) + base + (int64_t)p * lkv * hd, kp);
+      st_vec<EPL>(const_cast<float*>(vc) + base + (int64_t)p * lkv * hd, vp);
+    }
+    if (rot_out && sp == 0 && warp == 0) {
+      st_vec<EPL>(rot_out + (int64_t)t * nqkv + (lh + jl) * hd + lane * EPL, kp);
+      st_vec<EPL>(rot_out + (int64_t)t * nqkv + (lh + lkv + jl) * hd + lane * EPL, vp);
+    }
+  } else if (fused && !ok && sp == 0 && jl == 0 && threadIdx.x == 0) {
+    report_status(status, IF_ERR_ARG);
+  }
   for (int tau = tau0 + warp * U; tau < tau1; tau += NW * U) {
     float kv[U][EPL], vv[U][EPL];
 #pragma unroll
     for (int u = 0; u < U; u++) {
       if (tau + u < tau1) {
-        ld_vec<EPL>(kc + base + (int64_t)(tau + u) * lkv * hd, kv[u]);
-        ld_vec<EPL>(vc + base + (int64_t)(tau + u) * lkv * hd, vv[u]);
+        if (fused && tau + u == p) {
+#pragma unroll
+          for (int e = 0; e < EPL; e++) kv[u][e] = kp[e], vv[u][e] = vp[e];
+        } else {
+          ld_vec<EPL>(kc + base + (int64_t)(tau + u) * lkv * hd, kv[u]);
+          ld_vec<EPL>(vc + base + (int64_t)(tau + u) * lkv * hd, vv[u]);
+        }
       }
     }
 #pragma unroll
@@ -362,14 +411,23 @@ size_t attn_cnt_words(int lkv) { return (size_t)ATT_MAXT * lkv + ATT_MAXT; }
 
 template <int EPL>
 static void attn_launch(const AttnArgs& a, float* kc, float* vc, int ns, cudaStream_t st) {
-  const int npad = a.x2 ? a.bp - (int)a.T : 0;
-  const dim3 ga((unsigned)(a.T + npad), (unsigned)((a.lh + 2 * a.lkv + 3) / 4));
-  launch_attn(rope_append_kernel<EPL>, ga, 128, 0, st, a.pdl, a.qkv, (int)a.T, a.lh, a.lkv, a.slot_ids, a.positions,
-              kc, vc, a.slots, a.max_ctx, a.status, a.x2, a.bp, a.x2sc);
+  // one token, no fp16 split / records: RoPE and the append fused into the attention
+  // kernel (one launch instead of two per layer)
+  static const int no_fuse = getenv("IFB_NO_ROPE_FUSE") != nullptr;  // A/B experiments only
+  const int fused = a.T == 1 && !a.x2 && !a.rec && !no_fuse;
+  if (!fused) {
+    const int npad = a.x2 ? a.bp - (int)a.T : 0;
+    const dim3 ga((unsigned)(a.T + npad), (unsigned)((a.lh + 2 * a.lkv + 3) / 4));
+    launch_attn(rope_append_kernel<EPL>, ga, 128, 0, st, a.pdl, a.qkv, (int)a.T, a.lh, a.lkv, a.slot_ids, a.positions,
+                kc, vc, a.slots, a.max_ctx, a.status, a.x2, a.bp, a.x2sc);
+  }
   const dim3 gb((unsigned)(a.T * a.lkv), (unsigned)ns);
   launch_attn(attn_kernel<EPL>, gb, 128, 0, st, a.pdl, (const float*)a.qkv, (int)a.T, a.lh, a.lkv, a.slot_ids,
               a.positions, (const float*)kc, (const float*)vc, a.slots, a.max_ctx, ns, a.part, a.cnt,
-              a.cnt ? a.cnt + (size_t)ATT_MAXT * a.lkv : nullptr, a.ctx, a.ctx16, a.x2, a.bp, a.x2sc, a.rec, a.rec_nt);
+              a.cnt ? a.cnt + (size_t)ATT_MAXT * a.lkv : nullptr, a.ctx, a.ctx16, a.x2, a.bp, a.x2sc, a.rec, a.rec_nt,
+              fused, fused ? a.rot_out : nullptr, a.status);
+  if (!fused && a.rot_out)  // the rope kernel rotated q, k in place
+    cudaMemcpyAsync(a.rot_out, a.qkv, (size_t)a.T * (a.lh + 2 * a.lkv) * a.hd * 4, cudaMemcpyDeviceToDevice, st);
 }
 
 if_status attn_run(const AttnArgs& a, cudaStream_t st) {

@@ -31,6 +31,7 @@ struct AttnArgs {
   float* x2sc;              // per-token 2^-k of the split
   uint8_t* rec;             // nullable: fragment records of ctx for the fused batched chain (ms_rec.cuh)
   int rec_nt;               // token tiles of 8 per record block (1 or 2)
+  float* rot_out;           // nullable [T, (lh + 2 lkv) hd]: q, k after RoPE and v (the stack's last_qkv)
   bool pdl;
 };
 

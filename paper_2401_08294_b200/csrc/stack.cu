@@ -464,10 +464,8 @@ static if_status run_stack(const if_stack_shape* shape, const if_plan* plan, int
         one.positions = kvr->positions + t;
         AttnArgs aa = attn_args(L, &one, w, 1, nlayers, k);
         aa.ctx = w.ctx;
+        aa.rot_out = (k == nlayers - 1 && last_qkv) ? last_qkv + t * L.nqkv : nullptr;  // q, k after RoPE
         st = attn_run(aa, cs);
-        if (!st && k == nlayers - 1 && last_qkv &&
-            cudaMemcpyAsync(last_qkv + t * L.nqkv, w.qkv, (size_t)L.nqkv * 4, cudaMemcpyDeviceToDevice, cs) != cudaSuccess)
-          st = check_launch("if_run_stack: last_qkv");
       }
     }
     if (st != IF_ERR_UNSUPPORTED) {
@@ -508,11 +506,8 @@ static if_status run_stack(const if_stack_shape* shape, const if_plan* plan, int
         aa.rec = rec;
         aa.rec_nt = nt;
         aa.pdl = true;
-        if_status r = attn_run(aa, k.cs);
-        if (!r && l == k.nlayers - 1 && k.last_qkv &&
-            cudaMemcpyAsync(k.last_qkv, k.w->qkv, (size_t)k.T * k.L->nqkv * 4, cudaMemcpyDeviceToDevice, k.cs) != cudaSuccess)
-          r = check_launch("if_run_stack: last_qkv");
-        return r;
+        aa.rot_out = (l == k.nlayers - 1) ? k.last_qkv : nullptr;  // q, k after RoPE
+        return attn_run(aa, k.cs);
       };
     st = ms_chain_run(ml.data(), nlayers, L.d, L.lh, L.lkv, L.hd, L.lf, per, T, h_out, last_qkv, w.msrec, cs, fn, &kc, w.qkv);
     if (st != IF_ERR_UNSUPPORTED) {
@@ -548,6 +543,7 @@ static if_status run_stack(const if_stack_shape* shape, const if_plan* plan, int
         // GQA attention over the KV cache (attn.cu, NEXT-1): RoPE + append, split
         // partials, combine -> ctx (and its fp16 split for the batched qGEMV)
         AttnArgs aa = attn_args(L, kvr, w, T, nlayers, l);
+        aa.rot_out = (l == nlayers - 1) ? last_qkv : nullptr;  // q, k after RoPE
         aa.ctx = w.ctx;
         aa.x2 = x2h;
         aa.bp = bpx;
@@ -604,6 +600,7 @@ static if_status run_stack(const if_stack_shape* shape, const if_plan* plan, int
         return st;
       if (kvr) {  // causal attention of the chunk over the cache (all tokens append first)
         AttnArgs aa = attn_args(L, kvr, w, T, nlayers, l);
+        aa.rot_out = (l == nlayers - 1) ? last_qkv : nullptr;  // q, k after RoPE
         aa.ctx16 = c16;
         if ((st = attn_run(aa, cs))) return st;
       } else {
@@ -634,7 +631,7 @@ static if_status run_stack(const if_stack_shape* shape, const if_plan* plan, int
         if ((st = comm_allreduce_into(comm, w.part, h_out, nh, 1, cs))) return st;
       }
     }
-    if (l == nlayers - 1 && last_qkv) {
+    if (l == nlayers - 1 && last_qkv && !kvr) {  // (with a cache, the attention returns q, k after RoPE)
       if (cudaMemcpyAsync(last_qkv, w.qkv, (size_t)T * L.nqkv * 4, cudaMemcpyDeviceToDevice, cs) != cudaSuccess)
         return check_launch("if_run_stack: last_qkv");
     }
