@@ -681,16 +681,15 @@ __device__ __forceinline__ void ms_emit_blocks(const float* vals, int ld, int co
   }
 }
 
-// V = 0: ring 8 (NT = 1) / 4 blocks deep per warp, two CTAs per SM (112 KB each);
-// V = 1: ring 4 deep, three CTAs per SM (74 KB each) -- more warps to hide latency
-template <int NT, int V = 0>
+// per-warp weight ring 8 (NT = 1) / 4 blocks deep, two CTAs per SM (112 KB each)
+template <int NT>
 struct MsGeo {
   static constexpr int BP = 8 * NT;
-  static constexpr int DEPTH = (NT == 1 && V == 0) ? 8 : 4;
+  static constexpr int DEPTH = NT == 1 ? 8 : 4;
   static constexpr int RING = MS_WARPS * DEPTH * 512;
   static constexpr int REC = NT * FR_REC;  // per block
-  static constexpr int MINB = V == 1 ? 3 : 2;
-  static constexpr int SMEM_HI = V == 1 ? 74 * 1024 : 112 * 1024;
+  static constexpr int MINB = 2;
+  static constexpr int SMEM_HI = 112 * 1024;
 };
 
 // rms inverse per token into sinv[BP] (threads tok < BP), fixed-order sum of partials
@@ -858,10 +857,10 @@ __device__ __forceinline__ unsigned long long ms_gtimer() {
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
 }
-template <int NT, int KIND, int V>
-__global__ void __launch_bounds__(MS_THREADS, MsGeo<NT, V>::MINB) ms_chain_kernel(const __grid_constant__ MsChainP P,
+template <int NT, int KIND>
+__global__ void __launch_bounds__(MS_THREADS, MsGeo<NT>::MINB) ms_chain_kernel(const __grid_constant__ MsChainP P,
                                                                                    uint32_t zero) {
-  using Gm = MsGeo<NT, V>;
+  using Gm = MsGeo<NT>;
   unsigned long long* dbg = P.dbg && P.seq < 16 && threadIdx.x == 0
                                 ? P.dbg + ((size_t)P.seq * 1024 + (blockIdx.y * gridDim.x + blockIdx.x) % 1024) * 8
                                 : nullptr;
@@ -991,16 +990,16 @@ __global__ void __launch_bounds__(MS_THREADS, MsGeo<NT, V>::MINB) ms_chain_kerne
   }
 }
 
-// split-K geometry of one phase: splits (cluster size) and blocks per CTA; false when
-// the K-range of the fewest CTAs the cluster allows does not fit shared memory
-template <int NT, int V>
+// split-K geometry of one phase: splits and blocks per CTA; false when the K-range of the
+// fewest split CTAs allowed (MS_MAXS) does not fit shared memory
+template <int NT>
 static bool ms_geo(int N, int K, int sms, int* splits_out, int* kper_out) {
-  using Gm = MsGeo<NT, V>;
+  using Gm = MsGeo<NT>;
   const int nb = K / 64, nrt = N / MS_ROWS;
   // MINB CTAs per SM while the records fit SMEM_HI, else one (up to 220 KB)
   const int kmax2 = (Gm::SMEM_HI - Gm::RING - 1024) / Gm::REC, kmax1 = (220 * 1024 - Gm::RING - 1024) / Gm::REC;
   // cost model (per-warp latency-bound CTAs): waves x (blocks per CTA + fixed cost
-  // of ~6 blocks for prologue / epilogue + 1 per cluster rank in the reduction)
+  // of ~6 blocks for prologue / epilogue + 1 per split in the reduction)
   int best = -1, best_cost = 0;
   for (int sp = 1; sp <= std::min(MS_MAXS, nb); sp++) {
     const int kper = (nb + sp - 1) / sp;
@@ -1017,10 +1016,10 @@ static bool ms_geo(int N, int K, int sms, int* splits_out, int* kper_out) {
   return true;
 }
 
-template <int NT, int KIND, int V>
+template <int NT, int KIND>
 static if_status ms_chain_launch(MsChainP P, cudaStream_t st, int sms) {
-  using Gm = MsGeo<NT, V>;
-  auto kern = ms_chain_kernel<NT, KIND, V>;
+  using Gm = MsGeo<NT>;
+  auto kern = ms_chain_kernel<NT, KIND>;
   static bool configured = false;
   if (!configured) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
@@ -1038,7 +1037,7 @@ static if_status ms_chain_launch(MsChainP P, cudaStream_t st, int sms) {
     cfg.dynamicSmemBytes = 25 * 1024;
   } else {
     int kper = 0;
-    if (!ms_geo<NT, V>(P.N, P.K, sms, &splits, &kper)) return IF_ERR_UNSUPPORTED;
+    if (!ms_geo<NT>(P.N, P.K, sms, &splits, &kper)) return IF_ERR_UNSUPPORTED;
     static const char* so = getenv("IFB_MS_SPLITS");  // experiments: "qkv,o,gu,down"
     if (so) {
       int v[4] = {0, 0, 0, 0};
@@ -1104,18 +1103,18 @@ if_status ms_chain_run(const MsChainLayer* layers, int nlayers, int64_t d, int64
     int sp, kp;
     const int64_t dims[4][2] = {{nqkv, d}, {d, nq}, {2 * lf, d}, {d, lf}};
     for (const auto& nk : dims)
-      if (!(NT == 1 ? ms_geo<1, 0>((int)nk[0], (int)nk[1], sms, &sp, &kp)
-                    : ms_geo<2, 0>((int)nk[0], (int)nk[1], sms, &sp, &kp)))
+      if (!(NT == 1 ? ms_geo<1>((int)nk[0], (int)nk[1], sms, &sp, &kp)
+                    : ms_geo<2>((int)nk[0], (int)nk[1], sms, &sp, &kp)))
         return IF_ERR_UNSUPPORTED;
   }
-  auto run = [&]<int NTc, int V>() -> if_status {
+  auto run = [&]<int NTc>() -> if_status {
     MsChainP P = {};
     P.B = (int)T;
     P.d = (int)d;
     P.h = h;
     P.ssq_out = ssq;
     P.fout = rec_h;
-    if_status r = ms_chain_launch<NTc, MSK_PREP, V>(P, st, sms);
+    if_status r = ms_chain_launch<NTc, MSK_PREP>(P, st, sms);
     for (int l = 0; l < nlayers && !r; l++) {
       const bool lastl = l == nlayers - 1;
       MsChainP q = {};
@@ -1128,7 +1127,7 @@ if_status ms_chain_run(const MsChainLayer* layers, int nlayers, int64_t d, int64
       q.qkv_out = attn ? qkv_buf : (lastl ? last_qkv : nullptr);
       q.kv = attn ? 1 : 0;
       q.v_off = (int)((lh + lkv) * hd), q.hd = (int)hd, q.per = per, q.lh = (int)lh;
-      if ((r = ms_chain_launch<NTc, MSK_QKV, V>(q, st, sms))) break;
+      if ((r = ms_chain_launch<NTc, MSK_QKV>(q, st, sms))) break;
       // KV decode (NEXT-1): RoPE + append + attention over the cache, whose merge writes
       // the ctx records (attn.cu)
       if (attn && (r = attn(actx, l, rec_ctx, NTc))) break;
@@ -1137,23 +1136,23 @@ if_status ms_chain_run(const MsChainLayer* layers, int nlayers, int64_t d, int64
       o.part = part, o.cnt = cnt;
       o.B = (int)T, o.d = (int)d, o.W = layers[l].wo, o.N = (int)d, o.K = (int)nq, o.fin = rec_ctx, o.h = h;
       o.ssq_out = ssq, o.fout = rec_h;
-      if ((r = ms_chain_launch<NTc, MSK_O, V>(o, st, sms))) break;
+      if ((r = ms_chain_launch<NTc, MSK_O>(o, st, sms))) break;
       // gate/up: act records
       MsChainP g = {};
       g.part = part, g.cnt = cnt;
       g.B = (int)T, g.d = (int)d, g.nt_ssq = (int)(d / 128), g.W = layers[l].wgu, g.N = (int)(2 * lf), g.K = (int)d;
       g.fin = rec_h, g.ssq_in = ssq, g.fout = rec_act;
-      if ((r = ms_chain_launch<NTc, MSK_GU, V>(g, st, sms))) break;
+      if ((r = ms_chain_launch<NTc, MSK_GU>(g, st, sms))) break;
       // down: h += W_down act; next layer's h records
       MsChainP dn = {};
       dn.part = part, dn.cnt = cnt;
       dn.B = (int)T, dn.d = (int)d, dn.W = layers[l].wdown, dn.N = (int)d, dn.K = (int)lf, dn.fin = rec_act, dn.h = h;
       dn.ssq_out = ssq, dn.fout = lastl ? nullptr : rec_h;
-      if ((r = ms_chain_launch<NTc, MSK_DOWN, V>(dn, st, sms))) break;
+      if ((r = ms_chain_launch<NTc, MSK_DOWN>(dn, st, sms))) break;
     }
     return r;
   };
-  return NT == 1 ? run.template operator()<1, 0>() : run.template operator()<2, 0>();
+  return NT == 1 ? run.template operator()<1>() : run.template operator()<2>();
 }
 
 }  // namespace ifb
