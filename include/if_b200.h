@@ -242,14 +242,17 @@ if_status if_comm_recv_prev(if_comm c, float* buf, int64_t n, if_stream_t stream
  * h_in  device fp32 [T, d] (ignored on stages > 0, which receive from stage-1),
  * h_out device fp32 [T, d] (valid on the last stage), last_qkv device fp32
  * [T, (lh + 2 lkv) head_dim] of the stage's last layer (nullable).
- * mode IF_DECODE (1 <= T <= 64, fp32 activations: T <= 2 (3.5-bit) or T <= 6 (k-bit
+ * mode IF_DECODE (1 <= T <= 64, fp32 activations: T = 1 (3.5-bit) or T <= 6 (k-bit
  * schemes) runs the persistent engine -- one launch per token for the whole stage, with the TP
- * merges inside it when comm is a peer-memory communicator; otherwise per-layer
- * qGEMVs (3.5-bit 3 <= T <= 32: the warp-MMA kernel, else as in if_qgemv) or IF_PREFILL (T <= 4096,
+ * merges inside it when comm is a peer-memory communicator; 3.5-bit 2 <= T <= 16 on one
+ * tensor-parallel rank runs the fused batched chain (qgemv_ms.cu: 4 launches per layer, the
+ * glue in the GEMV epilogues, results bit-identical run to run); otherwise per-layer
+ * qGEMVs (3.5-bit T <= 32: the warp-MMA kernel, else as in if_qgemv) or IF_PREFILL (T <= 4096,
  * qGEMM on tcgen05 with bf16 activations).
  * workspace: device, if_stack_workspace_bytes(); ZERO-FILL IT ONCE before the
  * first call (cudaMemset) and keep it with this (shape, plan, rank): it carries
- * the decode engine's step epoch across calls.  comm may be NULL when
+ * the decode engine's step epoch and the chain's self-resetting split-K counters across
+ * calls.  comm may be NULL when
  * plan->devices == 1.  Never synchronises; graph capturable.
  * ------------------------------------------------------------------------- */
 enum { IF_DECODE = 0, IF_PREFILL = 1 };
