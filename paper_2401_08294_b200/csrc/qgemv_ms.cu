@@ -857,7 +857,10 @@ __device__ __forceinline__ unsigned long long ms_gtimer() {
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
 }
-template <int NT, int KIND>
+// RG = row groups per warp: 1 (128-row tiles) or 2 (256-row tiles, both halves sharing the
+// CTA's input records and its split-K reduction: half the CTAs for the same rows, used where
+// it turns two waves into one -- the 7B gate/up phase)
+template <int NT, int KIND, int RG = 1>
 __global__ void __launch_bounds__(MS_THREADS, MsGeo<NT>::MINB) ms_chain_kernel(const __grid_constant__ MsChainP P,
                                                                                    uint32_t zero) {
   using Gm = MsGeo<NT>;
@@ -865,13 +868,14 @@ __global__ void __launch_bounds__(MS_THREADS, MsGeo<NT>::MINB) ms_chain_kernel(c
                                 ? P.dbg + ((size_t)P.seq * 1024 + (blockIdx.y * gridDim.x + blockIdx.x) % 1024) * 8
                                 : nullptr;
   if (dbg) dbg[0] = ms_gtimer();
-  constexpr int BP = Gm::BP, DEPTH = Gm::DEPTH;
+  constexpr int BP = Gm::BP, DEPTH = RG == 1 ? Gm::DEPTH : 6, RING = MS_WARPS * DEPTH * 512 * RG;
+  constexpr int TILE = 128 * RG;  // rows per CTA
   extern __shared__ __align__(16) unsigned char smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  float* vals = reinterpret_cast<float*>(smem);  // epilogue: [BP][128] (reuses the ring)
-  float* acts = vals + BP * 128;                 // gu: [BP][64]
+  float* vals = reinterpret_cast<float*>(smem);  // epilogue: [RG][BP][128] (reuses the ring)
+  float* acts = vals + RG * BP * 128;            // gu: [RG][BP][64]
   // tail (never aliased by the ring, the records or vals/acts): mbarrier, sinv [BP], red [128]
-  unsigned char* tail = KIND == MSK_PREP ? smem + 24 * 1024 : smem + Gm::RING + (size_t)P.kper * Gm::REC;
+  unsigned char* tail = KIND == MSK_PREP ? smem + 24 * 1024 : smem + RING + (size_t)P.kper * Gm::REC;
   uint64_t* xbar = reinterpret_cast<uint64_t*>(tail);
   float* sinv = reinterpret_cast<float*>(tail + 64);
   float* red = reinterpret_cast<float*>(tail + 256);
@@ -884,27 +888,35 @@ __global__ void __launch_bounds__(MS_THREADS, MsGeo<NT>::MINB) ms_chain_kernel(c
   } else {
     const int nb = P.K >> 6;
     const int kb0 = blockIdx.y * P.kper, kb1 = min(nb, kb0 + P.kper), nkb = kb1 - kb0;
-    uint32_t* ring = reinterpret_cast<uint32_t*>(smem) + warp * DEPTH * 128;
-    unsigned char* xr = smem + Gm::RING;  // this CTA's input records
-    const int rbase = blockIdx.x * MS_ROWS + warp * 16;
+    uint32_t* ring = reinterpret_cast<uint32_t*>(smem) + warp * DEPTH * 128 * RG;  // [DEPTH][RG][16 rows][8 words]
+    unsigned char* xr = smem + RING;  // this CTA's input records
     const int64_t row_bytes = (int64_t)nb * 32;
-    const int lrow = rbase + (lane >> 1);
-    const uint8_t* wrow = P.W + (int64_t)min(lrow, P.N - 1) * row_bytes + (lane & 1) * 16;
-    const uint32_t src_size = lrow < P.N ? 16u : 0u;
+    const uint8_t* wrow[RG];
+    uint32_t src_size[RG];
+#pragma unroll
+    for (int h = 0; h < RG; h++) {
+      const int lrow = blockIdx.x * TILE + h * 128 + warp * 16 + (lane >> 1);
+      wrow[h] = P.W + (int64_t)min(lrow, P.N - 1) * row_bytes + (lane & 1) * 16;
+      src_size[h] = lrow < P.N ? 16u : 0u;
+    }
     const uint32_t ring_s = (uint32_t)__cvta_generic_to_shared(ring) + lane * 16;
     if (threadIdx.x == 0) {
       mbar_init(xbar, 1);
       fence_mbar_init();
     }
     pdl_trigger();
+    auto refill = [&](int sl, int kb_next) {
+      if (kb_next < nkb) {
 #pragma unroll
-    for (int i = 0; i < DEPTH; i++) {
-      if (i < nkb)
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(ring_s + i * 512),
-                     "l"(wrow + (int64_t)(kb0 + i) * 32), "r"(src_size)
-                     : "memory");
+        for (int h = 0; h < RG; h++)
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(ring_s + (sl * RG + h) * 512),
+                       "l"(wrow[h] + (int64_t)(kb0 + kb_next) * 32), "r"(src_size[h])
+                       : "memory");
+      }
       asm volatile("cp.async.commit_group;" ::: "memory");
-    }
+    };
+#pragma unroll
+    for (int i = 0; i < DEPTH; i++) refill(i, i);
     __syncthreads();  // mbarrier initialised
     pdl_wait();       // the previous phase's records are complete
     if (dbg) dbg[1] = ms_gtimer();
@@ -917,47 +929,48 @@ __global__ void __launch_bounds__(MS_THREADS, MsGeo<NT>::MINB) ms_chain_kernel(c
     mbar_wait(xbar, 0);
     if (dbg) dbg[2] = ms_gtimer();
     const int g = lane >> 2, c = lane & 3;
-    u64 ya[NT][2], yb[NT][2];
+    u64 ya[RG][NT][2], yb[RG][NT][2];
 #pragma unroll
-    for (int t = 0; t < NT; t++) ya[t][0] = ya[t][1] = yb[t][0] = yb[t][1] = 0ull;
+    for (int h = 0; h < RG; h++)
+#pragma unroll
+      for (int t = 0; t < NT; t++) ya[h][t][0] = ya[h][t][1] = yb[h][t][0] = yb[h][t][1] = 0ull;
     const MsLane ML = ms_lane(lane, zero);
-    auto refill = [&](int sl, int kb_next) {
-      if (kb_next < nkb)
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(ring_s + sl * 512),
-                     "l"(wrow + (int64_t)(kb0 + kb_next) * 32), "r"(src_size)
-                     : "memory");
-      asm volatile("cp.async.commit_group;" ::: "memory");
-    };
     int slot = 0;
     for (int kb = 0; kb < nkb; kb++) {
       asm volatile("cp.async.wait_group %0;" ::"n"(DEPTH - 1) : "memory");  // block kb (this lane)
-      __syncwarp();                                                                         // ... and every lane's
-      MsBlk bk;
-      ms_decode(ring + slot * 128, ML, bk);
+      __syncwarp();                                                         // ... and every lane's
+      MsBlk bk[RG];
+#pragma unroll
+      for (int h = 0; h < RG; h++) ms_decode(ring + (slot * RG + h) * 128, ML, bk[h]);
       __syncwarp();  // the slot is read: refill it with block kb + DEPTH
       refill(slot, kb + DEPTH);
       slot = slot + 1 == DEPTH ? 0 : slot + 1;
 #pragma unroll
-      for (int t = 0; t < NT; t++) ms_mma(xr + (size_t)(kb * NT + t) * FR_REC, lane, ML.c, bk, ya[t], yb[t]);
+      for (int h = 0; h < RG; h++)
+#pragma unroll
+        for (int t = 0; t < NT; t++) ms_mma(xr + (size_t)(kb * NT + t) * FR_REC, lane, ML.c, bk[h], ya[h][t], yb[h][t]);
     }
     asm volatile("cp.async.wait_group 0;" ::: "memory");
     if (dbg) dbg[3] = ms_gtimer();
-    __syncthreads();  // the ring is free: partial tile [BP][128]
+    __syncthreads();  // the ring is free: partial tile [RG][BP][128]
 #pragma unroll
-    for (int t = 0; t < NT; t++)
+    for (int h = 0; h < RG; h++)
 #pragma unroll
-      for (int e = 0; e < 4; e++) {
-        const int tok = 8 * t + 2 * c + (e & 1), r = warp * 16 + g + (e >> 1) * 8;
-        vals[tok * 128 + r] = fmaf(0.1f, ms2_el(ya[t], e), ms2_el(yb[t], e));
-      }
+      for (int t = 0; t < NT; t++)
+#pragma unroll
+        for (int e = 0; e < 4; e++) {
+          const int tok = 8 * t + 2 * c + (e & 1), r = warp * 16 + g + (e >> 1) * 8;
+          vals[(h * BP + tok) * 128 + r] = fmaf(0.1f, ms2_el(ya[h][t], e), ms2_el(yb[h][t], e));
+        }
+    constexpr int TV = RG * BP * 128;  // values of a partial tile
     const int S = gridDim.y;
     if (S > 1) {
       // split-K: every CTA stores its partial tile; the LAST to arrive (per-tile counter,
       // self-resetting) sums the S partials in split order (deterministic) and owns the
       // epilogue -- the others exit at once (no cluster barrier to wait on)
       __syncthreads();
-      float* mine = P.part + ((size_t)blockIdx.x * S + blockIdx.y) * (BP * 128);
-      for (int i = threadIdx.x; i < BP * 128; i += MS_THREADS) __stcg(mine + i, vals[i]);
+      float* mine = P.part + ((size_t)blockIdx.x * S + blockIdx.y) * TV;
+      for (int i = threadIdx.x; i < TV; i += MS_THREADS) __stcg(mine + i, vals[i]);
       __syncthreads();  // the CTA's stores happen-before thread 0's release (bar.sync cumulativity)
       if (threadIdx.x == 0) {
         uint32_t old;
@@ -968,11 +981,11 @@ __global__ void __launch_bounds__(MS_THREADS, MsGeo<NT>::MINB) ms_chain_kernel(c
       }
       __syncthreads();  // ... and thread 0's acquire happens-before every thread's loads below
       if (red[0] == 0.f) return;
-      const float* all = P.part + (size_t)blockIdx.x * S * (BP * 128);
-      for (int i = threadIdx.x; i < BP * 128; i += MS_THREADS) {
+      const float* all = P.part + (size_t)blockIdx.x * S * TV;
+      for (int i = threadIdx.x; i < TV; i += MS_THREADS) {
         float pv[MS_MAXS];
 #pragma unroll
-        for (int q = 0; q < MS_MAXS; q++) pv[q] = q < S ? __ldcg(all + (size_t)q * (BP * 128) + i) : 0.f;
+        for (int q = 0; q < MS_MAXS; q++) pv[q] = q < S ? __ldcg(all + (size_t)q * TV + i) : 0.f;
         float v = pv[0];
 #pragma unroll
         for (int q = 1; q < MS_MAXS; q++) v += pv[q];
@@ -984,8 +997,12 @@ __global__ void __launch_bounds__(MS_THREADS, MsGeo<NT>::MINB) ms_chain_kernel(c
       __syncthreads();
       if (dbg) dbg[4] = ms_gtimer();
     }
-    // ---- the owner's epilogue: stack glue + the next phase's records ----
-    ms_owner_epilogue<NT, KIND>(P, blockIdx.x, vals, acts, red, sinv);
+    // ---- the owner's epilogue (per 128-row half): stack glue + the next phase's records ----
+#pragma unroll
+    for (int h = 0; h < RG; h++) {
+      if (h) __syncthreads();  // red / sinv reuse
+      ms_owner_epilogue<NT, KIND>(P, blockIdx.x * RG + h, vals + h * BP * 128, acts + h * BP * 64, red, sinv);
+    }
     if (dbg) dbg[5] = ms_gtimer();
   }
 }
@@ -1032,6 +1049,46 @@ static if_status ms_chain_launch(MsChainP P, cudaStream_t st, int sms) {
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   int splits = 1;
+  if constexpr (KIND == MSK_GU && NT == 1) {
+    // 256-row tiles (RG = 2) when they fit one wave of 2 CTAs per SM better than the
+    // 128-row tiles do (cost: waves x (rows-groups x blocks per CTA + fixed ~6 + splits))
+    static const int rg_off = getenv("IFB_NO_MS_RG2") != nullptr;  // A/B experiments only
+    const int nb = P.K / 64;
+    int s1 = 0, k1 = 0;
+    if (!rg_off && P.N % 256 == 0 && ms_geo<NT>(P.N, P.K, sms, &s1, &k1)) {
+      const int nrt1 = P.N / 128, nrt2 = P.N / 256;
+      const int cost1 = ((nrt1 * s1 + 2 * sms - 1) / (2 * sms)) * (k1 + 6 + s1);
+      constexpr int RING2 = MS_WARPS * 6 * 512 * 2;
+      int best = -1, bcost = 0;
+      for (int sp = 1; sp <= std::min(MS_MAXS, nb); sp++) {
+        const int kper = (nb + sp - 1) / sp;
+        if ((size_t)RING2 + (size_t)kper * Gm::REC + 1024 > 112 * 1024) continue;
+        const int cost = ((nrt2 * sp + 2 * sms - 1) / (2 * sms)) * (2 * kper + 6 + sp);
+        if (best < 0 || cost < bcost) best = sp, bcost = cost;
+      }
+      if (best > 0 && bcost < cost1) {
+        const int kper = (nb + best - 1) / best;
+        splits = (nb + kper - 1) / kper;
+        P.kper = kper;
+        auto k2 = ms_chain_kernel<NT, KIND, 2>;
+        static bool cfg2 = false;
+        if (!cfg2) {
+          cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize, 112 * 1024);
+          cfg2 = true;
+        }
+        cfg.gridDim = dim3((unsigned)nrt2, (unsigned)splits);
+        cfg.dynamicSmemBytes = (size_t)RING2 + (size_t)kper * Gm::REC + 1024;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        P.dbg = g_mk_dbg;
+        P.seq = g_mk_dbg ? g_ms_seq++ : 0;
+        if (!g_mk_dbg) g_ms_seq = 0;
+        cudaLaunchKernelEx(&cfg, k2, P, 0u);
+        count_launch();
+        return check_launch("ms_chain (256-row tiles)");
+      }
+    }
+  }
   if constexpr (KIND == MSK_PREP) {
     cfg.gridDim = dim3((unsigned)(P.d / 128));
     cfg.dynamicSmemBytes = 25 * 1024;
