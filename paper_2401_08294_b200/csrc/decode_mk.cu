@@ -1555,7 +1555,8 @@ if_status mk_launch(MkParams& P, cudaStream_t st) {
   // measured (7B B = 1, 200 steps): all CTAs 897 tok/s, all but 4 905, 8 908, 16 911, 24 911,
   // 48 832 (the late words' re-reads congest L2)
   static const char* early_env = getenv("IFB_MK_EARLY");  // A/B experiments only
-  P.early = std::max(0, std::min(early_env ? atoi(early_env) : 16, (int)G / 8));
+  // (k-bit schemes: Q4_B32 +0.7%, Q8_B64 -3% at 16 -- the early start is the 3.5-bit engine's)
+  P.early = std::max(0, std::min(early_env ? atoi(early_env) : (q3h ? 16 : 0), (int)G / 8));
   if (P.part && !no_pdl) {
     attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[na].val.programmaticStreamSerializationAllowed = 1;
